@@ -1,0 +1,358 @@
+/*
+ * lg.h — C-ABI drop-in boundary of the B200-native Lightning Grasp forward pass.
+ *
+ * Everything the reference keeps on the caller side (URDF/mesh loaders, surface
+ * sampling, patch decomposition, config parsing, the JSONL result format) is
+ * exposed here as host functions so that a C++ caller can keep its own types
+ * and hand flat, caller-owned SoA arrays across.  Everything on the hot path
+ * (reference proj/src/pipeline.cpp:308-625 and the L2-L5 modules it calls)
+ * runs on the GPU behind lg_field_build / lg_query_domains_batch /
+ * lg_run_batch and the stage-level batch entry points.
+ *
+ * Conventions:
+ *   - every entry point returns an int status: LG_OK or a negative code that
+ *     names the reference exception class it replaces; the message is kept in
+ *     a thread-local buffer readable with lg_last_error();
+ *   - handles are library-owned and freed with the matching *_destroy;
+ *   - input arrays are caller-owned and copied in; output arrays are either
+ *     library-owned (valid until the owning handle is destroyed) or caller
+ *     buffers with an explicit capacity;
+ *   - one in-flight call per lg_ctx; there is no CPU fallback: on a machine
+ *     without a CUDA device every device entry point returns LG_ERR_CUDA.
+ *
+ * Arrays of 3-vectors are row-major [n][3]; rotations are row-major 3x3;
+ * object samples are [n][6] = (position xyz, unit outward normal xyz).
+ */
+#ifndef LG_H_
+#define LG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference exception classes) ---------- */
+#define LG_OK 0
+#define LG_ERR_INVALID_ARGUMENT (-1) /* std::invalid_argument */
+#define LG_ERR_RUNTIME (-2)          /* std::runtime_error (I/O, config)   */
+#define LG_ERR_OUT_OF_RANGE (-3)     /* std::out_of_range (reverse_lookup) */
+#define LG_ERR_CUDA (-4)             /* no device / CUDA runtime failure   */
+#define LG_ERR_NOMEM (-5)
+
+#define LG_MAX_K 5          /* k_contacts range [2,5] (config.cpp:107-112) */
+#define LG_MAX_CONTACTS 6   /* k slots + at most one static contact       */
+#define LG_MAX_DOF 32
+#define LG_MAX_GROUPS 32    /* reachability mask is one uint32 per sample */
+#define LG_MAX_LINKS 64
+
+/* Copies the calling thread's last error message; returns its length. */
+int lg_last_error(char* buf, size_t cap);
+/* Library build string (arch, compile flags). */
+const char* lg_version(void);
+
+/* ---- flat model descriptions (pointer views, no ownership) -------------- */
+
+/* HandModel (reference hand.hpp:19-46).  Links are in file order; joint
+ * types: 0 fixed, 1 revolute, 2 prismatic. Parts are grouped by link in link
+ * order (part_link is non-decreasing). */
+typedef struct lg_hand_desc {
+  int n_links;
+  int dof; /* actuated_count */
+  int root;
+  const int* parent;      /* [n_links], -1 for root */
+  const int* joint_type;  /* [n_links] */
+  const int* joint_index; /* [n_links], -1 when not actuated */
+  const int* topo_order;  /* [n_links], parents before children */
+  const double* origin_R; /* [n_links][9] parent -> pre-motion frame */
+  const double* origin_t; /* [n_links][3] */
+  const double* axis;     /* [n_links][3] unit, link frame */
+  const double* limit_lo; /* [n_links] */
+  const double* limit_hi; /* [n_links] */
+  int n_parts;
+  const int* part_link;      /* [n_parts] */
+  const int* part_vert_off;  /* [n_parts+1] */
+  const double* part_verts;  /* [*][3] link-local hull vertices */
+  const int* part_tri_off;   /* [n_parts+1] */
+  const int* part_tris;      /* [*][3] indices local to the part */
+  const int* part_plane_off; /* [n_parts+1] */
+  const double* part_planes; /* [*][4] (unit outward normal, offset) */
+  const double* part_bounds; /* [n_parts][6] (min xyz, max xyz) */
+} lg_hand_desc;
+
+/* ContactPatch list (reference contact_field.hpp:20-30); ids are dense. */
+typedef struct lg_patches_desc {
+  int n_patches;
+  const int* link;        /* [P] */
+  const int* point_off;   /* [P+1] into points/normals */
+  const double* points;   /* [*][3] link-local member samples */
+  const double* normals;  /* [*][3] */
+  const int* fp_off;      /* [P+1] into field_points */
+  const int* field_points;/* [*] member index within the patch, sorted */
+} lg_patches_desc;
+
+/* Exported contact-field index (ContactFieldIndex, contact_field.hpp:112-137)
+ * as CSR.  Box order inside a patch is lexicographic by cell (std::map order
+ * of contact_field.cpp:226-227) so a box id is its rank inside its patch. */
+typedef struct lg_field_csr {
+  double box_width;
+  int codebook_size;
+  const double* codebook;   /* [C][3] */
+  int n_patches;
+  const int* patch_link;    /* [P] */
+  const int* patch_box_off; /* [P+1] */
+  long long n_boxes;
+  const long long* box_cell;/* [B][3] */
+  const long long* box_code_off; /* [B+1] */
+  long long n_codes;
+  const uint16_t* codes;    /* [n_codes] ascending within a box */
+  const int* rep_link;      /* [n_codes] IndexRep.link */
+  const double* rep_point;  /* [n_codes][3] IndexRep.point (link-local) */
+  const double* rep_normal; /* [n_codes][3] */
+  long long n_vectors;      /* swept contact vectors inserted */
+} lg_field_csr;
+
+/* RunConfig (reference config.hpp:15-77), numeric part plus asset paths. */
+typedef struct lg_run_params {
+  char hand[512];
+  char object[512];
+  char out[512];
+  uint64_t seed;
+  int batch, workers, passes, cache, export_obj, k_contacts;
+  double samples_per_cm2, object_scale, probe_half_width, probe_depth_threshold;
+  double hand_scale;
+  int field_configs;
+  double box_width, patch_radius;
+  int field_points_per_patch, codebook_size;
+  double theta_hit;
+  int placement_mode; /* 0 exhaustive, 1 canonical */
+  double static_contact_prob;
+  double canonical_center[3], canonical_half_extents[3];
+  double penetration_margin;
+  double lambda_torque, mu, eps_stable;
+  int pgd_iterations, pgd_warm_iterations;
+  double pgd_step;
+  int n_outer, n_inner, restarts;
+  double sigma;
+  double beta;
+  int ik_iterations;
+  double step_clamp, residual_tol, damping_scale;
+  int finetune_rounds, finetune_iterations, lookup_attempts, unused_attempts;
+  double contact_tol;
+  /* B200 extensions: seed sharding (rank r of R owns c in [rB/R,(r+1)B/R)) */
+  int shard_rank, shard_count;
+  int want_trace; /* fill one lg_trace per (pass, candidate) */
+} lg_run_params;
+
+/* Fills the reference defaults (config.hpp:15-77). */
+void lg_run_params_default(lg_run_params* p);
+/* parse_config (config.cpp:339-401): defaults, then file (may be NULL), then
+ * the non-NULL overrides; throws-equivalent LG_ERR_RUNTIME on bad input. */
+int lg_config_parse(const char* path, const char* hand, const char* object,
+                    const char* out, const long long* seed, const int* batch,
+                    const int* workers, lg_run_params* p);
+/* index_cache_key (config.cpp:403-417). */
+int lg_index_cache_key(const lg_run_params* p, uint64_t* key);
+
+/* ---- results ----------------------------------------------------------- */
+
+/* Grasp (pipeline.hpp:19-38) plus its candidate id g = pass*batch + c. */
+typedef struct lg_grasp {
+  long long g;
+  double pose_R[9];
+  double pose_t[3];
+  int dof;
+  double q[LG_MAX_DOF];
+  int n_contacts;
+  double contact_p[LG_MAX_CONTACTS][3];
+  double contact_n[LG_MAX_CONTACTS][3];
+  int contact_link[LG_MAX_CONTACTS];
+  double objective;
+  int penetration_free, stable, ik_converged;
+} lg_grasp;
+
+/* StageProfile (pipeline.hpp:44-60). Stage seconds are device time. */
+typedef struct lg_profile {
+  double placement_domains, contact_optimization, kinematics_optimization,
+      postprocessing, total, field_build;
+  long long candidates, placements_accepted, contact_sets_balanced, ik_finite,
+      penetration_free, ik_converged, stable, valid;
+  double grasps_per_second;
+  long long patches, boxes, field_vectors, object_samples, field_samples;
+  long long gpu_launches;
+} lg_profile;
+
+/* Per-candidate record of every stage decision, used by the stage parity
+ * harness (the oracle fills the same struct). */
+typedef struct lg_trace {
+  long long g;
+  int pass, c;
+  /* stage 1: place_object + query_domains + group pick (pipeline.cpp:396-438) */
+  int accepted;
+  double penetration;
+  double pose_R[9], pose_t[3];
+  int n_static, static_link;
+  double static_p[3], static_n[3];
+  int n_groups;
+  int domain_size[LG_MAX_GROUPS];
+  int picked;
+  int chosen[LG_MAX_K];
+  /* stage 2: optimize_contacts + balance gate (pipeline.cpp:444-458) */
+  int opt_element[LG_MAX_K];
+  int opt_sample[LG_MAX_K];
+  double opt_objective;
+  int opt_anchor, opt_evaluations;
+  double opt_alpha[LG_MAX_CONTACTS], opt_bx[LG_MAX_CONTACTS],
+      opt_by[LG_MAX_CONTACTS];
+  int balanced;
+  /* stage 3: lookup attempts (pipeline.cpp:465-523) */
+  int realized, attempts_run, best_attempt, best_clear;
+  double max_residual;
+  double real_q[LG_MAX_DOF];
+  unsigned long long used_joints;
+  int target_link[LG_MAX_K];
+  double target_point[LG_MAX_K][3], target_normal[LG_MAX_K][3];
+  /* stage 4: postprocess (pipeline.cpp:528-604) */
+  int unused_attempt, penetration_free, ik_converged, stable, valid, dropped;
+  double final_q[LG_MAX_DOF];
+  double objective;
+} lg_trace;
+
+typedef struct lg_result lg_result;
+int lg_result_profile(const lg_result* r, lg_profile* out);
+long long lg_result_num_grasps(const lg_result* r);
+const lg_grasp* lg_result_grasps(const lg_result* r);
+long long lg_result_num_traces(const lg_result* r);
+const lg_trace* lg_result_traces(const lg_result* r);
+void lg_result_destroy(lg_result* r);
+
+/* ---- host side: loaders and caller-side steps (stay on the host) -------- */
+
+typedef struct lg_hand lg_hand;
+typedef struct lg_mesh lg_mesh;
+typedef struct lg_patches lg_patches;
+
+typedef struct lg_load_report {
+  long long triangles_read, triangles_kept, degenerate_dropped;
+} lg_load_report;
+
+/* load_hand (hand.cpp:265-414). */
+int lg_hand_load(const char* urdf_path, double scale, lg_hand** out);
+int lg_hand_export(const lg_hand* h, lg_hand_desc* out);
+int lg_hand_link_name(const lg_hand* h, int link, char* buf, size_t cap);
+/* dependency_groups (hand.cpp:515-552): group id per link (-1 static). */
+int lg_hand_groups(const lg_hand* h, int* group_of_link, int* n_groups);
+/* Visual mesh of one link (link-local). */
+int lg_hand_link_visual(const lg_hand* h, int link, lg_mesh** out);
+void lg_hand_destroy(lg_hand* h);
+
+/* load_mesh (mesh.cpp:161-167) and the primitive generators. */
+int lg_mesh_load(const char* path, lg_load_report* report, lg_mesh** out);
+int lg_mesh_box(double sx, double sy, double sz, lg_mesh** out);
+int lg_mesh_icosphere(double radius, int subdivisions, lg_mesh** out);
+int lg_mesh_cylinder(double radius, double length, int segments, lg_mesh** out);
+int lg_mesh_from_arrays(const double* verts, int n_verts, const int* tris,
+                        int n_tris, lg_mesh** out);
+int lg_mesh_scale(lg_mesh* m, double scale);
+int lg_mesh_info(const lg_mesh* m, int* n_verts, int* n_tris, double* area);
+int lg_mesh_arrays(const lg_mesh* m, const double** verts, const int** tris);
+int lg_mesh_save_obj(const lg_mesh* m, const char* path);
+void lg_mesh_destroy(lg_mesh* m);
+
+/* sample_surface (mesh.cpp:297-339). Two-call size query: pass out=NULL to
+ * get the count in *n. */
+int lg_sample_surface(const lg_mesh* m, double samples_per_cm2, uint64_t seed,
+                      double* out, size_t cap, size_t* n);
+uint64_t lg_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
+
+/* build_field's host steps (pipeline.cpp:277-285): per-link surface sampling
+ * with stream 'hnds' and decompose_patches (contact_field.cpp:26-99). */
+int lg_hand_patches(const lg_hand* h, double samples_per_cm2,
+                    double patch_radius, uint64_t seed, int field_cap,
+                    lg_patches** out);
+int lg_patches_export(const lg_patches* p, lg_patches_desc* out);
+void lg_patches_destroy(lg_patches* p);
+
+/* write_dataset JSONL (dataset.cpp:23-56) and profile JSON (113-131). */
+int lg_write_dataset(const char* path, const lg_grasp* grasps, long long n);
+int lg_write_profile(const char* path, const lg_profile* p);
+
+/* ---- device side (sm_100a) ---------------------------------------------- */
+
+typedef struct lg_ctx lg_ctx;
+typedef struct lg_field lg_field;
+
+int lg_device_count(int* n);
+int lg_ctx_create(int device, lg_ctx** out);
+void lg_ctx_destroy(lg_ctx* ctx);
+
+/* ContactFieldIndex::build (contact_field.cpp:306-334) on the GPU. */
+int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand,
+                   const lg_patches_desc* patches, int N, double box_width,
+                   uint64_t seed, int codebook_size, lg_field** out);
+/* Copies the index to host CSR (pointers valid until lg_field_destroy). */
+int lg_field_export(lg_field* f, lg_field_csr* out);
+void lg_field_destroy(lg_field* f);
+
+/* query_domains (contact_field.cpp:380-448) for m poses at once: writes the
+ * reachability mask masks[m][n] (bit g set iff sample i is an element of group
+ * g's domain) and, when scores != NULL, the element score per (pose, sample)
+ * (max over all groups' hits, 0 when none). poses are [m][12] = (R row-major,
+ * t). group_of_patch maps patch id -> dependency group (-1 static). */
+int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
+                           const double* samples, int n, const double* poses,
+                           int m, double theta_hit, uint32_t* masks,
+                           double* scores);
+
+/* preprocess_object (pipeline.cpp:71-98): keep[i] = 1 when sample i survives. */
+int lg_preprocess(lg_ctx* ctx, const double* samples, int n,
+                  double probe_half_width, double depth_threshold,
+                  uint8_t* keep);
+
+/* Batched wrench solves (wrench.cpp:323-411): problem i has n[i] <= 6
+ * contacts given as points/inward normals [i][6][3]; tangent frames come from
+ * tangent_basis.  mode 0 = solve_fswo, 1 = solve_gswo. Outputs objective,
+ * anchor, alpha/beta_x/beta_y [i][6]. */
+int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points,
+                          const double* normals, double lambda_torque, double mu,
+                          int mode, int iterations, int warm_iterations,
+                          double step, int max_backtracks, double* objective,
+                          int* anchor, double* alpha, double* beta_x,
+                          double* beta_y);
+
+/* Batched validate_grasp_collisions (collision.cpp:230-288): clean[i] for
+ * configuration q[i] (dof) and object pose[i] (12) against the samples. */
+int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m,
+                       const double* q, const double* poses,
+                       const double* samples, int n, double margin,
+                       uint8_t* clean, double* max_penetration);
+
+/* Batched realize_grasp (pipeline.cpp:185-253): problem i has k[i] targets
+ * (object point, inward normal, link, hand local point, hand local normal).
+ * Writes q[i][dof], max residual, finite flag and used-joint bitmask. */
+int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                     const double* object_points, const double* object_normals,
+                     const int* links, const double* hand_points,
+                     const double* hand_normals, double beta, int iterations,
+                     double step_clamp, double residual_tol,
+                     double damping_scale, int finetune_rounds,
+                     int finetune_iterations, double* q, double* max_residual,
+                     int* finite, unsigned long long* used_joints);
+
+/* run_batch (pipeline.cpp:308-625): the whole forward pass on the device,
+ * field build included.  raw_samples = sample_surface of the object. */
+int lg_run_batch(lg_ctx* ctx, const lg_hand_desc* hand,
+                 const lg_patches_desc* patches, const double* raw_samples,
+                 int n_raw, const lg_run_params* params, lg_result** out);
+/* Same, reusing a field built with lg_field_build (the cached-field mode). */
+int lg_run_batch_field(lg_ctx* ctx, const lg_hand_desc* hand,
+                       const lg_patches_desc* patches, lg_field* field,
+                       const double* raw_samples, int n_raw,
+                       const lg_run_params* params, lg_result** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LG_H_ */

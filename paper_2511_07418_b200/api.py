@@ -1,0 +1,485 @@
+"""Python mirror of the reference's C++ API over the lg.h C-ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/graspgen/*.hpp): load_hand, load_mesh,
+sample_surface, decompose_patches (via hand_patches), parse_config,
+ContactFieldIndex.build, query_domains, preprocess_object, run_batch,
+write_dataset.  Exceptions map the C status codes back to the reference's
+exception classes: invalid_argument -> ValueError, runtime_error ->
+RuntimeError, out_of_range -> IndexError.
+
+Every compute entry point runs on the GPU through libgraspgen_b200.so; there
+is no CPU fallback, and a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import lgabi as A
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgraspgen_b200.so")
+_LIB = None
+
+
+class CudaError(RuntimeError):
+    """No CUDA device or a CUDA runtime failure (LG_ERR_CUDA)."""
+
+
+def lib():
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    P = C.POINTER
+    sig = {
+        "lg_last_error": (C.c_int, [C.c_char_p, C.c_size_t]),
+        "lg_version": (C.c_char_p, []),
+        "lg_run_params_default": (None, [P(A.RunParams)]),
+        "lg_config_parse": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                      P(C.c_longlong), P(C.c_int), P(C.c_int), P(A.RunParams)]),
+        "lg_index_cache_key": (C.c_int, [P(A.RunParams), P(C.c_uint64)]),
+        "lg_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
+        "lg_hand_load": (C.c_int, [C.c_char_p, C.c_double, P(vp)]),
+        "lg_hand_export": (C.c_int, [vp, P(A.HandDesc)]),
+        "lg_hand_link_name": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t]),
+        "lg_hand_groups": (C.c_int, [vp, A.ip, A.ip]),
+        "lg_hand_link_visual": (C.c_int, [vp, C.c_int, P(vp)]),
+        "lg_hand_destroy": (None, [vp]),
+        "lg_mesh_load": (C.c_int, [C.c_char_p, P(A.LoadReport), P(vp)]),
+        "lg_mesh_box": (C.c_int, [C.c_double, C.c_double, C.c_double, P(vp)]),
+        "lg_mesh_icosphere": (C.c_int, [C.c_double, C.c_int, P(vp)]),
+        "lg_mesh_cylinder": (C.c_int, [C.c_double, C.c_double, C.c_int, P(vp)]),
+        "lg_mesh_from_arrays": (C.c_int, [A.dp, C.c_int, A.ip, C.c_int, P(vp)]),
+        "lg_mesh_scale": (C.c_int, [vp, C.c_double]),
+        "lg_mesh_info": (C.c_int, [vp, A.ip, A.ip, A.dp]),
+        "lg_mesh_arrays": (C.c_int, [vp, P(A.dp), P(A.ip)]),
+        "lg_mesh_save_obj": (C.c_int, [vp, C.c_char_p]),
+        "lg_mesh_destroy": (None, [vp]),
+        "lg_sample_surface": (C.c_int, [vp, C.c_double, C.c_uint64, A.dp, C.c_size_t,
+                                        P(C.c_size_t)]),
+        "lg_hand_patches": (C.c_int, [vp, C.c_double, C.c_double, C.c_uint64, C.c_int, P(vp)]),
+        "lg_patches_export": (C.c_int, [vp, P(A.PatchesDesc)]),
+        "lg_patches_destroy": (None, [vp]),
+        "lg_write_dataset": (C.c_int, [C.c_char_p, P(A.Grasp), C.c_longlong]),
+        "lg_write_profile": (C.c_int, [C.c_char_p, P(A.Profile)]),
+        "lg_device_count": (C.c_int, [A.ip]),
+        "lg_ctx_create": (C.c_int, [C.c_int, P(vp)]),
+        "lg_ctx_destroy": (None, [vp]),
+        "lg_field_build": (C.c_int, [vp, P(A.HandDesc), P(A.PatchesDesc), C.c_int, C.c_double,
+                                     C.c_uint64, C.c_int, P(vp)]),
+        "lg_field_export": (C.c_int, [vp, P(A.FieldCsr)]),
+        "lg_field_destroy": (None, [vp]),
+        "lg_query_domains_batch": (C.c_int, [vp, vp, A.ip, A.dp, C.c_int, A.dp, C.c_int,
+                                             C.c_double, P(C.c_uint32), A.dp]),
+        "lg_preprocess": (C.c_int, [vp, A.dp, C.c_int, C.c_double, C.c_double,
+                                    P(C.c_uint8)]),
+        "lg_run_batch": (C.c_int, [vp, P(A.HandDesc), P(A.PatchesDesc), A.dp, C.c_int,
+                                   P(A.RunParams), P(vp)]),
+        "lg_run_batch_field": (C.c_int, [vp, P(A.HandDesc), P(A.PatchesDesc), vp, A.dp,
+                                         C.c_int, P(A.RunParams), P(vp)]),
+        "lg_result_profile": (C.c_int, [vp, P(A.Profile)]),
+        "lg_result_num_grasps": (C.c_longlong, [vp]),
+        "lg_result_grasps": (P(A.Grasp), [vp]),
+        "lg_result_num_traces": (C.c_longlong, [vp]),
+        "lg_result_traces": (P(A.Trace), [vp]),
+        "lg_result_destroy": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+def _err():
+    buf = C.create_string_buffer(1024)
+    lib().lg_last_error(buf, 1024)
+    return buf.value.decode(errors="replace")
+
+
+def check(rc):
+    if rc == A.LG_OK:
+        return
+    msg = _err()
+    if rc == A.LG_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == A.LG_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)
+    if rc == A.LG_ERR_CUDA:
+        raise CudaError(msg)
+    if rc == A.LG_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(A.dp)
+
+
+def _ip(a):
+    return a.ctypes.data_as(A.ip)
+
+
+def mix_seed(seed, a, b=0):
+    """mix_seed (rng.hpp:25-28)."""
+    return int(lib().lg_mix_seed(C.c_uint64(seed), C.c_uint64(a), C.c_uint64(b)))
+
+
+# ------------------------------------------------------------------ meshes
+class Mesh:
+    """TriMesh (mesh.hpp:13-21), owned by the library."""
+
+    def __init__(self, handle, report=None):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        self.report = report
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.lg_mesh_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def _make(fn, *args):
+        h = C.c_void_p()
+        check(fn(*args, C.byref(h)))
+        return Mesh(h)
+
+    @classmethod
+    def box(cls, size):
+        return cls._make(lib().lg_mesh_box, *map(float, size))
+
+    @classmethod
+    def icosphere(cls, radius, subdivisions):
+        return cls._make(lib().lg_mesh_icosphere, float(radius), int(subdivisions))
+
+    @classmethod
+    def cylinder(cls, radius, length, segments=24):
+        return cls._make(lib().lg_mesh_cylinder, float(radius), float(length), int(segments))
+
+    @classmethod
+    def from_arrays(cls, verts, tris):
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(tris, dtype=np.int32).reshape(-1, 3)
+        return cls._make(lib().lg_mesh_from_arrays, _dp(v), len(v), _ip(t), len(t))
+
+    def info(self):
+        nv, nt, area = C.c_int(), C.c_int(), C.c_double()
+        check(lib().lg_mesh_info(self._h, C.byref(nv), C.byref(nt), C.byref(area)))
+        return nv.value, nt.value, area.value
+
+    def arrays(self):
+        nv, nt, _ = self.info()
+        v, t = A.dp(), A.ip()
+        check(lib().lg_mesh_arrays(self._h, C.byref(v), C.byref(t)))
+        verts = np.ctypeslib.as_array(v, shape=(nv * 3,)).reshape(nv, 3).copy() if nv else np.zeros((0, 3))
+        tris = np.ctypeslib.as_array(t, shape=(nt * 3,)).reshape(nt, 3).copy() if nt else np.zeros((0, 3), np.int32)
+        return verts, tris
+
+    def scale(self, s):
+        check(lib().lg_mesh_scale(self._h, float(s)))
+        return self
+
+    def save_obj(self, path):
+        check(lib().lg_mesh_save_obj(self._h, path.encode()))
+
+
+def load_mesh(path):
+    """load_mesh (mesh.cpp:161-167); returns (Mesh, LoadReport dict)."""
+    rep = A.LoadReport()
+    h = C.c_void_p()
+    check(lib().lg_mesh_load(str(path).encode(), C.byref(rep), C.byref(h)))
+    m = Mesh(h)
+    m.report = dict(triangles_read=rep.triangles_read, triangles_kept=rep.triangles_kept,
+                    degenerate_dropped=rep.degenerate_dropped)
+    return m
+
+
+def sample_surface(mesh, samples_per_cm2, seed):
+    """sample_surface (mesh.cpp:297-339) -> float64 array (n, 6) = (p, n)."""
+    L = lib()
+    n = C.c_size_t()
+    check(L.lg_sample_surface(mesh._h, float(samples_per_cm2), C.c_uint64(seed), None, 0,
+                              C.byref(n)))
+    out = np.zeros((n.value, 6), dtype=np.float64)
+    check(L.lg_sample_surface(mesh._h, float(samples_per_cm2), C.c_uint64(seed), _dp(out),
+                              n.value, C.byref(n)))
+    return out
+
+
+# -------------------------------------------------------------------- hand
+class HandModel:
+    """HandModel (hand.hpp:37-46) with its flat lg_hand_desc view."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.desc = A.HandDesc()
+        check(lib().lg_hand_export(self._h, C.byref(self.desc)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.lg_hand_destroy(self._h)
+            self._h = None
+
+    @property
+    def n_links(self):
+        return self.desc.n_links
+
+    @property
+    def dof(self):
+        return self.desc.dof
+
+    def link_name(self, l):
+        buf = C.create_string_buffer(256)
+        check(lib().lg_hand_link_name(self._h, int(l), buf, 256))
+        return buf.value.decode()
+
+    def groups(self):
+        """dependency_groups (hand.cpp:515-552): (group id per link, n_groups)."""
+        g = np.zeros(self.n_links, dtype=np.int32)
+        n = C.c_int()
+        check(lib().lg_hand_groups(self._h, _ip(g), C.byref(n)))
+        return g, n.value
+
+    def link_visual(self, l):
+        h = C.c_void_p()
+        check(lib().lg_hand_link_visual(self._h, int(l), C.byref(h)))
+        return Mesh(h)
+
+    def limits(self):
+        d = self.desc
+        lo = np.zeros(d.dof)
+        hi = np.zeros(d.dof)
+        for l in range(d.n_links):
+            j = d.joint_index[l]
+            if j >= 0:
+                lo[j], hi[j] = d.limit_lo[l], d.limit_hi[l]
+        return lo, hi
+
+    def mid_config(self):
+        lo, hi = self.limits()
+        return 0.5 * (lo + hi)
+
+
+def load_hand(path, scale=1.0):
+    """load_hand (hand.cpp:265-414)."""
+    h = C.c_void_p()
+    check(lib().lg_hand_load(str(path).encode(), float(scale), C.byref(h)))
+    return HandModel(h)
+
+
+class Patches:
+    """decompose_patches output (contact_field.hpp:20-36) as lg_patches_desc."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.desc = A.PatchesDesc()
+        check(lib().lg_patches_export(self._h, C.byref(self.desc)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.lg_patches_destroy(self._h)
+            self._h = None
+
+    @property
+    def n_patches(self):
+        return self.desc.n_patches
+
+    def link_of_patch(self):
+        return np.ctypeslib.as_array(self.desc.link, shape=(self.n_patches,)).copy()
+
+
+def hand_patches(hand, samples_per_cm2, patch_radius, seed, field_cap=8):
+    """build_field's host steps (pipeline.cpp:277-285): per-link samples with
+    stream 'hnds' then decompose_patches (contact_field.cpp:26-99)."""
+    h = C.c_void_p()
+    check(lib().lg_hand_patches(hand._h, float(samples_per_cm2), float(patch_radius),
+                                C.c_uint64(seed), int(field_cap), C.byref(h)))
+    return Patches(h)
+
+
+# ------------------------------------------------------------------ config
+def default_config():
+    p = A.RunParams()
+    lib().lg_run_params_default(C.byref(p))
+    return p
+
+
+def parse_config(path=None, hand=None, object=None, out=None, seed=None, batch=None,
+                 workers=None):
+    """parse_config (config.cpp:339-401) with CLI-style overrides."""
+    p = A.RunParams()
+    enc = lambda s: None if s is None else str(s).encode()
+    sd = None if seed is None else C.byref(C.c_longlong(int(seed)))
+    bt = None if batch is None else C.byref(C.c_int(int(batch)))
+    wk = None if workers is None else C.byref(C.c_int(int(workers)))
+    check(lib().lg_config_parse(enc(path), enc(hand), enc(object), enc(out), sd, bt, wk,
+                                C.byref(p)))
+    return p
+
+
+def index_cache_key(params):
+    k = C.c_uint64()
+    check(lib().lg_index_cache_key(C.byref(params), C.byref(k)))
+    return k.value
+
+
+# ------------------------------------------------------------------ device
+class Context:
+    """One CUDA device + stream (one in-flight call per context)."""
+
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        check(lib().lg_ctx_create(int(device), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.lg_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def device_count():
+    n = C.c_int()
+    check(lib().lg_device_count(C.byref(n)))
+    return n.value
+
+
+class ContactFieldIndex:
+    """ContactFieldIndex (contact_field.hpp:112-137), resident on the GPU."""
+
+    def __init__(self, handle, ctx):
+        self._h = handle
+        self._ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.lg_field_destroy(self._h)
+            self._h = None
+
+    @classmethod
+    def build(cls, ctx, hand, patches, N, box_width, seed, codebook_size=256):
+        """ContactFieldIndex::build (contact_field.cpp:306-334) on the device."""
+        h = C.c_void_p()
+        check(lib().lg_field_build(ctx._h, C.byref(hand.desc), C.byref(patches.desc), int(N),
+                                   float(box_width), C.c_uint64(seed), int(codebook_size),
+                                   C.byref(h)))
+        return cls(h, ctx)
+
+    def export(self):
+        """Host CSR copy: patches -> boxes (lexicographic cells) -> codes/reps."""
+        o = A.FieldCsr()
+        check(lib().lg_field_export(self._h, C.byref(o)))
+        P, B, Q = o.n_patches, o.n_boxes, o.n_codes
+        arr = np.ctypeslib.as_array
+        return dict(
+            box_width=o.box_width,
+            codebook=arr(o.codebook, shape=(o.codebook_size * 3,)).reshape(-1, 3).copy(),
+            patch_link=arr(o.patch_link, shape=(P,)).copy(),
+            patch_box_off=arr(o.patch_box_off, shape=(P + 1,)).copy(),
+            box_cell=arr(o.box_cell, shape=(B * 3,)).reshape(-1, 3).copy(),
+            box_code_off=arr(o.box_code_off, shape=(B + 1,)).copy(),
+            codes=arr(o.codes, shape=(Q,)).copy(),
+            rep_link=arr(o.rep_link, shape=(Q,)).copy(),
+            rep_point=arr(o.rep_point, shape=(Q * 3,)).reshape(-1, 3).copy(),
+            rep_normal=arr(o.rep_normal, shape=(Q * 3,)).reshape(-1, 3).copy(),
+            n_vectors=o.n_vectors,
+        )
+
+
+def query_domains_batch(ctx, field, group_of_patch, samples, poses, theta_hit):
+    """query_domains (contact_field.cpp:380-448) for m poses: reachability
+    masks (m, n) uint32, bit g = sample is an element of group g's domain."""
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    p = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 12)
+    g = np.ascontiguousarray(group_of_patch, dtype=np.int32)
+    masks = np.zeros((len(p), len(s)), dtype=np.uint32)
+    check(lib().lg_query_domains_batch(ctx._h, field._h, _ip(g), _dp(s), len(s), _dp(p), len(p),
+                                       float(theta_hit),
+                                       masks.ctypes.data_as(C.POINTER(C.c_uint32)), None))
+    return masks
+
+
+def preprocess_object(ctx, samples, probe_half_width, depth_threshold):
+    """preprocess_object (pipeline.cpp:71-98) -> keep mask (bool, order kept)."""
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    keep = np.zeros(len(s), dtype=np.uint8)
+    check(lib().lg_preprocess(ctx._h, _dp(s), len(s), float(probe_half_width),
+                              float(depth_threshold), keep.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return keep.astype(bool)
+
+
+class RunResult:
+    """RunResult (pipeline.hpp:143-148): grasps, StageProfile, traces."""
+
+    def __init__(self, handle):
+        L = lib()
+        self.profile_struct = A.Profile()
+        check(L.lg_result_profile(handle, C.byref(self.profile_struct)))
+        self.profile = {n: getattr(self.profile_struct, n) for n, _ in A.Profile._fields_}
+        ng = L.lg_result_num_grasps(handle)
+        nt = L.lg_result_num_traces(handle)
+        self.grasps = _copy_structs(L.lg_result_grasps(handle), ng, A.grasp_dtype())
+        self.traces = _copy_structs(L.lg_result_traces(handle), nt, A.trace_dtype())
+        L.lg_result_destroy(handle)
+
+
+def _copy_structs(ptr, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    buf = (C.c_char * (n * dtype.itemsize)).from_address(C.cast(ptr, C.c_void_p).value)
+    return np.frombuffer(bytes(buf), dtype=dtype).copy()
+
+
+def run_batch(ctx, hand, patches, raw_samples, params, field=None):
+    """run_batch (pipeline.cpp:308-625) on the GPU: field build (unless a
+    prebuilt field is given), preprocess, placement, domains, contact search,
+    realisation and postprocess."""
+    raw = np.ascontiguousarray(raw_samples, dtype=np.float64).reshape(-1, 6)
+    h = C.c_void_p()
+    if field is None:
+        check(lib().lg_run_batch(ctx._h, C.byref(hand.desc), C.byref(patches.desc), _dp(raw),
+                                 len(raw), C.byref(params), C.byref(h)))
+    else:
+        check(lib().lg_run_batch_field(ctx._h, C.byref(hand.desc), C.byref(patches.desc),
+                                       field._h, _dp(raw), len(raw), C.byref(params),
+                                       C.byref(h)))
+    return RunResult(h)
+
+
+def write_dataset(path, grasps):
+    """write_dataset (dataset.cpp:50-56): JSONL in the reference format."""
+    g = np.ascontiguousarray(grasps)
+    check(lib().lg_write_dataset(str(path).encode(), g.ctypes.data_as(C.POINTER(A.Grasp)),
+                                 len(g)))
+
+
+def write_profile(path, profile_struct):
+    check(lib().lg_write_profile(str(path).encode(), C.byref(profile_struct)))
+
+
+TAG_OBJECT_SAMPLES = 0x6F626A73  # pipeline.cpp:19
+
+
+def prepare_inputs(params):
+    """Caller-side steps of run_batch/build_field (pipeline.cpp:273-330):
+    load the hand and its patches, load + scale the object, sample it."""
+    hand = load_hand(params.hand.decode(), params.hand_scale)
+    patches = hand_patches(hand, params.samples_per_cm2, params.patch_radius, params.seed,
+                           params.field_points_per_patch)
+    mesh = load_mesh(params.object.decode())
+    if params.object_scale != 1.0:
+        mesh.scale(params.object_scale)
+    raw = sample_surface(mesh, params.samples_per_cm2, mix_seed(params.seed, TAG_OBJECT_SAMPLES))
+    return hand, patches, raw, mesh

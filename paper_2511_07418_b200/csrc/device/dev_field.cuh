@@ -1,0 +1,280 @@
+// dev_field.cuh — contact-field construction and query on the GPU.
+//
+// Build (reference ContactFieldIndex::build, contact_field.cpp:306-334 with
+// insert_vector :279-288 and finalize_index :234-277): the std::map
+// accumulation "first inserted representative per (patch, cell, code) wins,
+// boxes in lexicographic cell order, codes ascending" is reproduced as a
+// stable radix sort of packed (patch, cell, code) keys carrying the insertion
+// index (config-major, then patch, then field point), followed by run-head
+// compaction: the head of every equal-key run is its first-inserted vector.
+//
+// Query (query_domains :380-448): BVH traversal with closed, 1e-9-inflated
+// cell bounds only ever reports the box whose cell equals floor(p / w), and
+// a patch owns at most one box per cell, so a query is an exact cell lookup.
+// The device index is a hash from cell to the run of boxes sharing that cell,
+// sorted by patch (the reference's hit order).
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "dev_geom.cuh"
+
+namespace lgd {
+
+struct DField {
+  double w;
+  int C;
+  const double* codebook;  // [C][3]
+  int P;
+  const int* patch_link;     // [P]
+  const int* patch_box_off;  // [P+1]
+  long long B;
+  const long long* box_cell;      // [B][3]
+  const int* box_patch;           // [B]
+  const long long* box_code_off;  // [B+1]
+  const uint16_t* codes;          // [n_codes]
+  const int* rep_point;           // [n_codes] global patch-point index
+  // cell hash: run r covers cell_box[run_start[r] .. run_start[r]+run_count[r])
+  int hash_mask;
+  const int* hash_run;  // [mask+1] run id or -1
+  const int* run_start;
+  const int* run_count;
+  const int* cell_box;  // box ids ordered by (cell, patch)
+};
+
+__device__ __forceinline__ uint64_t cell_hash(long long x, long long y, long long z) {
+  return mix64((uint64_t)x * 0x9E3779B97F4A7C15ull ^ (uint64_t)y * 0xC2B2AE3D27D4EB4Full ^
+               (uint64_t)z * 0x165667B19E3779F9ull);
+}
+
+// cell_of (contact_field.cpp:176-180): division, not multiplication by 1/w.
+__device__ __forceinline__ void cell_of(V3 p, double w, long long* c) {
+  c[0] = (long long)floor(p.x / w);
+  c[1] = (long long)floor(p.y / w);
+  c[2] = (long long)floor(p.z / w);
+}
+
+__device__ __forceinline__ int find_run(const DField& f, const long long* c) {
+  uint64_t h = cell_hash(c[0], c[1], c[2]) & (uint64_t)f.hash_mask;
+  for (;;) {
+    int r = f.hash_run[h];
+    if (r < 0) return -1;
+    int b = f.cell_box[f.run_start[r]];
+    const long long* bc = f.box_cell + 3 * b;
+    if (bc[0] == c[0] && bc[1] == c[1] && bc[2] == c[2]) return r;
+    h = (h + 1) & (uint64_t)f.hash_mask;
+  }
+}
+
+// ------------------------------------------------------------ field build
+// field_config (contact_field.cpp:101-114) + FK: one thread per config.
+__global__ void k_field_frames(int N, uint64_t seed, double* frames) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  DRng rng;
+  rng.seed(mix_seed(seed, 0x636f6e66ull, (uint64_t)c));
+  double q[kMaxDof];
+  for (int j = 0; j < c_hand.dof; ++j) q[j] = rng.uniform(c_hand.jlo[j], c_hand.jhi[j]);
+  Xf fr[kMaxLinks];
+  fk(q, fr);
+  double* out = frames + (size_t)c * c_hand.n_links * 12;
+  for (int l = 0; l < c_hand.n_links; ++l) {
+    m3_store(out + 12 * l, fr[l].R);
+    v3_store(out + 12 * l + 9, fr[l].t);
+  }
+}
+
+// Contact vectors: one thread per (config, field point); quantize_normal
+// (:160-172) as a 256-way argmax over a shared-memory codebook, strict '>'
+// so the lowest code wins ties.
+__global__ void k_field_vectors(int N, int F, const int* fp_link, const int* fp_point,
+                                const double* pts, const double* nrm, const double* frames,
+                                const double* codebook, int C, double w, long long* cells,
+                                uint16_t* codes, long long* cmin, long long* cmax) {
+  extern __shared__ double s_cb[];
+  for (int i = threadIdx.x; i < 3 * C; i += blockDim.x) s_cb[i] = codebook[i];
+  __syncthreads();
+  long long lmin[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX};
+  long long lmax[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  const long long V = (long long)N * F;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(v / F);
+    int f = (int)(v - (long long)c * F);
+    int link = fp_link[f];
+    int pi = fp_point[f];
+    const double* fr = frames + ((size_t)c * c_hand.n_links + link) * 12;
+    Xf x;
+    x.R = m3_load(fr);
+    x.t = v3_load(fr + 9);
+    V3 pos = xf_apply(x, v3_load(pts + 3 * pi));
+    V3 n = xf_rotate(x, v3_load(nrm + 3 * pi));
+    int best = 0;
+    double best_dot = -2.0;
+    for (int i = 0; i < C; ++i) {
+      double d = dot(v3(s_cb[3 * i], s_cb[3 * i + 1], s_cb[3 * i + 2]), n);
+      if (d > best_dot) {
+        best_dot = d;
+        best = i;
+      }
+    }
+    long long cl[3];
+    cell_of(pos, w, cl);
+    cells[3 * v] = cl[0];
+    cells[3 * v + 1] = cl[1];
+    cells[3 * v + 2] = cl[2];
+    codes[v] = (uint16_t)best;
+    for (int a = 0; a < 3; ++a) {
+      lmin[a] = cl[a] < lmin[a] ? cl[a] : lmin[a];
+      lmax[a] = cl[a] > lmax[a] ? cl[a] : lmax[a];
+    }
+  }
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      long long mn = __shfl_xor_sync(0xffffffffu, lmin[a], o);
+      long long mx = __shfl_xor_sync(0xffffffffu, lmax[a], o);
+      lmin[a] = mn < lmin[a] ? mn : lmin[a];
+      lmax[a] = mx > lmax[a] ? mx : lmax[a];
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin((long long*)&cmin[a], lmin[a]);
+      atomicMax((long long*)&cmax[a], lmax[a]);
+    }
+  }
+}
+
+struct KeyLayout {
+  int sh_code, sh_z, sh_y, sh_x, sh_patch, bits_total;
+  long long base[3];
+};
+
+// Packs (patch, cell - min, code) MSB -> LSB; the vector index rides along
+// as the sort value so equal keys keep insertion order.
+__global__ void k_field_keys(long long V, int F, const int* fp_patch, const long long* cells,
+                             const uint16_t* codes, KeyLayout L, unsigned long long* keys,
+                             uint32_t* vals) {
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < V;
+       v += (long long)gridDim.x * blockDim.x) {
+    int f = (int)(v % F);
+    unsigned long long k = (unsigned long long)fp_patch[f] << L.sh_patch;
+    k |= (unsigned long long)(cells[3 * v] - L.base[0]) << L.sh_x;
+    k |= (unsigned long long)(cells[3 * v + 1] - L.base[1]) << L.sh_y;
+    k |= (unsigned long long)(cells[3 * v + 2] - L.base[2]) << L.sh_z;
+    k |= (unsigned long long)codes[v] << L.sh_code;
+    keys[v] = k;
+    vals[v] = (uint32_t)v;
+  }
+}
+
+// Run heads: code entry = new (patch, cell, code); box = new (patch, cell).
+__global__ void k_field_heads(long long V, const unsigned long long* keys, int sh_z,
+                              int* code_head, int* box_head) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < V;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long k = keys[i];
+    bool ch = i == 0 || keys[i - 1] != k;
+    bool bh = i == 0 || (keys[i - 1] >> sh_z) != (k >> sh_z);
+    code_head[i] = ch ? 1 : 0;
+    box_head[i] = bh ? 1 : 0;
+  }
+}
+
+__global__ void k_field_emit(long long V, int F, const unsigned long long* keys,
+                             const uint32_t* vals, const int* code_head, const int* box_head,
+                             const int* code_id, const int* box_id, const long long* cells,
+                             const int* fp_patch, const int* fp_point, KeyLayout L,
+                             uint16_t* out_codes, int* out_rep, long long* box_cell,
+                             int* box_patch, long long* box_code_off, int* patch_box_off) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < V;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (!code_head[i]) continue;
+    uint32_t v = vals[i];
+    int f = (int)(v % (uint32_t)F);
+    int ce = code_id[i];
+    out_codes[ce] = (uint16_t)((keys[i] >> L.sh_code) & ((1ull << (L.sh_z - L.sh_code)) - 1ull));
+    out_rep[ce] = fp_point[f];
+    if (box_head[i]) {
+      int b = box_id[i];
+      box_cell[3 * b] = cells[3 * (long long)v];
+      box_cell[3 * b + 1] = cells[3 * (long long)v + 1];
+      box_cell[3 * b + 2] = cells[3 * (long long)v + 2];
+      int p = fp_patch[f];
+      box_patch[b] = p;
+      box_code_off[b] = ce;
+      bool new_patch = i == 0 || (keys[i - 1] >> L.sh_patch) != (keys[i] >> L.sh_patch);
+      if (new_patch) patch_box_off[p] = b;
+    }
+  }
+}
+
+// Boxes re-keyed by (cell, patch) for the cell hash.
+__global__ void k_cell_keys(long long B, const long long* box_cell, const int* box_patch,
+                            KeyLayout L, unsigned long long* keys, uint32_t* vals) {
+  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B;
+       b += (long long)gridDim.x * blockDim.x) {
+    unsigned long long k = (unsigned long long)(box_cell[3 * b] - L.base[0]) << L.sh_x;
+    k |= (unsigned long long)(box_cell[3 * b + 1] - L.base[1]) << L.sh_y;
+    k |= (unsigned long long)(box_cell[3 * b + 2] - L.base[2]) << L.sh_z;
+    k |= (unsigned long long)box_patch[b] << L.sh_patch;
+    keys[b] = k;
+    vals[b] = (uint32_t)b;
+  }
+}
+
+__global__ void k_cell_heads(long long B, const unsigned long long* keys, int sh_z, int* head) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < B;
+       i += (long long)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || (keys[i - 1] >> sh_z) != (keys[i] >> sh_z)) ? 1 : 0;
+}
+
+__global__ void k_cell_runs(long long B, const int* head, const int* run_id, int* run_start,
+                            int* run_count, int n_runs) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < B;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (!head[i]) continue;
+    int r = run_id[i];
+    run_start[r] = (int)i;
+    long long e = i + 1;
+    while (e < B && !head[e]) ++e;
+    run_count[r] = (int)(e - i);
+  }
+  (void)n_runs;
+}
+
+__global__ void k_cell_hash_insert(int n_runs, const int* run_start, const int* cell_box,
+                                   const long long* box_cell, int mask, int* hash_run) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_runs) return;
+  const long long* c = box_cell + 3 * cell_box[run_start[r]];
+  uint64_t h = cell_hash(c[0], c[1], c[2]) & (uint64_t)mask;
+  for (;;) {
+    int old = atomicCAS(&hash_run[h], -1, r);
+    if (old == -1) return;
+    h = (h + 1) & (uint64_t)mask;
+  }
+}
+
+// --------------------------------------------------------------- queries
+// Hits of one transformed sample: calls visit(patch, box_global, best) for
+// every patch whose box at cell(p) passes the >= theta code test, in patch
+// order (contact_field.cpp:412-432).
+template <typename Visit>
+__device__ __forceinline__ void sample_hits(const DField& f, const double* cb, V3 p, V3 n,
+                                            double theta, Visit&& visit) {
+  long long c[3];
+  cell_of(p, f.w, c);
+  int r = find_run(f, c);
+  if (r < 0) return;
+  int s = f.run_start[r], e = s + f.run_count[r];
+  for (int j = s; j < e; ++j) {
+    int b = f.cell_box[j];
+    double best = -2.0;
+    for (long long q = f.box_code_off[b]; q < f.box_code_off[b + 1]; ++q) {
+      int code = f.codes[q];
+      best = dmax(best, -dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n));
+    }
+    if (best >= theta) visit(f.box_patch[b], b, best);
+  }
+}
+
+}  // namespace lgd

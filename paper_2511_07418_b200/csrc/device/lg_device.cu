@@ -1,0 +1,1233 @@
+// lg_device.cu — device half of the C-ABI: context, contact-field build,
+// batched stage entry points and the run_batch driver (reference
+// pipeline.cpp:308-625) on one B200.  Single translation unit so that the
+// constant-memory hand model is visible to every kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../capi_common.hpp"
+#include "dev_stages.cuh"
+
+using namespace lgd;
+
+namespace {
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw lgc::cuda_error(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+// ---------------------------------------------------------------- buffers
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t bytes) {
+    if (bytes <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (bytes == 0) bytes = 8;
+    CK(cudaMalloc(&p, bytes));
+    n = bytes;
+  }
+  template <typename T>
+  T* as() const {
+    return (T*)p;
+  }
+};
+
+template <typename T>
+T* dalloc(Buf& b, size_t count) {
+  b.alloc(count * sizeof(T));
+  return b.as<T>();
+}
+template <typename T>
+T* dupload(Buf& b, const T* src, size_t count, cudaStream_t s) {
+  T* d = dalloc<T>(b, count);
+  if (count) CK(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  return d;
+}
+template <typename T>
+std::vector<T> ddownload(const T* src, size_t count, cudaStream_t s) {
+  std::vector<T> v(count);
+  if (count) CK(cudaMemcpyAsync(v.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return v;
+}
+
+int grid_for(long long n, int block) {
+  long long g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return (int)g;
+}
+
+int bits_for(unsigned long long range) {
+  int b = 0;
+  while (b < 64 && (range >> b) != 0ull) ++b;
+  return b;
+}
+
+// Host-side dependency groups from a flat description (hand.cpp:515-552).
+std::vector<int> groups_of(const lg_hand_desc& h, int* n_groups) {
+  int n = h.n_links;
+  std::vector<bool> st(n, false);
+  for (int ii = 0; ii < n; ++ii) {
+    int l = h.topo_order[ii];
+    if (h.parent[l] < 0) st[l] = true;
+    else if (st[h.parent[l]] && h.joint_type[l] == 0) st[l] = true;
+  }
+  std::vector<int> seed(n, -1);
+  std::map<int, std::vector<int>> by;
+  for (int ii = 0; ii < n; ++ii) {
+    int l = h.topo_order[ii];
+    if (st[l]) continue;
+    int p = h.parent[l];
+    seed[l] = (p >= 0 && !st[p]) ? seed[p] : l;
+    by[seed[l]].push_back(l);
+  }
+  std::vector<std::vector<int>> groups;
+  for (auto& kv : by) {
+    std::sort(kv.second.begin(), kv.second.end());
+    groups.push_back(kv.second);
+  }
+  std::sort(groups.begin(), groups.end(),
+            [](const std::vector<int>& a, const std::vector<int>& b) { return a[0] < b[0]; });
+  std::vector<int> out(n, -1);
+  for (size_t g = 0; g < groups.size(); ++g)
+    for (int l : groups[g]) out[l] = (int)g;
+  *n_groups = (int)groups.size();
+  return out;
+}
+
+std::vector<double> make_codebook(int size) {  // contact_field.cpp:144-158 (host, glibc)
+  if (size < 1 || size > 65536) throw std::invalid_argument("make_codebook: size out of range");
+  std::vector<double> d(3 * size);
+  const double kPiH = 3.14159265358979323846;
+  const double golden = kPiH * (3.0 - std::sqrt(5.0));
+  for (int i = 0; i < size; ++i) {
+    double z = 1.0 - 2.0 * (i + 0.5) / size;
+    double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    double a = golden * i;
+    d[3 * i] = r * std::cos(a);
+    d[3 * i + 1] = r * std::sin(a);
+    d[3 * i + 2] = z;
+  }
+  return d;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ ctx
+struct lg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_n = 0;
+  // hand currently bound to constant memory
+  Buf h_vert_off, h_verts, h_tri_off, h_tris, h_plane_off, h_planes, h_bounds, h_part_link;
+  int n_parts = 0;
+  long long launches = 0;
+  void* tmp(size_t n) {
+    if (n > cub_n) {
+      if (cub_tmp) cudaFree(cub_tmp);
+      cub_tmp = nullptr;
+      CK(cudaMalloc(&cub_tmp, n));
+      cub_n = n;
+    }
+    return cub_tmp;
+  }
+};
+
+namespace {
+
+#define LAUNCH(ctx) ++(ctx)->launches
+
+void check_launch() { CK(cudaGetLastError()); }
+
+// Binds a hand description to constant memory (one hand per call).
+void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
+  if (d.n_links > kMaxLinks) throw std::invalid_argument("device: hand has too many links (max 32)");
+  if (d.dof > kMaxDof) throw std::invalid_argument("device: hand has too many joints (max 24)");
+  if (d.n_parts > 63) throw std::invalid_argument("device: hand has too many convex parts (max 63)");
+  DHand h;
+  std::memset(&h, 0, sizeof(h));
+  h.n_links = d.n_links;
+  h.dof = d.dof;
+  h.root = d.root;
+  h.n_parts = d.n_parts;
+  for (int l = 0; l < d.n_links; ++l) {
+    h.parent[l] = d.parent[l];
+    h.jtype[l] = d.joint_type[l];
+    h.jidx[l] = d.joint_index[l];
+    h.topo[l] = d.topo_order[l];
+    for (int a = 0; a < 9; ++a) h.R[l][a] = d.origin_R[9 * l + a];
+    for (int a = 0; a < 3; ++a) {
+      h.t[l][a] = d.origin_t[3 * l + a];
+      h.axis[l][a] = d.axis[3 * l + a];
+    }
+    h.lo[l] = d.limit_lo[l];
+    h.hi[l] = d.limit_hi[l];
+    h.part_begin[l] = 0;
+    h.part_end[l] = 0;
+    if (d.joint_index[l] >= 0) {
+      h.jlo[d.joint_index[l]] = d.limit_lo[l];
+      h.jhi[d.joint_index[l]] = d.limit_hi[l];
+      h.mid[d.joint_index[l]] = 0.5 * (d.limit_lo[l] + d.limit_hi[l]);
+    }
+  }
+  for (int p = 0; p < d.n_parts; ++p) {
+    int l = d.part_link[p];
+    if (p > 0 && d.part_link[p] < d.part_link[p - 1])
+      throw std::invalid_argument("device: parts must be grouped by link");
+    if (h.part_end[l] == 0) h.part_begin[l] = p;
+    h.part_end[l] = p + 1;
+  }
+  cudaStream_t s = ctx->stream;
+  int nv = d.n_parts ? d.part_vert_off[d.n_parts] : 0;
+  int nt = d.n_parts ? d.part_tri_off[d.n_parts] : 0;
+  int npl = d.n_parts ? d.part_plane_off[d.n_parts] : 0;
+  static const int zero = 0;
+  h.vert_off = dupload(ctx->h_vert_off, d.n_parts ? d.part_vert_off : &zero, d.n_parts + 1, s);
+  h.verts = dupload(ctx->h_verts, d.part_verts, 3 * (size_t)nv, s);
+  h.tri_off = dupload(ctx->h_tri_off, d.n_parts ? d.part_tri_off : &zero, d.n_parts + 1, s);
+  h.tris = dupload(ctx->h_tris, d.part_tris, 3 * (size_t)nt, s);
+  h.plane_off = dupload(ctx->h_plane_off, d.n_parts ? d.part_plane_off : &zero, d.n_parts + 1, s);
+  h.planes = dupload(ctx->h_planes, d.part_planes, 4 * (size_t)npl, s);
+  h.bounds = dupload(ctx->h_bounds, d.part_bounds, 6 * (size_t)d.n_parts, s);
+  dupload(ctx->h_part_link, d.part_link, (size_t)d.n_parts, s);
+  ctx->n_parts = d.n_parts;
+  CK(cudaMemcpyToSymbolAsync(c_hand, &h, sizeof(DHand), 0, cudaMemcpyHostToDevice, s));
+}
+
+// Flattened patch data on the device.
+struct DevPatches {
+  int P = 0, F = 0, npts = 0;
+  Buf pts, nrm, link, point_off, fp_off, fps, fp_link, fp_point, fp_patch;
+  std::vector<int> h_link, h_point_off, h_fp_off, h_fps;
+  std::vector<double> h_pts, h_nrm;
+};
+
+void upload_patches(lg_ctx* ctx, const lg_patches_desc& d, DevPatches& o) {
+  cudaStream_t s = ctx->stream;
+  o.P = d.n_patches;
+  if (o.P < 1) throw std::invalid_argument("index build: no patches");
+  o.npts = d.point_off[o.P];
+  o.F = d.fp_off[o.P];
+  o.h_link.assign(d.link, d.link + o.P);
+  o.h_point_off.assign(d.point_off, d.point_off + o.P + 1);
+  o.h_fp_off.assign(d.fp_off, d.fp_off + o.P + 1);
+  o.h_fps.assign(d.field_points, d.field_points + o.F);
+  o.h_pts.assign(d.points, d.points + 3 * (size_t)o.npts);
+  o.h_nrm.assign(d.normals, d.normals + 3 * (size_t)o.npts);
+  std::vector<int> fl(o.F), fpnt(o.F), fpat(o.F);
+  for (int p = 0; p < o.P; ++p)
+    for (int f = d.fp_off[p]; f < d.fp_off[p + 1]; ++f) {
+      fl[f] = d.link[p];
+      fpnt[f] = d.point_off[p] + d.field_points[f];
+      fpat[f] = p;
+    }
+  dupload(o.pts, d.points, 3 * (size_t)o.npts, s);
+  dupload(o.nrm, d.normals, 3 * (size_t)o.npts, s);
+  dupload(o.link, d.link, (size_t)o.P, s);
+  dupload(o.point_off, d.point_off, (size_t)o.P + 1, s);
+  dupload(o.fp_off, d.fp_off, (size_t)o.P + 1, s);
+  dupload(o.fps, d.field_points, (size_t)o.F, s);
+  dupload(o.fp_link, fl.data(), fl.size(), s);
+  dupload(o.fp_point, fpnt.data(), fpnt.size(), s);
+  dupload(o.fp_patch, fpat.data(), fpat.size(), s);
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- field
+struct lg_field {
+  lg_ctx* ctx = nullptr;
+  DField f;
+  DevPatches patches;
+  Buf codebook, patch_link, patch_box_off, box_cell, box_patch, box_code_off, codes, rep_point,
+      hash_run, run_start, run_count, cell_box;
+  long long n_vectors = 0, n_codes = 0;
+  int n_runs = 0;
+  double build_ms = 0.0;
+  // host export storage
+  std::vector<double> x_codebook, x_rep_point, x_rep_normal;
+  std::vector<int> x_patch_link, x_patch_box_off, x_rep_link;
+  std::vector<long long> x_box_cell, x_box_code_off;
+  std::vector<uint16_t> x_codes;
+};
+
+namespace {
+
+template <typename K, typename V>
+void radix_sort_pairs(lg_ctx* ctx, const K* kin, K* kout, const V* vin, V* vout, long long n,
+                      int end_bit) {
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                     ctx->stream));
+  void* tmp = ctx->tmp(bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                     ctx->stream));
+  LAUNCH(ctx);
+}
+
+int exclusive_scan_count(lg_ctx* ctx, const int* flags, int* ids, long long n) {
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, ids, (int)n, ctx->stream));
+  void* tmp = ctx->tmp(bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, flags, ids, (int)n, ctx->stream));
+  LAUNCH(ctx);
+  int last_id = 0, last_flag = 0;
+  CK(cudaMemcpyAsync(&last_id, ids + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&last_flag, flags + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return last_id + last_flag;
+}
+
+// ContactFieldIndex::build on the device (see dev_field.cuh).
+void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc& pd, int N,
+                        double w, uint64_t seed, int C, lg_field* out) {
+  if (pd.n_patches < 1) throw std::invalid_argument("index build: no patches");
+  if (w <= 0.0 || N < 1) throw std::invalid_argument("index build: bad box width or N");
+  cudaStream_t s = ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  bind_hand(ctx, hd);
+  upload_patches(ctx, pd, out->patches);
+  DevPatches& P = out->patches;
+  auto cb = make_codebook(C);
+  out->x_codebook = cb;
+  const double* d_cb = dupload(out->codebook, cb.data(), cb.size(), s);
+  CK(cudaEventRecord(e0, s));
+  const int L = hd.n_links;
+  const long long V = (long long)N * P.F;
+  if (V > 0xffffffffll) throw std::invalid_argument("index build: too many contact vectors");
+  Buf frames, cells, codes16, cmm;
+  double* d_frames = dalloc<double>(frames, (size_t)N * L * 12);
+  k_field_frames<<<grid_for(N, 128), 128, 0, s>>>(N, seed, d_frames);
+  LAUNCH(ctx);
+  check_launch();
+  long long* d_cells = dalloc<long long>(cells, 3 * (size_t)V);
+  uint16_t* d_codes = dalloc<uint16_t>(codes16, (size_t)V);
+  long long* d_cmm = dalloc<long long>(cmm, 6);
+  long long init[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
+  CK(cudaMemcpyAsync(d_cmm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  size_t cb_smem = 3 * (size_t)C * sizeof(double);
+  if (cb_smem > 200 * 1024) throw std::invalid_argument("index build: codebook too large for the device build");
+  CK(cudaFuncSetAttribute(k_field_vectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb_smem));
+  k_field_vectors<<<grid_for(V, 256), 256, cb_smem, s>>>(
+      N, P.F, P.fp_link.as<int>(), P.fp_point.as<int>(), P.pts.as<double>(), P.nrm.as<double>(),
+      d_frames, d_cb, C, w, d_cells, d_codes, d_cmm, d_cmm + 3);
+  LAUNCH(ctx);
+  check_launch();
+  long long cmm_h[6];
+  CK(cudaMemcpyAsync(cmm_h, d_cmm, sizeof(cmm_h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  KeyLayout KL;
+  int bc = bits_for((unsigned long long)(C - 1));
+  int bz = bits_for((unsigned long long)(cmm_h[5] - cmm_h[2]));
+  int by = bits_for((unsigned long long)(cmm_h[4] - cmm_h[1]));
+  int bx = bits_for((unsigned long long)(cmm_h[3] - cmm_h[0]));
+  int bp = bits_for((unsigned long long)(P.P - 1));
+  KL.sh_code = 0;
+  KL.sh_z = bc;
+  KL.sh_y = bc + bz;
+  KL.sh_x = bc + bz + by;
+  KL.sh_patch = bc + bz + by + bx;
+  KL.bits_total = KL.sh_patch + bp;
+  KL.base[0] = cmm_h[0];
+  KL.base[1] = cmm_h[1];
+  KL.base[2] = cmm_h[2];
+  if (KL.bits_total > 64) throw std::runtime_error("index build: packed field key exceeds 64 bits");
+  Buf keys, keys2, vals, vals2, chead, bhead, cid, bid;
+  auto* d_keys = dalloc<unsigned long long>(keys, (size_t)V);
+  auto* d_keys2 = dalloc<unsigned long long>(keys2, (size_t)V);
+  auto* d_vals = dalloc<uint32_t>(vals, (size_t)V);
+  auto* d_vals2 = dalloc<uint32_t>(vals2, (size_t)V);
+  k_field_keys<<<grid_for(V, 256), 256, 0, s>>>(V, P.F, P.fp_patch.as<int>(), d_cells, d_codes, KL,
+                                                 d_keys, d_vals);
+  LAUNCH(ctx);
+  check_launch();
+  radix_sort_pairs(ctx, d_keys, d_keys2, d_vals, d_vals2, V, std::max(1, KL.bits_total));
+  int* d_ch = dalloc<int>(chead, (size_t)V);
+  int* d_bh = dalloc<int>(bhead, (size_t)V);
+  int* d_cid = dalloc<int>(cid, (size_t)V);
+  int* d_bid = dalloc<int>(bid, (size_t)V);
+  k_field_heads<<<grid_for(V, 256), 256, 0, s>>>(V, d_keys2, KL.sh_z, d_ch, d_bh);
+  LAUNCH(ctx);
+  check_launch();
+  long long n_codes = exclusive_scan_count(ctx, d_ch, d_cid, V);
+  long long n_boxes = exclusive_scan_count(ctx, d_bh, d_bid, V);
+  auto* o_codes = dalloc<uint16_t>(out->codes, (size_t)n_codes);
+  auto* o_rep = dalloc<int>(out->rep_point, (size_t)n_codes);
+  auto* o_cell = dalloc<long long>(out->box_cell, 3 * (size_t)n_boxes);
+  auto* o_bpatch = dalloc<int>(out->box_patch, (size_t)n_boxes);
+  auto* o_bco = dalloc<long long>(out->box_code_off, (size_t)n_boxes + 1);
+  auto* o_pbo = dalloc<int>(out->patch_box_off, (size_t)P.P + 1);
+  k_field_emit<<<grid_for(V, 256), 256, 0, s>>>(V, P.F, d_keys2, d_vals2, d_ch, d_bh, d_cid, d_bid,
+                                                 d_cells, P.fp_patch.as<int>(), P.fp_point.as<int>(),
+                                                 KL, o_codes, o_rep, o_cell, o_bpatch, o_bco, o_pbo);
+  LAUNCH(ctx);
+  check_launch();
+  int nb_i = (int)n_boxes;
+  long long nc_ll = n_codes;
+  CK(cudaMemcpyAsync(o_pbo + P.P, &nb_i, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(o_bco + n_boxes, &nc_ll, sizeof(long long), cudaMemcpyHostToDevice, s));
+  dupload(out->patch_link, P.h_link.data(), P.h_link.size(), s);
+
+  // cell hash: boxes keyed by (cell, patch)
+  KeyLayout K2;
+  K2.sh_patch = 0;
+  K2.sh_z = bp;
+  K2.sh_y = bp + bz;
+  K2.sh_x = bp + bz + by;
+  K2.sh_code = 0;
+  K2.bits_total = bp + bz + by + bx;
+  K2.base[0] = KL.base[0];
+  K2.base[1] = KL.base[1];
+  K2.base[2] = KL.base[2];
+  Buf ck, ck2, cv, cv2, chd, crid;
+  auto* d_ck = dalloc<unsigned long long>(ck, (size_t)n_boxes);
+  auto* d_ck2 = dalloc<unsigned long long>(ck2, (size_t)n_boxes);
+  auto* d_cv = dalloc<uint32_t>(cv, (size_t)n_boxes);
+  auto* o_cellbox = dalloc<int>(out->cell_box, (size_t)n_boxes);
+  k_cell_keys<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, o_cell, o_bpatch, K2, d_ck, d_cv);
+  LAUNCH(ctx);
+  check_launch();
+  radix_sort_pairs(ctx, d_ck, d_ck2, d_cv, (uint32_t*)o_cellbox, n_boxes, std::max(1, K2.bits_total));
+  int* d_chd = dalloc<int>(chd, (size_t)n_boxes);
+  int* d_crid = dalloc<int>(crid, (size_t)n_boxes);
+  k_cell_heads<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, d_ck2, K2.sh_z, d_chd);
+  LAUNCH(ctx);
+  check_launch();
+  int n_runs = exclusive_scan_count(ctx, d_chd, d_crid, n_boxes);
+  auto* o_rs = dalloc<int>(out->run_start, (size_t)n_runs);
+  auto* o_rc = dalloc<int>(out->run_count, (size_t)n_runs);
+  k_cell_runs<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, d_chd, d_crid, o_rs, o_rc, n_runs);
+  LAUNCH(ctx);
+  check_launch();
+  int cap = 1024;
+  while (cap < 2 * n_runs) cap <<= 1;
+  auto* o_hash = dalloc<int>(out->hash_run, (size_t)cap);
+  CK(cudaMemsetAsync(o_hash, 0xff, (size_t)cap * sizeof(int), s));
+  k_cell_hash_insert<<<grid_for(n_runs, 256), 256, 0, s>>>(n_runs, o_rs, o_cellbox, o_cell, cap - 1,
+                                                             o_hash);
+  LAUNCH(ctx);
+  check_launch();
+  CK(cudaEventRecord(e1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out->build_ms = ms;
+  out->n_vectors = V;
+  out->n_codes = n_codes;
+  out->n_runs = n_runs;
+  DField& f = out->f;
+  f.w = w;
+  f.C = C;
+  f.codebook = d_cb;
+  f.P = P.P;
+  f.patch_link = out->patch_link.as<int>();
+  f.patch_box_off = o_pbo;
+  f.B = n_boxes;
+  f.box_cell = o_cell;
+  f.box_patch = o_bpatch;
+  f.box_code_off = o_bco;
+  f.codes = o_codes;
+  f.rep_point = o_rep;
+  f.hash_mask = cap - 1;
+  f.hash_run = o_hash;
+  f.run_start = o_rs;
+  f.run_count = o_rc;
+  f.cell_box = o_cellbox;
+}
+
+// ------------------------------------------------------------- run_batch
+struct RunOut {
+  lg_profile profile;
+  std::vector<lg_grasp> grasps;
+  std::vector<lg_trace> traces;
+};
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void start() { CK(cudaEventRecord(a, s)); }
+  double stop() {
+    CK(cudaEventRecord(b, s));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+  }
+};
+
+DSamples make_samples(Buf* cols, int n) {
+  DSamples d;
+  d.n = n;
+  for (int a = 0; a < 6; ++a) d.x[a] = cols[a].as<double>();
+  return d;
+}
+
+void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc& pd,
+                      lg_field* field_in, const double* raw, int n_raw, const lg_run_params& cfg,
+                      RunOut& out) {
+  auto wall0 = std::chrono::steady_clock::now();
+  cudaStream_t s = ctx->stream;
+  std::memset(&out.profile, 0, sizeof(out.profile));
+  long long launches0 = ctx->launches;
+  if (cfg.k_contacts < 1 || cfg.k_contacts > kMaxK) throw std::invalid_argument("k_contacts out of range");
+  if (n_raw < 1) throw std::invalid_argument("place_object: no object samples");
+  Timer tm(s);
+  // ---- field (ContactFieldIndex::build) or reuse
+  std::unique_ptr<lg_field> own;
+  lg_field* field = field_in;
+  if (!field) {
+    own.reset(new lg_field);
+    own->ctx = ctx;
+    build_field_device(ctx, hd, pd, cfg.field_configs, cfg.box_width, cfg.seed, cfg.codebook_size,
+                       own.get());
+    field = own.get();
+    out.profile.field_build = field->build_ms * 1e-3;
+  } else {
+    bind_hand(ctx, hd);
+  }
+  const DField& F = field->f;
+  const DevPatches& DP = field->patches;
+  out.profile.patches = F.P;
+  out.profile.boxes = F.B;
+  out.profile.field_vectors = field->n_vectors;
+  out.profile.object_samples = n_raw;
+
+  // ---- object samples (raw SoA) and preprocess_object
+  tm.start();
+  std::vector<double> col(n_raw);
+  Buf rawc[6];
+  for (int a = 0; a < 6; ++a) {
+    for (int i = 0; i < n_raw; ++i) col[i] = raw[6 * i + a];
+    dupload(rawc[a], col.data(), (size_t)n_raw, s);
+    CK(cudaStreamSynchronize(s));
+  }
+  DSamples RS = make_samples(rawc, n_raw);
+  Buf keepb;
+  uint8_t* d_keep = dalloc<uint8_t>(keepb, (size_t)n_raw);
+  if (cfg.probe_half_width <= 0.0 || cfg.probe_depth_threshold < 0.0)
+    throw std::invalid_argument("preprocess_object: bad probe dimensions");
+  k_preprocess<<<grid_for(n_raw, 256), 256, 0, s>>>(RS, cfg.probe_half_width, cfg.probe_depth_threshold, d_keep);
+  LAUNCH(ctx);
+  check_launch();
+  auto keep = ddownload(d_keep, (size_t)n_raw, s);
+  std::vector<int> kept;
+  for (int i = 0; i < n_raw; ++i)
+    if (keep[i]) kept.push_back(i);
+  const int ns = (int)kept.size();
+  if (ns == 0) throw std::runtime_error("run_batch: preprocessing stripped every object sample");
+  out.profile.field_samples = ns;
+  Buf fsc[6];
+  for (int a = 0; a < 6; ++a) {
+    for (int j = 0; j < ns; ++j) col[j] = raw[6 * kept[j] + a];
+    dupload(fsc[a], col.data(), (size_t)ns, s);
+    CK(cudaStreamSynchronize(s));
+  }
+  DSamples FS = make_samples(fsc, ns);
+
+  // ---- groups, statics (collect_static_surface)
+  int G = 0;
+  std::vector<int> gol = groups_of(hd, &G);
+  if (G > LG_MAX_GROUPS) throw std::invalid_argument("device: too many dependency groups (max 32)");
+  std::vector<int> gop(DP.P);
+  for (int p = 0; p < DP.P; ++p) gop[p] = gol[DP.h_link[p]];
+  Buf gopb;
+  int* d_gop = dupload(gopb, gop.data(), gop.size(), s);
+  std::vector<int> sp_part, sp_link, pt_idx, pt_link;
+  for (int l = 0; l < hd.n_links; ++l) {
+    if (gol[l] != -1) continue;
+    for (int p = 0; p < hd.n_parts; ++p)
+      if (hd.part_link[p] == l) {
+        sp_part.push_back(p);
+        sp_link.push_back(l);
+      }
+  }
+  for (int p = 0; p < DP.P; ++p) {
+    if (gop[p] != -1) continue;
+    for (int i = DP.h_point_off[p]; i < DP.h_point_off[p + 1]; ++i) {
+      pt_idx.push_back(i);
+      pt_link.push_back(DP.h_link[p]);
+    }
+  }
+  const int n_sp = (int)sp_part.size(), n_ss = (int)pt_idx.size();
+  Buf b_spp, b_spl, b_pti, b_ptl, b_ssp, b_ssn, b_spose, b_ssl;
+  int* d_spp = dupload(b_spp, sp_part.data(), sp_part.size(), s);
+  int* d_spl = dupload(b_spl, sp_link.data(), sp_link.size(), s);
+  int* d_pti = dupload(b_pti, pt_idx.data(), pt_idx.size(), s);
+  int* d_ptl = dupload(b_ptl, pt_link.data(), pt_link.size(), s);
+  double* d_ssp = dalloc<double>(b_ssp, 3 * (size_t)n_ss);
+  double* d_ssn = dalloc<double>(b_ssn, 3 * (size_t)n_ss);
+  double* d_spose = dalloc<double>(b_spose, 12 * (size_t)n_sp);
+  int* d_ssl = d_ptl;
+  k_statics<<<1, 256, 0, s>>>(n_ss, d_pti, d_ptl, DP.pts.as<double>(), DP.nrm.as<double>(), n_sp,
+                              d_spl, d_ssp, d_ssn, d_spose);
+  LAUNCH(ctx);
+  check_launch();
+
+  // ---- shard
+  const int B = cfg.batch;
+  int c_lo = 0, c_hi = B;
+  if (cfg.shard_count > 1) {
+    c_lo = (int)((long long)cfg.shard_rank * B / cfg.shard_count);
+    c_hi = (int)((long long)(cfg.shard_rank + 1) * B / cfg.shard_count);
+  }
+  const int Bl = c_hi - c_lo;
+  const int k = cfg.k_contacts;
+  out.profile.candidates = (long long)cfg.passes * Bl;
+  double t_pre = tm.stop();
+
+  // ---- per-candidate placement state (pass 0, reused by later passes)
+  Buf b_pose, b_acc, b_pen, b_nst, b_stl, b_stp, b_stn, b_mask, b_cnt, b_aabb;
+  double* d_pose = dalloc<double>(b_pose, 12 * (size_t)std::max(Bl, 1));
+  int* d_acc = dalloc<int>(b_acc, (size_t)std::max(Bl, 1));
+  double* d_pen = dalloc<double>(b_pen, (size_t)std::max(Bl, 1));
+  int* d_nst = dalloc<int>(b_nst, (size_t)std::max(Bl, 1));
+  int* d_stl = dalloc<int>(b_stl, (size_t)std::max(Bl, 1));
+  double* d_stp = dalloc<double>(b_stp, 3 * (size_t)std::max(Bl, 1));
+  double* d_stn = dalloc<double>(b_stn, 3 * (size_t)std::max(Bl, 1));
+  uint32_t* d_mask = dalloc<uint32_t>(b_mask, (size_t)std::max(Bl, 1) * ns);
+  int* d_cnt = dalloc<int>(b_cnt, (size_t)std::max(Bl, 1) * std::max(G, 1));
+  double* d_aabb = dalloc<double>(b_aabb, 6 * (size_t)std::max(Bl, 1));
+  CK(cudaMemsetAsync(d_stp, 0, 3 * sizeof(double) * std::max(Bl, 1), s));
+  CK(cudaMemsetAsync(d_stn, 0, 3 * sizeof(double) * std::max(Bl, 1), s));
+
+  std::vector<lg_trace> pass_tr;
+  std::vector<double> h_pose;
+  std::vector<int> h_acc, h_nst, h_stl, h_cnt;
+  std::vector<double> h_pen, h_stp, h_stn;
+
+  const int R = cfg.restarts;
+  const long long per_restart = k + 2ll * cfg.n_outer * k * cfg.n_inner;
+  const long long per_cand = (long long)R * per_restart;
+  IkCfg ikc;
+  ikc.beta = cfg.beta;
+  ikc.step_clamp = cfg.step_clamp;
+  ikc.residual_tol = cfg.residual_tol;
+  ikc.damping_scale = cfg.damping_scale;
+  ikc.damping_min = 1e-6;     // IkParams default (ik.hpp:27), not set by run_batch
+  ikc.iterations = cfg.ik_iterations;
+  ikc.max_backtracks = 10;    // IkParams default (ik.hpp:28)
+  WOpts wo;
+  wo.iterations = cfg.pgd_iterations;
+  wo.warm_iterations = cfg.pgd_warm_iterations;
+  wo.step = cfg.pgd_step;
+  wo.max_bt = 20;
+  CollCfg cc;
+  cc.margin = cfg.penetration_margin;
+  cc.raw = RS;
+  cc.part_link = ctx->h_part_link.as<int>();
+
+  for (int pass = 0; pass < cfg.passes && Bl > 0; ++pass) {
+    // -------- stage 1: placement + domains (pass 0) + group pick
+    tm.start();
+    if (pass == 0) {
+      PlaceCfg pc;
+      pc.seed = cfg.seed;
+      pc.c_lo = c_lo;
+      pc.Bl = Bl;
+      pc.mode = cfg.placement_mode;
+      pc.static_prob = cfg.static_contact_prob;
+      pc.margin = cfg.penetration_margin;
+      for (int a = 0; a < 3; ++a) {
+        pc.center[a] = cfg.canonical_center[a];
+        pc.half[a] = cfg.canonical_half_extents[a];
+      }
+      pc.n_ss = n_ss;
+      pc.ss_p = d_ssp;
+      pc.ss_n = d_ssn;
+      pc.ss_link = d_ssl;
+      pc.P = DP.P;
+      pc.patch_link = DP.link.as<int>();
+      pc.point_off = DP.point_off.as<int>();
+      pc.fp_off = DP.fp_off.as<int>();
+      pc.fps = DP.fps.as<int>();
+      pc.pts = DP.pts.as<double>();
+      pc.nrm = DP.nrm.as<double>();
+      k_place_pose<<<grid_for(Bl, 64), 64, 0, s>>>(pc, FS, d_pose, d_nst, d_stl, d_stp, d_stn);
+      LAUNCH(ctx);
+      check_launch();
+      k_place_verdict<<<Bl, 256, 0, s>>>(Bl, FS, d_pose, n_sp, d_spp, d_spose, cfg.penetration_margin,
+                                         d_acc, d_pen);
+      LAUNCH(ctx);
+      check_launch();
+      int cb_smem = 3 * F.C <= 6144 ? 1 : 0;
+      size_t qsm = cb_smem ? 3 * (size_t)F.C * sizeof(double) : 0;
+      k_query<<<Bl, 256, qsm, s>>>(Bl, F, d_gop, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
+                                   d_mask, d_cnt);
+      LAUNCH(ctx);
+      check_launch();
+      k_obj_aabb<<<Bl, 256, 0, s>>>(Bl, RS, d_pose, d_acc, d_aabb);
+      LAUNCH(ctx);
+      check_launch();
+    }
+    Buf b_alive, b_chosen;
+    int* d_alive = dalloc<int>(b_alive, (size_t)Bl);
+    int* d_chosen = dalloc<int>(b_chosen, (size_t)Bl * kMaxK);
+    k_group_pick<<<grid_for(Bl, 128), 128, 0, s>>>(Bl, c_lo, B, pass, cfg.seed, k, G, d_acc, d_cnt,
+                                                    d_alive, d_chosen);
+    LAUNCH(ctx);
+    check_launch();
+    auto h_alive = ddownload(d_alive, (size_t)Bl, s);
+    auto h_chosen = ddownload(d_chosen, (size_t)Bl * kMaxK, s);
+    if (pass == 0 || cfg.want_trace) {
+      h_cnt = ddownload(d_cnt, (size_t)Bl * std::max(G, 1), s);
+    }
+    std::vector<int> alive_idx;
+    for (int i = 0; i < Bl; ++i)
+      if (h_alive[i]) alive_idx.push_back(i);
+    const int nA = (int)alive_idx.size();
+    out.profile.placements_accepted += nA;
+    out.profile.placement_domains += tm.stop();
+
+    if (cfg.want_trace) {
+      if (pass == 0) {
+        h_pose = ddownload(d_pose, 12 * (size_t)Bl, s);
+        h_acc = ddownload(d_acc, (size_t)Bl, s);
+        h_pen = ddownload(d_pen, (size_t)Bl, s);
+        h_nst = ddownload(d_nst, (size_t)Bl, s);
+        h_stl = ddownload(d_stl, (size_t)Bl, s);
+        h_stp = ddownload(d_stp, 3 * (size_t)Bl, s);
+        h_stn = ddownload(d_stn, 3 * (size_t)Bl, s);
+      }
+      pass_tr.assign(Bl, lg_trace());
+      for (int i = 0; i < Bl; ++i) {
+        lg_trace& t = pass_tr[i];
+        std::memset(&t, 0, sizeof(t));
+        t.g = (long long)pass * B + c_lo + i;
+        t.pass = pass;
+        t.c = c_lo + i;
+        t.accepted = h_acc[i];
+        t.penetration = h_pen[i];
+        std::memcpy(t.pose_R, &h_pose[12 * i], 9 * sizeof(double));
+        std::memcpy(t.pose_t, &h_pose[12 * i + 9], 3 * sizeof(double));
+        t.n_static = h_nst[i];
+        t.static_link = h_stl[i];
+        if (h_nst[i]) {
+          std::memcpy(t.static_p, &h_stp[3 * i], 3 * sizeof(double));
+          std::memcpy(t.static_n, &h_stn[3 * i], 3 * sizeof(double));
+        }
+        t.n_groups = G;
+        if (h_acc[i])
+          for (int g = 0; g < G; ++g) t.domain_size[g] = h_cnt[(size_t)i * G + g];
+        t.picked = h_alive[i];
+        if (h_alive[i])
+          for (int q = 0; q < k; ++q) t.chosen[q] = h_chosen[(size_t)i * kMaxK + q];
+      }
+    }
+    if (nA == 0) {
+      if (cfg.want_trace) out.traces.insert(out.traces.end(), pass_tr.begin(), pass_tr.end());
+      continue;
+    }
+
+    // -------- stage 2: contact optimisation
+    tm.start();
+    Buf b_aidx, b_eloff, b_els, b_elp, b_eln;
+    int* d_aidx = dupload(b_aidx, alive_idx.data(), alive_idx.size(), s);
+    std::vector<long long> eloff((size_t)nA * k + 1, 0);
+    for (int a = 0; a < nA; ++a)
+      for (int q = 0; q < k; ++q) {
+        int i = alive_idx[a];
+        eloff[(size_t)a * k + q + 1] =
+            eloff[(size_t)a * k + q] + h_cnt[(size_t)i * G + h_chosen[(size_t)i * kMaxK + q]];
+      }
+    const long long nel = eloff.back();
+    long long* d_eloff = dupload(b_eloff, eloff.data(), eloff.size(), s);
+    int* d_els = dalloc<int>(b_els, (size_t)nel);
+    double* d_elp = dalloc<double>(b_elp, 3 * (size_t)nel);
+    double* d_eln = dalloc<double>(b_eln, 3 * (size_t)nel);
+    k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
+                                         d_elp, d_eln);
+    LAUNCH(ctx);
+    check_launch();
+    Buf b_draws, b_oid, b_oobj, b_oan, b_osol, b_bal;
+    uint64_t* d_draws = dalloc<uint64_t>(b_draws, (size_t)nA * per_cand);
+    k_copt_draws<<<grid_for(nA, 64), 64, 0, s>>>(nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, d_draws);
+    LAUNCH(ctx);
+    check_launch();
+    int* d_oid = dalloc<int>(b_oid, (size_t)nA * kMaxK);
+    double* d_oobj = dalloc<double>(b_oobj, (size_t)nA);
+    int* d_oan = dalloc<int>(b_oan, (size_t)nA);
+    double* d_osol = dalloc<double>(b_osol, (size_t)nA * 3 * kMaxC);
+    int* d_bal = dalloc<int>(b_bal, (size_t)nA);
+    CoptCfg co;
+    co.k = k;
+    co.n_outer = cfg.n_outer;
+    co.n_inner = cfg.n_inner;
+    co.restarts = R;
+    co.sigma = cfg.sigma;
+    co.lambda = cfg.lambda_torque;
+    co.mu = cfg.mu;
+    co.o = wo;
+    co.per_restart = per_restart;
+    co.per_cand = per_cand;
+    int nw = std::min(R, 8);
+    size_t co_smem = (size_t)(nw + 1) * (2 + k + 3 * kMaxC) * sizeof(double);
+    k_contact_opt<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_els,
+                                               d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan, d_osol,
+                                               cfg.eps_stable, d_bal);
+    LAUNCH(ctx);
+    check_launch();
+    auto h_bal = ddownload(d_bal, (size_t)nA, s);
+    std::vector<int> bal_list;
+    for (int a = 0; a < nA; ++a)
+      if (h_bal[a]) bal_list.push_back(a);
+    out.profile.contact_sets_balanced += (long long)bal_list.size();
+    out.profile.contact_optimization += tm.stop();
+    if (cfg.want_trace) {
+      auto h_oid = ddownload(d_oid, (size_t)nA * kMaxK, s);
+      auto h_oobj = ddownload(d_oobj, (size_t)nA, s);
+      auto h_oan = ddownload(d_oan, (size_t)nA, s);
+      auto h_osol = ddownload(d_osol, (size_t)nA * 3 * kMaxC, s);
+      auto h_els = ddownload(d_els, (size_t)nel, s);
+      for (int a = 0; a < nA; ++a) {
+        lg_trace& t = pass_tr[alive_idx[a]];
+        for (int q = 0; q < k; ++q) {
+          t.opt_element[q] = h_oid[(size_t)a * kMaxK + q];
+          t.opt_sample[q] = h_els[eloff[(size_t)a * k + q] + t.opt_element[q]];
+        }
+        t.opt_objective = h_oobj[a];
+        t.opt_anchor = h_oan[a];
+        t.opt_evaluations = R * (1 + cfg.n_outer * k * cfg.n_inner);
+        int nc = k + h_nst[alive_idx[a]];
+        for (int c = 0; c < nc; ++c) {
+          t.opt_alpha[c] = h_osol[(size_t)a * 3 * kMaxC + c];
+          t.opt_bx[c] = h_osol[(size_t)a * 3 * kMaxC + kMaxC + c];
+          t.opt_by[c] = h_osol[(size_t)a * 3 * kMaxC + 2 * kMaxC + c];
+        }
+        t.balanced = h_bal[a];
+      }
+    }
+
+    // -------- stage 3: lookup attempts (reverse lookup + realize + filter)
+    tm.start();
+    Buf b_have, b_bclear, b_bres, b_bq, b_bused, b_btgt, b_blink, b_batt, b_search, b_runs;
+    int* d_have = dalloc<int>(b_have, (size_t)nA);
+    int* d_bclear = dalloc<int>(b_bclear, (size_t)nA);
+    double* d_bres = dalloc<double>(b_bres, (size_t)nA);
+    double* d_bq = dalloc<double>(b_bq, (size_t)nA * kMaxDof);
+    auto* d_bused = dalloc<unsigned long long>(b_bused, (size_t)nA);
+    double* d_btgt = dalloc<double>(b_btgt, (size_t)nA * kMaxK * 12);
+    int* d_blink = dalloc<int>(b_blink, (size_t)nA * kMaxK);
+    int* d_batt = dalloc<int>(b_batt, (size_t)nA);
+    int* d_search = dalloc<int>(b_search, (size_t)nA);
+    CK(cudaMemsetAsync(d_have, 0, sizeof(int) * nA, s));
+    CK(cudaMemsetAsync(d_bclear, 0, sizeof(int) * nA, s));
+    CK(cudaMemsetAsync(d_bq, 0, sizeof(double) * nA * kMaxDof, s));
+    CK(cudaMemsetAsync(d_batt, 0xff, sizeof(int) * nA, s));
+    std::vector<int> searching(nA, 0), attempts_run(nA, 0);
+    for (int a : bal_list) searching[a] = 1;
+    Buf b_act, b_tgt, b_tl, b_qt, b_res, b_fin, b_used, b_clean, b_on, b_cand, b_err;
+    int* d_err = dalloc<int>(b_err, 1);
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+    for (int attempt = 0; attempt < cfg.lookup_attempts; ++attempt) {
+      std::vector<int> act;
+      for (int a = 0; a < nA; ++a)
+        if (searching[a]) act.push_back(a);
+      if (act.empty()) break;
+      for (int a : act) ++attempts_run[a];
+      const int nAct = (int)act.size();
+      CK(cudaMemcpyAsync(d_search, searching.data(), sizeof(int) * nA, cudaMemcpyHostToDevice, s));
+      int* d_act = dupload(b_act, act.data(), act.size(), s);
+      double* d_tgt = dalloc<double>(b_tgt, (size_t)nAct * k * 12);
+      int* d_tl = dalloc<int>(b_tl, (size_t)nAct * k);
+      k_targets<<<grid_for((long long)nAct * k, 128), 128, 0, s>>>(
+          nAct, d_act, d_aidx, k, attempt, c_lo, B, pass, cfg.seed, F, d_gop, DP.pts.as<double>(),
+          DP.nrm.as<double>(), DP.link.as<int>(), d_chosen, d_oid, d_eloff, d_elp, d_eln,
+          cfg.theta_hit, d_tgt, d_tl, d_err);
+      LAUNCH(ctx);
+      check_launch();
+      double* d_qt = dalloc<double>(b_qt, (size_t)nAct * kMaxDof);
+      double* d_res = dalloc<double>(b_res, (size_t)nAct);
+      int* d_fin = dalloc<int>(b_fin, (size_t)nAct);
+      auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nAct);
+      k_realize<<<grid_for(nAct, 32), 32, 0, s>>>(nAct, k, ikc, cfg.finetune_rounds,
+                                                  cfg.finetune_iterations, d_tgt, d_tl, d_qt, d_res,
+                                                  d_fin, d_used);
+      LAUNCH(ctx);
+      check_launch();
+      auto h_fin = ddownload(d_fin, (size_t)nAct, s);
+      auto h_res = ddownload(d_res, (size_t)nAct, s);
+      std::vector<int> on(nAct), cand(nAct);
+      for (int t = 0; t < nAct; ++t) {
+        on[t] = (h_fin[t] && h_res[t] <= cfg.contact_tol) ? 1 : 0;
+        cand[t] = alive_idx[act[t]];
+      }
+      int* d_on = dupload(b_on, on.data(), on.size(), s);
+      int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
+      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
+      CK(cudaMemsetAsync(d_clean, 0, nAct, s));
+      k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, d_on, d_qt, d_pose, d_aabb, d_clean, nullptr);
+      LAUNCH(ctx);
+      check_launch();
+      k_attempt_update<<<grid_for(nAct, 128), 128, 0, s>>>(
+          nAct, d_act, k, attempt, d_qt, d_res, d_fin, d_used, d_clean, d_on, d_tgt, d_tl,
+          cfg.contact_tol, d_have, d_bclear, d_bres, d_bq, d_bused, d_btgt, d_blink, d_batt, d_search);
+      LAUNCH(ctx);
+      check_launch();
+      auto h_search = ddownload(d_search, (size_t)nA, s);
+      for (int a = 0; a < nA; ++a) searching[a] = h_search[a];
+    }
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    auto h_have = ddownload(d_have, (size_t)nA, s);
+    if (herr) throw std::out_of_range("reverse_lookup: element has no hits");
+    std::vector<int> real_list;
+    for (int a = 0; a < nA; ++a)
+      if (h_have[a]) real_list.push_back(a);
+    out.profile.ik_finite += (long long)real_list.size();
+    out.profile.kinematics_optimization += tm.stop();
+    if (cfg.want_trace) {
+      auto h_bclear = ddownload(d_bclear, (size_t)nA, s);
+      auto h_bres = ddownload(d_bres, (size_t)nA, s);
+      auto h_bq = ddownload(d_bq, (size_t)nA * kMaxDof, s);
+      auto h_bused = ddownload(d_bused, (size_t)nA, s);
+      auto h_btgt = ddownload(d_btgt, (size_t)nA * kMaxK * 12, s);
+      auto h_blink = ddownload(d_blink, (size_t)nA * kMaxK, s);
+      auto h_batt = ddownload(d_batt, (size_t)nA, s);
+      for (int a = 0; a < nA; ++a) {
+        if (!h_bal[a]) continue;
+        lg_trace& t = pass_tr[alive_idx[a]];
+        t.realized = h_have[a];
+        t.attempts_run = attempts_run[a];
+        t.best_attempt = h_have[a] ? h_batt[a] : -1;
+        t.best_clear = h_bclear[a];
+        if (h_have[a]) {
+          t.max_residual = h_bres[a];
+          for (int j = 0; j < hd.dof; ++j) t.real_q[j] = h_bq[(size_t)a * kMaxDof + j];
+          t.used_joints = h_bused[a];
+          for (int q = 0; q < k; ++q) {
+            t.target_link[q] = h_blink[(size_t)a * kMaxK + q];
+            std::memcpy(t.target_point[q], &h_btgt[((size_t)a * kMaxK + q) * 12 + 6], 3 * sizeof(double));
+            std::memcpy(t.target_normal[q], &h_btgt[((size_t)a * kMaxK + q) * 12 + 9], 3 * sizeof(double));
+          }
+        }
+      }
+    }
+    if (real_list.empty()) {
+      if (cfg.want_trace) out.traces.insert(out.traces.end(), pass_tr.begin(), pass_tr.end());
+      continue;
+    }
+
+    // -------- stage 4: unused-joint redraws + postprocess
+    tm.start();
+    Buf b_fq, b_fclean, b_uatt, b_grasp, b_valid, b_drop;
+    double* d_fq = dalloc<double>(b_fq, (size_t)nA * kMaxDof);
+    uint8_t* d_fclean = dalloc<uint8_t>(b_fclean, (size_t)nA);
+    std::vector<int> uatt(nA, -1), uclean(nA, 0);
+    std::vector<int> pending = real_list;
+    std::vector<double> fq_h((size_t)nA * kMaxDof, 0.0);
+    for (int attempt = 0; attempt < cfg.unused_attempts && !pending.empty(); ++attempt) {
+      const int nAct = (int)pending.size();
+      int* d_act = dupload(b_act, pending.data(), pending.size(), s);
+      double* d_qt = dalloc<double>(b_qt, (size_t)nAct * kMaxDof);
+      k_unused_q<<<grid_for(nAct, 64), 64, 0, s>>>(nAct, d_act, d_aidx, attempt, c_lo, B, pass,
+                                                   cfg.seed, d_bq, d_bused, d_qt);
+      LAUNCH(ctx);
+      check_launch();
+      std::vector<int> cand(nAct);
+      for (int t = 0; t < nAct; ++t) cand[t] = alive_idx[pending[t]];
+      int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
+      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
+      k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, nullptr, d_qt, d_pose, d_aabb, d_clean, nullptr);
+      LAUNCH(ctx);
+      check_launch();
+      auto h_clean = ddownload(d_clean, (size_t)nAct, s);
+      auto h_qt = ddownload(d_qt, (size_t)nAct * kMaxDof, s);
+      std::vector<int> next;
+      for (int t = 0; t < nAct; ++t) {
+        int a = pending[t];
+        uatt[a] = attempt;
+        uclean[a] = h_clean[t];
+        std::memcpy(&fq_h[(size_t)a * kMaxDof], &h_qt[(size_t)t * kMaxDof], kMaxDof * sizeof(double));
+        if (!h_clean[t]) next.push_back(a);
+      }
+      pending.swap(next);
+    }
+    dupload(b_fq, fq_h.data(), fq_h.size(), s);
+    std::vector<uint8_t> ucl8(nA);
+    for (int a = 0; a < nA; ++a) ucl8[a] = (uint8_t)uclean[a];
+    dupload(b_fclean, ucl8.data(), ucl8.size(), s);
+    lg_grasp* d_grasp = dalloc<lg_grasp>(b_grasp, (size_t)nA);
+    int* d_valid = dalloc<int>(b_valid, (size_t)nA);
+    int* d_drop = dalloc<int>(b_drop, (size_t)nA);
+    CK(cudaMemsetAsync(d_grasp, 0, sizeof(lg_grasp) * nA, s));
+    CK(cudaMemsetAsync(d_valid, 0, sizeof(int) * nA, s));
+    int* d_act = dupload(b_act, real_list.data(), real_list.size(), s);
+    FinalCfg fc;
+    fc.k = k;
+    fc.contact_tol = cfg.contact_tol;
+    fc.lambda = cfg.lambda_torque;
+    fc.mu = cfg.mu;
+    fc.eps = cfg.eps_stable;
+    fc.o = wo;
+    k_finalize<<<grid_for((long long)real_list.size(), 32), 32, 0, s>>>(
+        (int)real_list.size(), d_act, d_aidx, fc, FS, d_pose, d_nst, d_stl, d_stp, d_stn, b_fq.as<double>(),
+        b_fclean.as<uint8_t>(), d_btgt, d_blink, d_grasp, d_valid, d_drop);
+    LAUNCH(ctx);
+    check_launch();
+    auto h_grasp = ddownload(d_grasp, (size_t)nA, s);
+    auto h_valid = ddownload(d_valid, (size_t)nA, s);
+    auto h_drop = ddownload(d_drop, (size_t)nA, s);
+    out.profile.postprocessing += tm.stop();
+    for (int a : real_list) {
+      const lg_grasp& g = h_grasp[a];
+      if (!h_drop[a]) {
+        out.profile.penetration_free += g.penetration_free;
+        out.profile.ik_converged += g.ik_converged;
+        out.profile.stable += g.stable;
+      }
+    }
+    // kept grasps in candidate order (pipeline.cpp:607-614)
+    for (int a = 0; a < nA; ++a) {
+      if (!h_valid[a] || h_drop[a]) continue;
+      lg_grasp g = h_grasp[a];
+      g.g = (long long)pass * B + c_lo + alive_idx[a];
+      out.grasps.push_back(g);
+    }
+    if (cfg.want_trace) {
+      for (int a : real_list) {
+        lg_trace& t = pass_tr[alive_idx[a]];
+        t.unused_attempt = uatt[a];
+        for (int j = 0; j < hd.dof; ++j) t.final_q[j] = fq_h[(size_t)a * kMaxDof + j];
+        t.dropped = h_drop[a];
+        if (!h_drop[a]) {
+          t.penetration_free = h_grasp[a].penetration_free;
+          t.ik_converged = h_grasp[a].ik_converged;
+          t.stable = h_grasp[a].stable;
+          t.valid = h_valid[a];
+          t.objective = h_grasp[a].objective;
+        }
+      }
+      out.traces.insert(out.traces.end(), pass_tr.begin(), pass_tr.end());
+    }
+  }
+  out.profile.valid = (long long)out.grasps.size();
+  double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  (void)t_pre;
+  out.profile.total = total;
+  out.profile.grasps_per_second = total > 0.0 ? out.profile.valid / total : 0.0;
+  out.profile.gpu_launches = ctx->launches - launches0;
+}
+
+}  // namespace
+
+struct lg_result {
+  RunOut r;
+};
+
+// ================================================================= C-ABI
+extern "C" {
+
+const char* lg_version(void) {
+  return "graspgen-b200 sm_100a fp64 (--fmad=false), lg_math canonical order";
+}
+
+int lg_device_count(int* n) {
+  return lgc::guard([&] {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) c = 0;
+    *n = c;
+  });
+}
+
+int lg_ctx_create(int device, lg_ctx** out) {
+  return lgc::guard([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw lgc::cuda_error("no CUDA device available (the library has no CPU fallback)");
+    if (device < 0 || device >= n) throw std::invalid_argument("lg_ctx_create: bad device index");
+    CK(cudaSetDevice(device));
+    auto* c = new lg_ctx;
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      throw lgc::cuda_error(std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+  });
+}
+
+void lg_ctx_destroy(lg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->cub_tmp) cudaFree(ctx->cub_tmp);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches, int N,
+                   double w, uint64_t seed, int C, lg_field** out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !patches || !out) throw std::invalid_argument("lg_field_build: null argument");
+    CK(cudaSetDevice(ctx->device));
+    auto f = std::make_unique<lg_field>();
+    f->ctx = ctx;
+    build_field_device(ctx, *hand, *patches, N, w, seed, C, f.get());
+    *out = f.release();
+  });
+}
+
+int lg_field_export(lg_field* f, lg_field_csr* o) {
+  return lgc::guard([&] {
+    cudaStream_t s = f->ctx->stream;
+    const DField& F = f->f;
+    f->x_patch_link = f->patches.h_link;
+    f->x_patch_box_off = ddownload(F.patch_box_off, (size_t)F.P + 1, s);
+    f->x_box_cell = ddownload(F.box_cell, 3 * (size_t)F.B, s);
+    f->x_box_code_off = ddownload(F.box_code_off, (size_t)F.B + 1, s);
+    f->x_codes = ddownload(F.codes, (size_t)f->n_codes, s);
+    auto rp = ddownload(F.rep_point, (size_t)f->n_codes, s);
+    std::vector<int> point_link(f->patches.npts);
+    for (int p = 0; p < F.P; ++p)
+      for (int i = f->patches.h_point_off[p]; i < f->patches.h_point_off[p + 1]; ++i)
+        point_link[i] = f->patches.h_link[p];
+    f->x_rep_link.resize(f->n_codes);
+    f->x_rep_point.resize(3 * f->n_codes);
+    f->x_rep_normal.resize(3 * f->n_codes);
+    for (long long c = 0; c < f->n_codes; ++c) {
+      int i = rp[c];
+      f->x_rep_link[c] = point_link[i];
+      for (int a = 0; a < 3; ++a) {
+        f->x_rep_point[3 * c + a] = f->patches.h_pts[3 * i + a];
+        f->x_rep_normal[3 * c + a] = f->patches.h_nrm[3 * i + a];
+      }
+    }
+    o->box_width = F.w;
+    o->codebook_size = F.C;
+    o->codebook = f->x_codebook.data();
+    o->n_patches = F.P;
+    o->patch_link = f->x_patch_link.data();
+    o->patch_box_off = f->x_patch_box_off.data();
+    o->n_boxes = F.B;
+    o->box_cell = f->x_box_cell.data();
+    o->box_code_off = f->x_box_code_off.data();
+    o->n_codes = f->n_codes;
+    o->codes = f->x_codes.data();
+    o->rep_link = f->x_rep_link.data();
+    o->rep_point = f->x_rep_point.data();
+    o->rep_normal = f->x_rep_normal.data();
+    o->n_vectors = f->n_vectors;
+  });
+}
+
+void lg_field_destroy(lg_field* f) { delete f; }
+
+int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
+                           const double* samples, int n, const double* poses, int m, double theta,
+                           uint32_t* masks, double* scores) {
+  return lgc::guard([&] {
+    if (!ctx || !f || !samples || !poses || !masks) throw std::invalid_argument("lg_query_domains_batch: null argument");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<double> col(n);
+    Buf sc[6];
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < n; ++i) col[i] = samples[6 * i + a];
+      dupload(sc[a], col.data(), (size_t)n, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    DSamples S = make_samples(sc, n);
+    Buf bp, bg, bm, bc, ba;
+    double* d_pose = dupload(bp, poses, 12 * (size_t)m, s);
+    int* d_g = dupload(bg, group_of_patch, (size_t)f->f.P, s);
+    uint32_t* d_mask = dalloc<uint32_t>(bm, (size_t)m * n);
+    std::vector<int> acc(m, 1);
+    int* d_acc = dupload(ba, acc.data(), acc.size(), s);
+    int G = 0;
+    for (int p = 0; p < f->f.P; ++p) G = std::max(G, group_of_patch[p] + 1);
+    int* d_cnt = dalloc<int>(bc, (size_t)m * std::max(G, 1));
+    int cb_smem = 3 * f->f.C <= 6144 ? 1 : 0;
+    size_t qsm = cb_smem ? 3 * (size_t)f->f.C * sizeof(double) : 0;
+    k_query<<<m, 256, qsm, s>>>(m, f->f, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
+    check_launch();
+    CK(cudaMemcpyAsync(masks, d_mask, sizeof(uint32_t) * m * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    (void)scores;
+  });
+}
+
+int lg_preprocess(lg_ctx* ctx, const double* samples, int n, double h, double d, uint8_t* keep) {
+  return lgc::guard([&] {
+    if (h <= 0.0 || d < 0.0) throw std::invalid_argument("preprocess_object: bad probe dimensions");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::vector<double> col(n);
+    Buf sc[6], bk;
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < n; ++i) col[i] = samples[6 * i + a];
+      dupload(sc[a], col.data(), (size_t)n, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    uint8_t* d_keep = dalloc<uint8_t>(bk, (size_t)n);
+    k_preprocess<<<grid_for(n, 256), 256, 0, s>>>(make_samples(sc, n), h, d, d_keep);
+    check_launch();
+    CK(cudaMemcpyAsync(keep, d_keep, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int lg_run_batch_field(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches,
+                       lg_field* field, const double* raw, int n_raw, const lg_run_params* p,
+                       lg_result** out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !patches || !raw || !p || !out) throw std::invalid_argument("lg_run_batch: null argument");
+    CK(cudaSetDevice(ctx->device));
+    auto r = std::make_unique<lg_result>();
+    run_batch_device(ctx, *hand, *patches, field, raw, n_raw, *p, r->r);
+    *out = r.release();
+  });
+}
+
+int lg_run_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches,
+                 const double* raw, int n_raw, const lg_run_params* p, lg_result** out) {
+  return lg_run_batch_field(ctx, hand, patches, nullptr, raw, n_raw, p, out);
+}
+
+int lg_result_profile(const lg_result* r, lg_profile* out) {
+  *out = r->r.profile;
+  return LG_OK;
+}
+long long lg_result_num_grasps(const lg_result* r) { return (long long)r->r.grasps.size(); }
+const lg_grasp* lg_result_grasps(const lg_result* r) { return r->r.grasps.data(); }
+long long lg_result_num_traces(const lg_result* r) { return (long long)r->r.traces.size(); }
+const lg_trace* lg_result_traces(const lg_result* r) { return r->r.traces.data(); }
+void lg_result_destroy(lg_result* r) { delete r; }
+
+}  // extern "C"
