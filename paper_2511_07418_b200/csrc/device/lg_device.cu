@@ -1050,6 +1050,205 @@ struct lg_result {
   RunOut r;
 };
 
+namespace {
+
+// Stage-level batch kernels for the parity harness.
+__global__ void k_wrench_batch(int m, const int* n, const double* pts, const double* nrm,
+                               double lambda, double mu, int mode, WOpts o, double* obj,
+                               int* anchor, double* sol) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  WProb w;
+  w.n = n[t];
+  w.lambda = lambda;
+  w.mu = mode ? mu : 0.0;  // solve_gswo with mu == 0 is solve_fswo
+  for (int c = 0; c < w.n; ++c)
+    wprob_set(w, c, v3_load(pts + (size_t)t * 18 + 3 * c), v3_load(nrm + (size_t)t * 18 + 3 * c));
+  WState s;
+  int an = -1;
+  double v = wsolve(w, o, nullptr, &an, s);
+  obj[t] = v;
+  anchor[t] = an;
+  for (int c = 0; c < kMaxC; ++c) {
+    sol[(size_t)t * 18 + c] = s.a[c];
+    sol[(size_t)t * 18 + 6 + c] = s.bx[c];
+    sol[(size_t)t * 18 + 12 + c] = s.by[c];
+  }
+}
+
+__global__ void k_realize_var(int m, const int* kk, IkCfg P, int rounds, int fine_iters,
+                              const double* tgt, const int* tl, double* q_out, double* max_res,
+                              int* finite, unsigned long long* used) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  int k = kk[t];
+  Target T[kMaxK];
+  load_targets(tgt + (size_t)t * kMaxK * 12, tl + t * kMaxK, k, T);
+  double q[kMaxDof];
+  for (int j = 0; j < c_hand.dof; ++j) q[j] = q_out[(size_t)t * kMaxDof + j];
+  double mr;
+  unsigned long long u;
+  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u);
+  for (int j = 0; j < c_hand.dof; ++j) q_out[(size_t)t * kMaxDof + j] = q[j];
+  max_res[t] = mr;
+  finite[t] = fin ? 1 : 0;
+  used[t] = u;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points,
+                          const double* normals, double lambda, double mu, int mode,
+                          int iterations, int warm_iterations, double step, int max_backtracks,
+                          double* objective, int* anchor, double* alpha, double* beta_x,
+                          double* beta_y) {
+  return lgc::guard([&] {
+    if (!ctx || m < 0) throw std::invalid_argument("lg_wrench_solve_batch: bad argument");
+    for (int i = 0; i < m; ++i)
+      if (n[i] < 1 || n[i] > kMaxC) throw std::invalid_argument("wrench solve: 1..6 contacts");
+    if (m == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    Buf bn, bp, bq, bo, ba, bs;
+    int* d_n = dupload(bn, n, (size_t)m, s);
+    double* d_p = dupload(bp, points, (size_t)m * 18, s);
+    double* d_q = dupload(bq, normals, (size_t)m * 18, s);
+    double* d_o = dalloc<double>(bo, (size_t)m);
+    int* d_a = dalloc<int>(ba, (size_t)m);
+    double* d_s = dalloc<double>(bs, (size_t)m * 18);
+    WOpts o;
+    o.iterations = iterations;
+    o.warm_iterations = warm_iterations;
+    o.step = step;
+    o.max_bt = max_backtracks;
+    k_wrench_batch<<<grid_for(m, 64), 64, 0, s>>>(m, d_n, d_p, d_q, lambda, mu, mode, o, d_o, d_a, d_s);
+    check_launch();
+    auto h_s = ddownload(d_s, (size_t)m * 18, s);
+    CK(cudaMemcpy(objective, d_o, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(anchor, d_a, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i)
+      for (int c = 0; c < kMaxC; ++c) {
+        alpha[6 * i + c] = h_s[18 * i + c];
+        beta_x[6 * i + c] = h_s[18 * i + 6 + c];
+        beta_y[6 * i + c] = h_s[18 * i + 12 + c];
+      }
+  });
+}
+
+int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const double* q,
+                       const double* poses, const double* samples, int n, double margin,
+                       uint8_t* clean, double* max_penetration) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || m < 0) throw std::invalid_argument("lg_collision_batch: bad argument");
+    if (margin < 0.0) throw std::invalid_argument("broad_phase: negative margin");
+    if (m == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    std::vector<double> col(std::max(n, 1));
+    Buf sc[6];
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < n; ++i) col[i] = samples[6 * i + a];
+      dupload(sc[a], col.data(), (size_t)std::max(n, 1), s);
+      CK(cudaStreamSynchronize(s));
+    }
+    DSamples S = make_samples(sc, n);
+    std::vector<double> qp((size_t)m * kMaxDof, 0.0);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < hand->dof; ++j) qp[(size_t)i * kMaxDof + j] = q[(size_t)i * hand->dof + j];
+    std::vector<int> ids(m), acc(m, 1);
+    for (int i = 0; i < m; ++i) ids[i] = i;
+    Buf bq, bp, bi, ba, bb, bc, bm;
+    double* d_q = dupload(bq, qp.data(), qp.size(), s);
+    double* d_p = dupload(bp, poses, (size_t)m * 12, s);
+    int* d_i = dupload(bi, ids.data(), ids.size(), s);
+    int* d_a = dupload(ba, acc.data(), acc.size(), s);
+    double* d_b = dalloc<double>(bb, (size_t)m * 6);
+    uint8_t* d_c = dalloc<uint8_t>(bc, (size_t)m);
+    double* d_m = dalloc<double>(bm, (size_t)m);
+    if (n > 0) {
+      k_obj_aabb<<<m, 256, 0, s>>>(m, S, d_p, d_a, d_b);
+      check_launch();
+    }
+    CollCfg cc;
+    cc.margin = margin;
+    cc.raw = S;
+    cc.part_link = ctx->h_part_link.as<int>();
+    k_collision<<<m, 128, 0, s>>>(m, cc, d_i, nullptr, d_q, d_p, d_b, d_c, d_m);
+    check_launch();
+    CK(cudaMemcpyAsync(clean, d_c, (size_t)m, cudaMemcpyDeviceToHost, s));
+    if (max_penetration)
+      CK(cudaMemcpyAsync(max_penetration, d_m, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                     const double* object_points, const double* object_normals, const int* links,
+                     const double* hand_points, const double* hand_normals, double beta,
+                     int iterations, double step_clamp, double residual_tol, double damping_scale,
+                     int finetune_rounds, int finetune_iterations, double* q, double* max_residual,
+                     int* finite, unsigned long long* used_joints) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || m < 0) throw std::invalid_argument("lg_realize_batch: bad argument");
+    if (beta <= 0.0) throw std::invalid_argument("solve_contact_ik: beta must be > 0");
+    if (m == 0) return;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    std::vector<double> tg((size_t)m * kMaxK * 12, 0.0);
+    std::vector<int> tl((size_t)m * kMaxK, 0);
+    size_t off = 0;
+    for (int i = 0; i < m; ++i) {
+      if (k[i] < 1 || k[i] > kMaxK) throw std::invalid_argument("realize_grasp: 1..5 targets");
+      for (int c = 0; c < k[i]; ++c, ++off) {
+        if (links[off] < 0 || links[off] >= hand->n_links)
+          throw std::invalid_argument("solve_contact_ik: invalid target link");
+        double* T = &tg[((size_t)i * kMaxK + c) * 12];
+        for (int a = 0; a < 3; ++a) {
+          T[a] = object_points[3 * off + a];
+          T[3 + a] = object_normals[3 * off + a];
+          T[6 + a] = hand_points[3 * off + a];
+          T[9 + a] = hand_normals[3 * off + a];
+        }
+        tl[(size_t)i * kMaxK + c] = links[off];
+      }
+    }
+    std::vector<double> q0((size_t)m * kMaxDof, 0.0);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < hand->dof; ++j) q0[(size_t)i * kMaxDof + j] = q[(size_t)i * hand->dof + j];
+    Buf bk, bt, bl, bq, br, bf, bu;
+    int* d_k = dupload(bk, k, (size_t)m, s);
+    double* d_t = dupload(bt, tg.data(), tg.size(), s);
+    int* d_l = dupload(bl, tl.data(), tl.size(), s);
+    double* d_q = dupload(bq, q0.data(), q0.size(), s);
+    double* d_r = dalloc<double>(br, (size_t)m);
+    int* d_f = dalloc<int>(bf, (size_t)m);
+    auto* d_u = dalloc<unsigned long long>(bu, (size_t)m);
+    IkCfg P;
+    P.beta = beta;
+    P.step_clamp = step_clamp;
+    P.residual_tol = residual_tol;
+    P.damping_scale = damping_scale;
+    P.damping_min = 1e-6;
+    P.iterations = iterations;
+    P.max_backtracks = 10;
+    k_realize_var<<<grid_for(m, 32), 32, 0, s>>>(m, d_k, P, finetune_rounds, finetune_iterations, d_t,
+                                                 d_l, d_q, d_r, d_f, d_u);
+    check_launch();
+    auto hq = ddownload(d_q, q0.size(), s);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < hand->dof; ++j) q[(size_t)i * hand->dof + j] = hq[(size_t)i * kMaxDof + j];
+    CK(cudaMemcpy(max_residual, d_r, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(finite, d_f, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(used_joints, d_u, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
+
 // ================================================================= C-ABI
 extern "C" {
 
