@@ -106,6 +106,21 @@ void orc_libm(int which, int n, const double* x, const double* y, double* out) {
   }
 }
 
+// random_problem of test_wrench.cpp:13-25 (fixture generator): points on a
+// 5 cm sphere, roughly inward unit normals.
+void orc_random_wrench_problem(uint64_t seed, int n, double* pts, double* nrm) {
+  Rng rng(seed);
+  for (int i = 0; i < n; ++i) {
+    V3 p = scale(0.05, rng.uniform_unit_vector());
+    // Vec3(normal(), normal(), normal()): argument evaluation order is
+    // unspecified in C++; g++ on x86-64 evaluates right to left.
+    double c = rng.normal(), b = rng.normal(), a = rng.normal();
+    V3 nin = normalized(add(neg(p), scale(0.3, v3(a, b, c))));
+    v3_store(pts + 3 * i, p);
+    v3_store(nrm + 3 * i, nin);
+  }
+}
+
 int orc_tangent_basis(const double* n, double* x, double* y) {
   return guard([&] {
     V3 a, b;

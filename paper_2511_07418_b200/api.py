@@ -483,3 +483,91 @@ def prepare_inputs(params):
         mesh.scale(params.object_scale)
     raw = sample_surface(mesh, params.samples_per_cm2, mix_seed(params.seed, TAG_OBJECT_SAMPLES))
     return hand, patches, raw, mesh
+
+
+def _bind_batch_sigs():
+    L = lib()
+    if getattr(L, "_batch_bound", False):
+        return L
+    P = C.POINTER
+    L.lg_wrench_solve_batch.restype = C.c_int
+    L.lg_wrench_solve_batch.argtypes = [C.c_void_p, C.c_int, A.ip, A.dp, A.dp, C.c_double,
+                                        C.c_double, C.c_int, C.c_int, C.c_int, C.c_double,
+                                        C.c_int, A.dp, A.ip, A.dp, A.dp, A.dp]
+    L.lg_collision_batch.restype = C.c_int
+    L.lg_collision_batch.argtypes = [C.c_void_p, P(A.HandDesc), C.c_int, A.dp, A.dp, A.dp,
+                                     C.c_int, C.c_double, P(C.c_uint8), A.dp]
+    L.lg_realize_batch.restype = C.c_int
+    L.lg_realize_batch.argtypes = [C.c_void_p, P(A.HandDesc), C.c_int, A.ip, A.dp, A.dp, A.ip,
+                                   A.dp, A.dp, C.c_double, C.c_int, C.c_double, C.c_double,
+                                   C.c_double, C.c_int, C.c_int, A.dp, A.dp, A.ip,
+                                   P(C.c_ulonglong)]
+    L._batch_bound = True
+    return L
+
+
+def wrench_solve_batch(ctx, problems, lambda_torque=10.0, mu=0.0, gswo=None, iterations=64,
+                       warm_iterations=8, step=0.1, max_backtracks=20):
+    """Batched solve_fswo / solve_gswo (wrench.cpp:391-402), cold start.
+    problems: list of (points (n,3), inward normals (n,3)), n <= 6."""
+    L = _bind_batch_sigs()
+    m = len(problems)
+    n = np.array([len(p[0]) for p in problems], dtype=np.int32)
+    pts = np.zeros((m, 6, 3))
+    nrm = np.zeros((m, 6, 3))
+    for i, (p, q) in enumerate(problems):
+        pts[i, :len(p)] = p
+        nrm[i, :len(q)] = q
+    mode = (1 if mu > 0 else 0) if gswo is None else int(gswo)
+    obj = np.zeros(m)
+    anchor = np.zeros(m, dtype=np.int32)
+    al, bx, by = np.zeros((m, 6)), np.zeros((m, 6)), np.zeros((m, 6))
+    check(L.lg_wrench_solve_batch(lib_ctx(ctx), m, _ip(n), _dp(pts), _dp(nrm),
+                                  float(lambda_torque), float(mu), mode, int(iterations),
+                                  int(warm_iterations), float(step), int(max_backtracks),
+                                  _dp(obj), _ip(anchor), _dp(al), _dp(bx), _dp(by)))
+    return obj, anchor, al, bx, by
+
+
+def lib_ctx(ctx):
+    return ctx._h
+
+
+def collision_batch(ctx, hand, q, poses, samples, margin=0.002):
+    """Batched validate_grasp_collisions (collision.cpp:230-288) -> (clean, max depth)."""
+    L = _bind_batch_sigs()
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, hand.dof)
+    p = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 12)
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    m = len(q)
+    clean = np.zeros(m, dtype=np.uint8)
+    mp = np.zeros(m)
+    check(L.lg_collision_batch(ctx._h, C.byref(hand.desc), m, _dp(q), _dp(p), _dp(s), len(s),
+                               float(margin), clean.ctypes.data_as(C.POINTER(C.c_uint8)), _dp(mp)))
+    return clean.astype(bool), mp
+
+
+def realize_batch(ctx, hand, q0, problems, beta=0.01, iterations=30, step_clamp=0.2,
+                  residual_tol=1e-4, damping_scale=1e-4, finetune_rounds=4,
+                  finetune_iterations=10):
+    """Batched realize_grasp (pipeline.cpp:185-253).  problems: list of target
+    lists, each target (object_point, inward normal, link, hand point, hand normal)."""
+    L = _bind_batch_sigs()
+    m = len(problems)
+    k = np.array([len(t) for t in problems], dtype=np.int32)
+    flat = [t for ts in problems for t in ts]
+    op = np.ascontiguousarray([t[0] for t in flat], dtype=np.float64).reshape(-1, 3)
+    on = np.ascontiguousarray([t[1] for t in flat], dtype=np.float64).reshape(-1, 3)
+    links = np.ascontiguousarray([t[2] for t in flat], dtype=np.int32)
+    hp = np.ascontiguousarray([t[3] for t in flat], dtype=np.float64).reshape(-1, 3)
+    hn = np.ascontiguousarray([t[4] for t in flat], dtype=np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(np.broadcast_to(q0, (m, hand.dof)), dtype=np.float64).copy()
+    mr = np.zeros(m)
+    fin = np.zeros(m, dtype=np.int32)
+    used = np.zeros(m, dtype=np.uint64)
+    check(L.lg_realize_batch(ctx._h, C.byref(hand.desc), m, _ip(k), _dp(op), _dp(on), _ip(links),
+                             _dp(hp), _dp(hn), float(beta), int(iterations), float(step_clamp),
+                             float(residual_tol), float(damping_scale), int(finetune_rounds),
+                             int(finetune_iterations), _dp(q), _dp(mr), _ip(fin),
+                             used.ctypes.data_as(C.POINTER(C.c_ulonglong))))
+    return q, mr, fin.astype(bool), used
