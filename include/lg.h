@@ -181,6 +181,14 @@ typedef struct lg_profile {
   double grasps_per_second;
   long long patches, boxes, field_vectors, object_samples, field_samples;
   long long gpu_launches;
+  /* B200 extensions: device time of the pass (CUDA events on the library
+   * stream, first kernel to last kernel; input upload and result download
+   * excluded), bytes moved across PCIe, and algorithmic work counters. */
+  double device_seconds;
+  long long h2d_bytes, d2h_bytes;
+  long long ik_iterations, fk_evals, wrench_evals, wrench_grads, proj_evals;
+  long long realize_calls, collision_calls;
+  double realize_seconds, contact_opt_seconds;
 } lg_profile;
 
 /* Per-candidate record of every stage decision, used by the stage parity

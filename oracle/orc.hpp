@@ -323,7 +323,7 @@ struct RunOutput {
 // loaded hand, its decomposed patches and the raw object samples.
 RunOutput run_batch(const Hand& h, const std::vector<Patch>& patches,
                     const std::vector<Sample>& raw, const lg_run_params& cfg,
-                    int workers);
+                    int workers, const FieldIndex* cached = nullptr);
 
 // parallel_for (parallel.hpp:24-56)
 void parallel_for(size_t begin, size_t end, int workers,

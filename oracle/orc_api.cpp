@@ -547,6 +547,25 @@ int orc_run_batch(const lg_hand_desc* hd, const lg_patches_desc* pd, const doubl
     *out = r;
   });
 }
+// run_batch over a prebuilt index (the reference's cache=true mode).
+int orc_run_batch_field(void* fp, const lg_hand_desc* hd, const lg_patches_desc* pd,
+                        const double* raw, int n_raw, const lg_run_params* cfg, int workers,
+                        orc_result** out) {
+  return guard([&] {
+    Hand h = Hand::from_desc(*hd);
+    auto patches = patches_from_desc(*pd);
+    auto s = samples_from(raw, n_raw);
+    auto* r = new orc_result;
+    try {
+      r->out = run_batch(h, patches, s, *cfg, workers, &((OrcField*)fp)->idx);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
 int orc_result_profile(const orc_result* r, lg_profile* p) {
   *p = r->out.profile;
   return LG_OK;

@@ -233,13 +233,17 @@ void v3out(double* d, V3 v) {
 }  // namespace
 
 RunOutput run_batch(const Hand& h, const std::vector<Patch>& patches,
-                    const std::vector<Sample>& raw, const lg_run_params& cfg,
-                    int workers) {  // pipeline.cpp:308-625
+                    const std::vector<Sample>& raw, const lg_run_params& cfg, int workers,
+                    const FieldIndex* cached) {  // pipeline.cpp:308-625
   auto wall0 = Clock::now();
   RunOutput out;
   std::memset(&out.profile, 0, sizeof(out.profile));
-  FieldIndex index = build_field_index(h, patches, cfg.field_configs, cfg.box_width, cfg.seed,
-                                       cfg.codebook_size);
+  // build_field (pipeline.cpp:273-306): build, or reuse a cached index
+  FieldIndex built;
+  if (!cached)
+    built = build_field_index(h, patches, cfg.field_configs, cfg.box_width, cfg.seed,
+                              cfg.codebook_size);
+  const FieldIndex& index = cached ? *cached : built;
   out.profile.field_build = since(wall0);
   auto field = preprocess_object(raw, cfg.probe_half_width, cfg.probe_depth_threshold);
   if (field.empty())

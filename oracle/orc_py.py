@@ -76,6 +76,8 @@ def lib():
                                       C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, dp,
                                       dp, ip, P(C.c_ulonglong)]),
             "orc_run_batch": (C.c_int, [HD, PD, dp, C.c_int, P(A.RunParams), C.c_int, P(vp)]),
+            "orc_run_batch_field": (C.c_int, [vp, HD, PD, dp, C.c_int, P(A.RunParams), C.c_int,
+                                              P(vp)]),
             "orc_result_profile": (C.c_int, [vp, P(A.Profile)]),
             "orc_result_num_grasps": (C.c_longlong, [vp]),
             "orc_result_grasps": (P(A.Grasp), [vp]),
@@ -411,4 +413,13 @@ def run_batch(hand_desc, patches_desc, raw_samples, params, workers=1):
     h = C.c_void_p()
     check(lib().orc_run_batch(C.byref(hand_desc), C.byref(patches_desc), _p(raw), len(raw),
                               C.byref(params), int(workers), C.byref(h)))
+    return OrcResult(h)
+
+
+def run_batch_field(field, hand_desc, patches_desc, raw_samples, params, workers=1):
+    """run_batch with a prebuilt OrcField (the reference's cached-index mode)."""
+    raw = _d(raw_samples).reshape(-1, 6)
+    h = C.c_void_p()
+    check(lib().orc_run_batch_field(field._h, C.byref(hand_desc), C.byref(patches_desc), _p(raw),
+                                    len(raw), C.byref(params), int(workers), C.byref(h)))
     return OrcResult(h)

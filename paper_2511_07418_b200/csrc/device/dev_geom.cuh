@@ -42,6 +42,21 @@ struct DHand {
 
 __constant__ DHand c_hand;
 
+// Algorithmic work counters (per thread in registers, folded into g_cnt with
+// one atomic per thread at kernel exit); feed the roofline's FLOP counts.
+struct Ctr {
+  unsigned long long ik_it, fk, weval, wgrad, proj;
+};
+enum { kCntIk = 0, kCntFk, kCntWeval, kCntWgrad, kCntProj, kCntN };
+__device__ unsigned long long g_cnt[kCntN];
+__device__ __forceinline__ void ctr_flush(const Ctr& c) {
+  if (c.ik_it) atomicAdd(&g_cnt[kCntIk], c.ik_it);
+  if (c.fk) atomicAdd(&g_cnt[kCntFk], c.fk);
+  if (c.weval) atomicAdd(&g_cnt[kCntWeval], c.weval);
+  if (c.wgrad) atomicAdd(&g_cnt[kCntWgrad], c.wgrad);
+  if (c.proj) atomicAdd(&g_cnt[kCntProj], c.proj);
+}
+
 // ------------------------------------------------------------ kinematics
 // forward_kinematics (hand.cpp:275-295)
 __device__ __forceinline__ void fk(const double* q, Xf* frames) {
@@ -500,14 +515,16 @@ __device__ __forceinline__ void wproject(const WProb& w, int anchor, bool fr, WS
 
 // descend (wrench.cpp:124-177)
 __device__ double wdescend(const WProb& w, int anchor, bool fr, int iterations, double step0,
-                           int max_bt, WState& s) {
+                           int max_bt, WState& s, Ctr& ctr) {
   wproject(w, anchor, fr, s);
   double current = weval(w, s);
+  ++ctr.weval;
   double ga[kMaxC], gx[kMaxC], gy[kMaxC];
   WState trial = s;
   for (int it = 0; it < iterations; ++it) {
     V3 force, torque;
     net_wrench(w, s, force, torque);
+    ++ctr.wgrad;
     torque = v3(torque.x * w.lambda, torque.y * w.lambda, torque.z * w.lambda);
 #pragma unroll
     for (int i = 0; i < kMaxC; ++i) {
@@ -537,6 +554,7 @@ __device__ double wdescend(const WProb& w, int anchor, bool fr, int iterations, 
       }
       wproject(w, anchor, fr, trial);
       double next = weval(w, trial);
+      ++ctr.weval;
       if (next <= current) {
         s = trial;
         current = next;
@@ -558,7 +576,8 @@ struct WOpts {
 // One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
 // warm-started; returns the anchor's final objective, state in s.
 __device__ __forceinline__ double wsolve_anchor(const WProb& w, int anchor, bool fr,
-                                                const WOpts& o, const WState* warm, WState& s) {
+                                                const WOpts& o, const WState* warm, WState& s,
+                                                Ctr& ctr) {
   int iters = warm ? o.warm_iterations : o.iterations;
 #pragma unroll
   for (int i = 0; i < kMaxC; ++i) {
@@ -573,22 +592,22 @@ __device__ __forceinline__ double wsolve_anchor(const WProb& w, int anchor, bool
     }
   }
   if (fr) {
-    wdescend(w, anchor, false, iters, o.step, o.max_bt, s);
-    return wdescend(w, anchor, true, iters, o.step, o.max_bt, s);
+    wdescend(w, anchor, false, iters, o.step, o.max_bt, s, ctr);
+    return wdescend(w, anchor, true, iters, o.step, o.max_bt, s, ctr);
   }
-  return wdescend(w, anchor, false, iters, o.step, o.max_bt, s);
+  return wdescend(w, anchor, false, iters, o.step, o.max_bt, s, ctr);
 }
 
 // run_solver (wrench.cpp:323-370) sequentially over anchors in one thread;
 // fr = (mu > 0) is solve() of contact_opt.cpp:37-41 / solve_gswo.
 __device__ double wsolve(const WProb& w, const WOpts& o, const WState* warm, int* anchor_out,
-                         WState& best) {
+                         WState& best, Ctr& ctr) {
   const bool fr = w.mu > 0.0;
   double best_obj = kInf;
   int best_anchor = -1;
   for (int anchor = 0; anchor < w.n; ++anchor) {
     WState s;
-    double value = wsolve_anchor(w, anchor, fr, o, warm, s);
+    double value = wsolve_anchor(w, anchor, fr, o, warm, s, ctr);
     if (value < best_obj) {
       best_obj = value;
       best_anchor = anchor;

@@ -148,7 +148,7 @@ __device__ __forceinline__ bool all_finite(const double* v, int n) {
 
 // solve_contact_ik (ik.cpp:31-139).  q in/out; returns finite.
 __device__ bool ik_solve(double* q, const Target* T, int k, const IkCfg& P, int iterations,
-                         unsigned long long* used) {
+                         unsigned long long* used, Ctr& ctr) {
   const int dof = c_hand.dof;
   const int rows = 6 * k;
   clamp_to_limits(q);
@@ -159,9 +159,11 @@ __device__ bool ik_solve(double* q, const Target* T, int k, const IkCfg& P, int 
   double r[6 * kMaxK], rt[6 * kMaxK];
   double JtJ[kMaxDof * kMaxDof], dq[kMaxDof], qt[kMaxDof], Jp[3 * kMaxDof], cmax[kMaxDof];
   fk(q, fr);
+  ++ctr.fk;
   ik_residual(fr, T, k, P.beta, r);
   double objective = sum_squares(r, rows);
   for (int it = 0; it < iterations; ++it) {
+    ++ctr.ik_it;
     for (int a = 0; a < dof * dof; ++a) JtJ[a] = 0.0;
     for (int a = 0; a < dof; ++a) {
       dq[a] = 0.0;
@@ -199,6 +201,7 @@ __device__ bool ik_solve(double* q, const Target* T, int k, const IkCfg& P, int 
       for (int c = 0; c < dof; ++c) qt[c] = q[c] + dmin(dmax(dq[c], -P.step_clamp), P.step_clamp);
       clamp_to_limits(qt);
       fk(qt, frt);
+      ++ctr.fk;
       ik_residual(frt, T, k, P.beta, rt);
       double obj_try = sum_squares(rt, rows);
       if (obj_try <= objective) {
@@ -224,9 +227,10 @@ __device__ bool ik_solve(double* q, const Target* T, int k, const IkCfg& P, int 
 // the object points to the assigned links' parts at q; optionally refreshes
 // the hand points/normals.
 __device__ double realize_project(const double* q, const Target* T, int k, Target* refreshed,
-                                  double* residuals) {
+                                  double* residuals, Ctr& ctr) {
   Xf fr[kMaxLinks];
   fk(q, fr);
+  ++ctr.fk;
   double worst = 0.0;
   for (int i = 0; i < k; ++i) {
     Xf inv = xf_inverse(fr[T[i].link]);
@@ -244,32 +248,33 @@ __device__ double realize_project(const double* q, const Target* T, int k, Targe
 
 // realize_grasp (pipeline.cpp:185-253) from q0 = q; q out.
 __device__ bool realize_grasp(double* q, const Target* T, int k, const IkCfg& P, int rounds,
-                              int fine_iters, double* max_res, unsigned long long* used_out) {
+                              int fine_iters, double* max_res, unsigned long long* used_out,
+                              Ctr& ctr) {
   const int dof = c_hand.dof;
   double q0[kMaxDof], qs[kMaxDof];
   for (int j = 0; j < dof; ++j) q0[j] = q[j];
   unsigned long long used = 0ull;
   *used_out = 0ull;
-  if (!ik_solve(q, T, k, P, P.iterations, &used)) {
+  if (!ik_solve(q, T, k, P, P.iterations, &used, ctr)) {
     for (int j = 0; j < dof; ++j) q[j] = q0[j];
     *max_res = kInf;
     return false;
   }
-  double worst = realize_project(q, T, k, nullptr, nullptr);
+  double worst = realize_project(q, T, k, nullptr, nullptr, ctr);
   Target ref[kMaxK];
   for (int round = 0; round < rounds; ++round) {
     for (int i = 0; i < k; ++i) ref[i] = T[i];
-    realize_project(q, T, k, ref, nullptr);
+    realize_project(q, T, k, ref, nullptr, ctr);
     for (int j = 0; j < dof; ++j) qs[j] = q[j];
     unsigned long long su = 0ull;
-    if (!ik_solve(qs, ref, k, P, fine_iters, &su)) break;
-    double w2 = realize_project(qs, T, k, nullptr, nullptr);
+    if (!ik_solve(qs, ref, k, P, fine_iters, &su, ctr)) break;
+    double w2 = realize_project(qs, T, k, nullptr, nullptr, ctr);
     if (w2 > worst + 1e-6) break;
     for (int j = 0; j < dof; ++j) q[j] = qs[j];
     worst = w2;
     used |= su;
   }
-  *max_res = realize_project(q, T, k, nullptr, nullptr);
+  *max_res = realize_project(q, T, k, nullptr, nullptr, ctr);
   *used_out = used;
   return all_finite(q, dof);
 }

@@ -412,6 +412,7 @@ __global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const i
     off[q] = el_off[a * k + q];
     cnt[q] = el_off[a * k + q + 1] - off[q];
   }
+  Ctr ctr = {0, 0, 0, 0, 0};
   for (int rbase = 0; rbase < cfg.restarts; rbase += nw) {
     const int r = rbase + warp;
     if (r < cfg.restarts) {
@@ -434,7 +435,7 @@ __global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const i
     {
       WState st;
       double val = kInf;
-      if (lane < n) val = wsolve_anchor(prob, lane, prob.mu > 0.0, cfg.o, nullptr, st);
+      if (lane < n) val = wsolve_anchor(prob, lane, prob.mu > 0.0, cfg.o, nullptr, st, ctr);
       if (!(val < kInf)) val = kInf;  // NaN / inf anchors never win (strict '<')
       double best = val;
       int bl = val < kInf ? lane : 99;
@@ -483,6 +484,7 @@ __global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const i
             const double* P = el_p + 3 * off[q];
             double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
             int bi = 0;
+            ctr.proj += (unsigned long long)cnt[q];
             for (long long e = 1; e < cnt[q]; ++e) {
               double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
               if (d2v < bd) {
@@ -494,7 +496,7 @@ __global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const i
             WProb trial = prob;
             long long e = off[q] + bi;
             wprob_set(trial, q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
-            val = wsolve(trial, cfg.o, anchor >= 0 ? &sol : nullptr, &an, ws);
+            val = wsolve(trial, cfg.o, anchor >= 0 ? &sol : nullptr, &an, ws, ctr);
           }
           // lowest (value, m) among value < best_obj
           double bv = (val < best_obj) ? val : kInf;
@@ -557,6 +559,7 @@ __global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const i
     }
     __syncthreads();
   }
+  ctr_flush(ctr);
   if (threadIdx.x == 0) {
     double* best = s_res + nw * stride;
     out_obj[a] = best[0];
@@ -652,7 +655,9 @@ __global__ void k_realize(int nAct, int k, IkCfg P, int rounds, int fine_iters,
   for (int j = 0; j < c_hand.dof; ++j) q[j] = c_hand.mid[j];
   double mr;
   unsigned long long u;
-  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u);
+  Ctr ctr = {0, 0, 0, 0, 0};
+  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u, ctr);
+  ctr_flush(ctr);
   for (int j = 0; j < c_hand.dof; ++j) q_out[(size_t)t * kMaxDof + j] = q[j];
   max_res[t] = mr;
   finite[t] = fin ? 1 : 0;
@@ -905,7 +910,9 @@ __global__ void k_finalize(int nT, const int* act, const int* alive_idx, FinalCf
   for (int c = 0; c < g.n_contacts; ++c) wprob_set(w, c, v3_load(g.contact_p[c]), v3_load(g.contact_n[c]));
   WState ws;
   int an;
-  double obj = wsolve(w, C.o, nullptr, &an, ws);
+  Ctr ctr = {0, 0, 0, 0, 0};
+  double obj = wsolve(w, C.o, nullptr, &an, ws, ctr);
+  ctr_flush(ctr);
   g.objective = obj;
   g.stable = obj < C.eps ? 1 : 0;
   g.g = 0;

@@ -58,15 +58,20 @@ T* dalloc(Buf& b, size_t count) {
   b.alloc(count * sizeof(T));
   return b.as<T>();
 }
+// PCIe traffic accounting (reported as h2d_bytes / d2h_bytes per run)
+long long g_h2d = 0, g_d2h = 0;
+
 template <typename T>
 T* dupload(Buf& b, const T* src, size_t count, cudaStream_t s) {
   T* d = dalloc<T>(b, count);
   if (count) CK(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  g_h2d += (long long)(count * sizeof(T));
   return d;
 }
 template <typename T>
 std::vector<T> ddownload(const T* src, size_t count, cudaStream_t s) {
   std::vector<T> v(count);
+  g_d2h += (long long)(count * sizeof(T));
   if (count) CK(cudaMemcpyAsync(v.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return v;
@@ -505,9 +510,18 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   cudaStream_t s = ctx->stream;
   std::memset(&out.profile, 0, sizeof(out.profile));
   long long launches0 = ctx->launches;
+  g_h2d = 0;
+  g_d2h = 0;
   if (cfg.k_contacts < 1 || cfg.k_contacts > kMaxK) throw std::invalid_argument("k_contacts out of range");
   if (n_raw < 1) throw std::invalid_argument("place_object: no object samples");
+  {
+    unsigned long long z[kCntN] = {0, 0, 0, 0, 0};
+    CK(cudaMemcpyToSymbolAsync(g_cnt, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+  }
   Timer tm(s);
+  Timer tdev(s);   // device span of the pass after the inputs are resident
+  Timer tk(s);     // per-kernel spans (realize, contact search)
+  double realize_s = 0.0, copt_s = 0.0;
   // ---- field (ContactFieldIndex::build) or reuse
   std::unique_ptr<lg_field> own;
   lg_field* field = field_in;
@@ -538,6 +552,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     CK(cudaStreamSynchronize(s));
   }
   DSamples RS = make_samples(rawc, n_raw);
+  tdev.start();
   Buf keepb;
   uint8_t* d_keep = dalloc<uint8_t>(keepb, (size_t)n_raw);
   if (cfg.probe_half_width <= 0.0 || cfg.probe_depth_threshold < 0.0)
@@ -797,11 +812,13 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     co.per_cand = per_cand;
     int nw = std::min(R, 8);
     size_t co_smem = (size_t)(nw + 1) * (2 + k + 3 * kMaxC) * sizeof(double);
+    tk.start();
     k_contact_opt<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_els,
                                                d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan, d_osol,
                                                cfg.eps_stable, d_bal);
     LAUNCH(ctx);
     check_launch();
+    copt_s += tk.stop();
     auto h_bal = ddownload(d_bal, (size_t)nA, s);
     std::vector<int> bal_list;
     for (int a = 0; a < nA; ++a)
@@ -875,11 +892,14 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       double* d_res = dalloc<double>(b_res, (size_t)nAct);
       int* d_fin = dalloc<int>(b_fin, (size_t)nAct);
       auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nAct);
+      tk.start();
       k_realize<<<grid_for(nAct, 32), 32, 0, s>>>(nAct, k, ikc, cfg.finetune_rounds,
                                                   cfg.finetune_iterations, d_tgt, d_tl, d_qt, d_res,
                                                   d_fin, d_used);
       LAUNCH(ctx);
       check_launch();
+      realize_s += tk.stop();
+      out.profile.realize_calls += nAct;
       auto h_fin = ddownload(d_fin, (size_t)nAct, s);
       auto h_res = ddownload(d_res, (size_t)nAct, s);
       std::vector<int> on(nAct), cand(nAct);
@@ -891,6 +911,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
       CK(cudaMemsetAsync(d_clean, 0, nAct, s));
+      for (int t = 0; t < nAct; ++t) out.profile.collision_calls += on[t];
       k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, d_on, d_qt, d_pose, d_aabb, d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
@@ -963,6 +984,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       for (int t = 0; t < nAct; ++t) cand[t] = alive_idx[pending[t]];
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
+      out.profile.collision_calls += nAct;
       k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, nullptr, d_qt, d_pose, d_aabb, d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
@@ -1037,6 +1059,20 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     }
   }
   out.profile.valid = (long long)out.grasps.size();
+  out.profile.device_seconds = tdev.stop() + out.profile.field_build;
+  {
+    unsigned long long c[kCntN];
+    CK(cudaMemcpyFromSymbol(c, g_cnt, sizeof(c)));
+    out.profile.ik_iterations = (long long)c[kCntIk];
+    out.profile.fk_evals = (long long)c[kCntFk];
+    out.profile.wrench_evals = (long long)c[kCntWeval];
+    out.profile.wrench_grads = (long long)c[kCntWgrad];
+    out.profile.proj_evals = (long long)c[kCntProj];
+  }
+  out.profile.realize_seconds = realize_s;
+  out.profile.contact_opt_seconds = copt_s;
+  out.profile.h2d_bytes = g_h2d;
+  out.profile.d2h_bytes = g_d2h;
   double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   (void)t_pre;
   out.profile.total = total;
@@ -1066,7 +1102,8 @@ __global__ void k_wrench_batch(int m, const int* n, const double* pts, const dou
     wprob_set(w, c, v3_load(pts + (size_t)t * 18 + 3 * c), v3_load(nrm + (size_t)t * 18 + 3 * c));
   WState s;
   int an = -1;
-  double v = wsolve(w, o, nullptr, &an, s);
+  Ctr ctr = {0, 0, 0, 0, 0};
+  double v = wsolve(w, o, nullptr, &an, s, ctr);
   obj[t] = v;
   anchor[t] = an;
   for (int c = 0; c < kMaxC; ++c) {
@@ -1088,7 +1125,8 @@ __global__ void k_realize_var(int m, const int* kk, IkCfg P, int rounds, int fin
   for (int j = 0; j < c_hand.dof; ++j) q[j] = q_out[(size_t)t * kMaxDof + j];
   double mr;
   unsigned long long u;
-  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u);
+  Ctr ctr = {0, 0, 0, 0, 0};
+  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u, ctr);
   for (int j = 0; j < c_hand.dof; ++j) q_out[(size_t)t * kMaxDof + j] = q[j];
   max_res[t] = mr;
   finite[t] = fin ? 1 : 0;

@@ -99,7 +99,12 @@ class Profile(C.Structure):
         "candidates", "placements_accepted", "contact_sets_balanced", "ik_finite",
         "penetration_free", "ik_converged", "stable", "valid")] + [
         ("grasps_per_second", C.c_double)] + [(n, C.c_longlong) for n in (
-        "patches", "boxes", "field_vectors", "object_samples", "field_samples", "gpu_launches")]
+        "patches", "boxes", "field_vectors", "object_samples", "field_samples", "gpu_launches")] + [
+        ("device_seconds", C.c_double), ("h2d_bytes", C.c_longlong),
+        ("d2h_bytes", C.c_longlong)] + [(n, C.c_longlong) for n in (
+        "ik_iterations", "fk_evals", "wrench_evals", "wrench_grads", "proj_evals",
+        "realize_calls", "collision_calls")] + [
+        ("realize_seconds", C.c_double), ("contact_opt_seconds", C.c_double)]
 
 
 class Trace(C.Structure):
