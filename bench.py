@@ -111,8 +111,8 @@ def fp64_peak():
             d = json.load(f)
         return float(d["fp64_tflops"]), "measured (profiles/fp64_peak.json, DFMA loop)"
     except (OSError, KeyError, ValueError):
-        # 148 SMs x 32 FP64 FMA/clk x 2 flop x 1.965 GHz
-        return 148 * 32 * 2 * 1.965e9 / 1e12, "derived (148 SM x 32 DFMA/clk x 2 x 1.965 GHz)"
+        # 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "derived (148 SM x 64 DFMA/clk x 2 x 1.965 GHz)"
 
 
 # ------------------------------------------------------------ CPU baseline

@@ -968,9 +968,11 @@ void ldlt_solve(int n, double* A, double* x) {
     if (std::abs(d) > 2.2250738585072014e-308) x[i] /= d;
     else x[i] = 0.0;
   }
+  // L^T back substitution; canonical order: the sum for x[i] accumulates
+  // j = n-1 down to i+1 (the order in which the x[j] become final).
   for (int i = n - 1; i >= 0; --i) {
     double s = 0.0;
-    for (int j = i + 1; j < n; ++j) s = s + A[j * n + i] * x[j];
+    for (int j = n - 1; j > i; --j) s = s + A[j * n + i] * x[j];
     x[i] -= s;
   }
   for (int k = n - 1; k >= 0; --k) std::swap(x[k], x[tr[k]]);

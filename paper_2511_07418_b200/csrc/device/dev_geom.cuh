@@ -16,6 +16,7 @@ using namespace lgm;
 
 constexpr int kMaxLinks = 32;   // device link cap (Shadow-class hands have ~25)
 constexpr int kMaxDof = 24;     // device dof cap (Shadow 22 DoF)
+constexpr int kMaxDepth = 10;   // device kinematic-chain depth cap
 constexpr int kMaxK = LG_MAX_K;
 constexpr int kMaxC = LG_MAX_CONTACTS;
 constexpr double kPi = 3.14159265358979323846;
@@ -30,6 +31,11 @@ struct DHand {
   double R[kMaxLinks][9], t[kMaxLinks][3], axis[kMaxLinks][3], lo[kMaxLinks], hi[kMaxLinks];
   double jlo[kMaxDof], jhi[kMaxDof];  // limits by joint index
   double mid[kMaxDof];                // mid_config (hand.cpp:24-32)
+  // warp-parallel FK: root -> link chain per link, joints on that chain
+  int chain_len[kMaxLinks];
+  int chain[kMaxLinks][kMaxDepth];
+  unsigned jmask[kMaxLinks];  // bit j: joint j drives link l
+  int jlink[kMaxDof];         // link carrying joint j
   // convex parts (global memory)
   const int* vert_off;
   const double* verts;

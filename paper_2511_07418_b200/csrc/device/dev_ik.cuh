@@ -114,7 +114,7 @@ __device__ void ldlt_solve(int n, double* A, double* x) {
   }
   for (int i = n - 1; i >= 0; --i) {
     double s = 0.0;
-    for (int j = i + 1; j < n; ++j) s = s + A[j * n + i] * x[j];
+    for (int j = n - 1; j > i; --j) s = s + A[j * n + i] * x[j];
     x[i] -= s;
   }
   for (int k = n - 1; k >= 0; --k) {

@@ -1,0 +1,469 @@
+// dev_ikw.cuh — warp-cooperative realize_grasp / solve_contact_ik: one warp
+// per problem (reference ik.cpp:31-139, pipeline.cpp:185-253).
+//
+// Lane roles (all summations keep the oracle's exact order, so results are
+// bit-identical to the serial restatement):
+//   - FK: lane l holds the frame of link l in registers and composes its own
+//     root -> l chain; that is the same sequence of compose() calls the
+//     topological-order FK performs for link l (hand.cpp:275-295).
+//   - Jacobian: lane j owns joint column j; rows are streamed per target point.
+//   - J^T J: lanes own entries (a <= b), each a row-ordered sum; mirrored.
+//   - LDLT (Eigen, diagonal pivoting): lane i owns row i of the trailing
+//     update; pivot = warp argmax (first index on ties).
+//   - triangular solves: lane i keeps a running sum that accumulates terms in
+//     the order the unknowns become final (ascending forward, descending
+//     backward: the canonical orders of oracle/orc_core.cpp ldlt_solve).
+#pragma once
+
+#include "dev_ik.cuh"
+
+namespace lgd {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ Xf shfl_xf(const Xf& x, int src) {
+  Xf o;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) o.R.m[a] = __shfl_sync(kFull, x.R.m[a], src);
+  o.t.x = __shfl_sync(kFull, x.t.x, src);
+  o.t.y = __shfl_sync(kFull, x.t.y, src);
+  o.t.z = __shfl_sync(kFull, x.t.z, src);
+  return o;
+}
+
+// Frame of link `lane` at q (q in shared memory, read by all lanes).
+__device__ __forceinline__ Xf wfk(const double* q, int lane) {
+  Xf f = xf_identity();
+  if (lane < c_hand.n_links) {
+    const int n = c_hand.chain_len[lane];
+    for (int d = 0; d < n; ++d) {
+      int l = c_hand.chain[lane][d];
+      Xf local;
+      local.R = m3_load(c_hand.R[l]);
+      local.t = v3_load(c_hand.t[l]);
+      int jt = c_hand.jtype[l];
+      if (jt == 1) {
+        Xf m;
+        m.R = angle_axis(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]));
+        m.t = v3(0.0, 0.0, 0.0);
+        local = xf_compose(local, m);
+      } else if (jt == 2) {
+        local.t = add(local.t, mul(local.R, scale(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]))));
+      }
+      f = d == 0 ? local : xf_compose(f, local);
+    }
+  }
+  return f;
+}
+
+// Target layout in shared memory: [k][12] = op(3) on(3) hp(3) hn(3); links [k].
+struct WTargets {
+  double* t;
+  int* link;
+};
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// stacked_residual (ik.cpp:13-27): lanes < k fill r[6i..6i+5]; returns the
+// row-ordered sum of squares (computed by lane 0, broadcast).
+__device__ __forceinline__ double wresidual(const Xf& f, const WTargets& T, int k, double beta,
+                                            double* r, int lane) {
+  int src = lane < k ? T.link[lane] : 0;
+  Xf F = shfl_xf(f, src);
+  if (lane < k) {
+    const double* t = T.t + 12 * lane;
+    V3 op = v3_load(t), on = v3_load(t + 3);
+    V3 hp = xf_apply(F, v3_load(t + 6));
+    V3 hn = xf_rotate(F, v3_load(t + 9));
+    V3 a = sub(op, hp);
+    V3 b = sub(axpy(op, beta, on), axpy(hp, beta, hn));
+    double* o = r + 6 * lane;
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = a.z;
+    o[3] = b.x;
+    o[4] = b.y;
+    o[5] = b.z;
+  }
+  __syncwarp();
+  double s = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < 6 * k; ++i) s = s + r[i] * r[i];
+  return __shfl_sync(kFull, s, 0);
+}
+
+struct WarpWs {
+  double *J, *A, *r, *rt, *x, *qt, *pts;
+  int* tr;
+};
+
+__host__ __device__ __forceinline__ size_t warp_ws_bytes(int k, int dof) {
+  size_t d = (size_t)6 * k * dof + (size_t)dof * dof + 12 * k + 2 * dof + 6 * k;
+  return (d * sizeof(double) + (size_t)dof * sizeof(int) + 15) & ~(size_t)15;
+}
+
+__device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
+  WarpWs w;
+  double* p = (double*)base;
+  w.J = p;
+  p += 6 * k * dof;
+  w.A = p;
+  p += dof * dof;
+  w.r = p;
+  p += 6 * k;
+  w.rt = p;
+  p += 6 * k;
+  w.x = p;
+  p += dof;
+  w.qt = p;
+  p += dof;
+  w.pts = p;
+  p += 6 * k;
+  w.tr = (int*)p;
+  return w;
+}
+
+// Eigen LDLT factor + solve, warp-parallel; A (n x n, smem) destroyed,
+// x (smem) rhs in / solution out.
+__device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
+  for (int k = 0; k < n; ++k) {
+    double v = (lane >= k && lane < n) ? dabs(A[lane * n + lane]) : -1.0;
+    int idx = (lane >= k && lane < n) ? lane : 0x7fff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(kFull, v, o);
+      int oi = __shfl_xor_sync(kFull, idx, o);
+      if (ov > v || (ov == v && oi < idx)) {
+        v = ov;
+        idx = oi;
+      }
+    }
+    const int big = idx;
+    if (lane == 0) tr[k] = big;
+    if (k != big) {
+      if (lane < k) {
+        double t = A[k * n + lane];
+        A[k * n + lane] = A[big * n + lane];
+        A[big * n + lane] = t;
+      }
+      if (lane > big && lane < n) {
+        double t = A[lane * n + k];
+        A[lane * n + k] = A[lane * n + big];
+        A[lane * n + big] = t;
+      }
+      if (lane == 0) {
+        double t = A[k * n + k];
+        A[k * n + k] = A[big * n + big];
+        A[big * n + big] = t;
+      }
+      if (lane > k && lane < big) {
+        double u = A[lane * n + k];
+        A[lane * n + k] = A[big * n + lane];
+        A[big * n + lane] = u;
+      }
+      __syncwarp();
+    }
+    if (k > 0) {
+      // temp_j = D_j * A(k, j), j < k (kept in registers of lane j)
+      double tj = lane < k ? A[lane * n + lane] * A[k * n + lane] : 0.0;
+      double acc = 0.0;
+      for (int j = 0; j < k; ++j) {
+        double t = __shfl_sync(kFull, tj, j);
+        if (lane >= k && lane < n) acc = acc + A[lane * n + j] * t;
+      }
+      __syncwarp();
+      if (lane >= k && lane < n) A[lane * n + k] -= acc;  // lane k: A(k,k); lanes > k: A21
+      __syncwarp();
+    }
+    double akk = A[k * n + k];
+    if (dabs(akk) > 0.0 && lane > k && lane < n) A[lane * n + k] /= akk;
+    __syncwarp();
+  }
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      double t = x[k];
+      x[k] = x[tr[k]];
+      x[tr[k]] = t;
+    }
+  __syncwarp();
+  double xi = lane < n ? x[lane] : 0.0;
+  double s = 0.0;
+  for (int j = 0; j < n; ++j) {  // forward: L unit lower
+    double xj = __shfl_sync(kFull, xi - s, j);
+    if (lane == j) xi = xj;
+    if (lane > j && lane < n) s = s + A[lane * n + j] * xj;
+  }
+  if (lane < n) {
+    double d = A[lane * n + lane];
+    if (dabs(d) > 2.2250738585072014e-308) xi /= d;
+    else xi = 0.0;
+  }
+  s = 0.0;
+  for (int j = n - 1; j >= 0; --j) {  // backward: L^T
+    double xj = __shfl_sync(kFull, xi - s, j);
+    if (lane == j) xi = xj;
+    if (lane < j) s = s + A[j * n + lane] * xj;
+  }
+  if (lane < n) x[lane] = xi;
+  __syncwarp();
+  if (lane == 0)
+    for (int k = n - 1; k >= 0; --k) {
+      double t = x[k];
+      x[k] = x[tr[k]];
+      x[tr[k]] = t;
+    }
+  __syncwarp();
+}
+
+// solve_contact_ik (ik.cpp:31-139).  q (smem) in/out; f = lane frame at q on
+// exit.  Returns finite; used = OR of joints with a nonzero column.
+__device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
+                    unsigned long long& used, WarpWs& ws, Xf& f, Ctr& ctr, int lane) {
+  const int dof = c_hand.dof;
+  const int rows = 6 * k;
+  if (lane < dof) q[lane] = dclamp(q[lane], c_hand.jlo[lane], c_hand.jhi[lane]);
+  __syncwarp();
+  used = 0ull;
+  if (k == 0) {
+    f = wfk(q, lane);
+    return true;
+  }
+  bool finite = true;
+  f = wfk(q, lane);
+  ++ctr.fk;
+  double* r = ws.r;
+  double* rt = ws.rt;
+  double objective = wresidual(f, T, k, P.beta, r, lane);
+  for (int it = 0; it < iterations; ++it) {
+    ++ctr.ik_it;
+    // Jacobian points: lane p < 2k -> target p/2, half p%2
+    {
+      int i = lane >> 1;
+      int src = lane < 2 * k ? T.link[i] : 0;
+      Xf F = shfl_xf(f, src);
+      if (lane < 2 * k) {
+        const double* t = T.t + 12 * i;
+        V3 lp = (lane & 1) ? axpy(v3_load(t + 6), P.beta, v3_load(t + 9)) : v3_load(t + 6);
+        v3_store(ws.pts + 3 * lane, xf_apply(F, lp));
+      }
+    }
+    // joint columns
+    {
+      int lj = lane < dof ? c_hand.jlink[lane] : 0;
+      Xf Fj = shfl_xf(f, lj);
+      __syncwarp();
+      if (lane < dof) {
+        V3 axis = mul(Fj.R, v3_load(c_hand.axis[lj]));
+        bool rev = c_hand.jtype[lj] == 1;
+        double cm = 0.0;
+        for (int p = 0; p < 2 * k; ++p) {
+          bool on = (c_hand.jmask[T.link[p >> 1]] >> lane) & 1u;
+          V3 col = v3(0.0, 0.0, 0.0);
+          if (on) col = rev ? cross(axis, sub(v3_load(ws.pts + 3 * p), Fj.t)) : axis;
+          int row = 3 * p;  // 6i + 3h
+          ws.J[(row + 0) * dof + lane] = col.x;
+          ws.J[(row + 1) * dof + lane] = col.y;
+          ws.J[(row + 2) * dof + lane] = col.z;
+          cm = dmax(cm, dabs(col.x));
+          cm = dmax(cm, dabs(col.y));
+          cm = dmax(cm, dabs(col.z));
+        }
+        if (cm > 1e-12) used |= 1ull << lane;
+      }
+    }
+    {
+      unsigned long long u = used;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) u |= __shfl_xor_sync(kFull, u, o);
+      used = u;
+    }
+    __syncwarp();
+    // J^T J (upper triangle, mirrored) and J^T r
+    const int ne = dof * (dof + 1) / 2;
+    for (int e = lane; e < ne; e += 32) {
+      int a = 0, rem = e;
+      while (rem >= dof - a) {
+        rem -= dof - a;
+        ++a;
+      }
+      int b = a + rem;
+      double s = 0.0;
+      for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
+      ws.A[a * dof + b] = s;
+      ws.A[b * dof + a] = s;
+    }
+    if (lane < dof) {
+      double s = 0.0;
+      for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + lane] * r[rr];
+      ws.x[lane] = s;
+    }
+    __syncwarp();
+    double tr = 0.0;
+    if (lane == 0)
+      for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * dof + a];
+    tr = __shfl_sync(kFull, tr, 0);
+    double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
+    if (lane < dof) ws.A[lane * dof + lane] += lambda;
+    __syncwarp();
+    wldlt_solve(dof, ws.A, ws.x, ws.tr, lane);
+    bool bad = lane < dof && !is_finite(ws.x[lane]);
+    if (__any_sync(kFull, bad)) {
+      finite = false;
+      break;
+    }
+    bool moved = false;
+    double dq = lane < dof ? ws.x[lane] : 0.0;
+    for (int bt = 0; bt <= P.max_backtracks; ++bt) {
+      if (lane < dof)
+        ws.qt[lane] = dclamp(q[lane] + dmin(dmax(dq, -P.step_clamp), P.step_clamp), c_hand.jlo[lane],
+                             c_hand.jhi[lane]);
+      __syncwarp();
+      Xf ft = wfk(ws.qt, lane);
+      ++ctr.fk;
+      double obj_try = wresidual(ft, T, k, P.beta, rt, lane);
+      if (obj_try <= objective) {
+        if (lane < dof) q[lane] = ws.qt[lane];
+        f = ft;
+        double* sw = r;
+        r = rt;
+        rt = sw;
+        objective = obj_try;
+        moved = true;
+        __syncwarp();
+        break;
+      }
+      dq *= 0.5;
+    }
+    if (!moved) break;
+    double mp = 0.0;
+    if (lane < k) mp = norm(v3(r[6 * lane], r[6 * lane + 1], r[6 * lane + 2]));
+    mp = warp_max_d(mp);
+    if (mp < P.residual_tol) break;
+  }
+  bool nonfin = lane < dof && !is_finite(q[lane]);
+  if (__any_sync(kFull, nonfin)) finite = false;
+  // keep the caller's r buffer in place (ws.r) for residual reads
+  if (r != ws.r) {
+    if (lane < rows) ws.r[lane] = r[lane];
+    __syncwarp();
+  }
+  return finite;
+}
+
+// realize_grasp's project (pipeline.cpp:196-220) at lane frames f: worst
+// distance (all lanes), optionally refreshing hand points into R.
+__device__ __forceinline__ double wproject(const Xf& f, const WTargets& T, int k, WTargets* R,
+                                           int lane) {
+  int src = lane < k ? T.link[lane] : 0;
+  Xf F = shfl_xf(f, src);
+  double d = 0.0;
+  if (lane < k) {
+    Xf inv = xf_inverse(F);
+    V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
+    d = closest_on_parts(T.link[lane], xf_apply(inv, v3_load(T.t + 12 * lane)), &sp, &sn);
+    if (R) {
+      v3_store(R->t + 12 * lane + 6, sp);
+      v3_store(R->t + 12 * lane + 9, sn);
+    }
+  }
+  __syncwarp();
+  return warp_max_d(d);
+}
+
+// realize_grasp (pipeline.cpp:185-253) for one warp; q (smem) starts at q0.
+__device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref, int k,
+                         const IkCfg& P, int rounds, int fine_iters, double* max_res,
+                         unsigned long long* used_out, WarpWs& ws, Ctr& ctr, int lane) {
+  const int dof = c_hand.dof;
+  double q0 = lane < dof ? q[lane] : 0.0;
+  unsigned long long used = 0ull;
+  Xf f;
+  if (!wik(q, T, k, P, P.iterations, used, ws, f, ctr, lane)) {
+    if (lane < dof) q[lane] = q0;
+    __syncwarp();
+    *max_res = kInf;
+    *used_out = 0ull;
+    return false;
+  }
+  double worst = wproject(f, T, k, nullptr, lane);
+  for (int round = 0; round < rounds; ++round) {
+    for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
+    if (lane < k) Ref.link[lane] = T.link[lane];
+    __syncwarp();
+    wproject(f, T, k, &Ref, lane);
+    if (lane < dof) qs[lane] = q[lane];
+    __syncwarp();
+    unsigned long long su = 0ull;
+    Xf fs;
+    if (!wik(qs, Ref, k, P, fine_iters, su, ws, fs, ctr, lane)) break;
+    double w2 = wproject(fs, T, k, nullptr, lane);
+    if (w2 > worst + 1e-6) break;
+    if (lane < dof) q[lane] = qs[lane];
+    __syncwarp();
+    f = fs;
+    worst = w2;
+    used |= su;
+  }
+  *max_res = wproject(f, T, k, nullptr, lane);
+  *used_out = used;
+  bool nonfin = lane < dof && !is_finite(q[lane]);
+  return !__any_sync(kFull, nonfin);
+}
+
+// Per-warp shared bytes: workspace + targets, refreshed targets, q, qs, links
+// (16-byte aligned so every warp's double arrays stay aligned).
+__host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof) {
+  size_t b = warp_ws_bytes(kMaxK, dof) + (size_t)(24 * kMaxK + 2 * kMaxDof) * sizeof(double) +
+             2 * kMaxK * sizeof(int);
+  return (b + 15) & ~(size_t)15;
+}
+
+// One warp per problem; targets [t][kMaxK][12] + links [t][kMaxK]; q_out
+// [t][kMaxDof] holds q0 on entry (mid_config when q_init == nullptr).
+__global__ void k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_iters,
+                               const double* tgt, int tgt_stride, const int* tl, int tl_stride,
+                               const double* q_init, double* q_out, double* max_res, int* finite,
+                               unsigned long long* used) {
+  extern __shared__ __align__(16) char s_ik[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (t >= nAct) return;  // warp-uniform
+  const int kt = kk ? kk[t] : k;
+  const int dof = c_hand.dof;
+  char* base = s_ik + (size_t)warp * realize_warp_bytes(dof);
+  WarpWs ws = warp_ws(base, kt, dof);
+  double* extra = (double*)(base + warp_ws_bytes(kMaxK, dof));
+  WTargets T, Ref;
+  T.t = extra;
+  Ref.t = extra + 12 * kMaxK;
+  double* q = extra + 24 * kMaxK;
+  double* qs = q + kMaxDof;
+  T.link = (int*)(qs + kMaxDof);
+  Ref.link = T.link + kMaxK;
+  const double* src = tgt + (size_t)t * tgt_stride;
+  for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
+  if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
+  if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : c_hand.mid[lane];
+  __syncwarp();
+  Ctr ctr = {0, 0, 0, 0, 0};
+  double mr;
+  unsigned long long u;
+  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, ctr, lane);
+  if (lane == 0) ctr_flush(ctr);
+  if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
+  if (lane == 0) {
+    max_res[t] = mr;
+    finite[t] = fin ? 1 : 0;
+    used[t] = u;
+  }
+}
+
+__host__ __forceinline__ size_t realize_warp_smem(int dof, int warps) {
+  return realize_warp_bytes(dof) * warps;
+}
+
+}  // namespace lgd

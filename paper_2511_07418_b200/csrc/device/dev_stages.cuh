@@ -5,7 +5,7 @@
 #include <cub/cub.cuh>
 
 #include "dev_field.cuh"
-#include "dev_ik.cuh"
+#include "dev_ikw.cuh"
 
 namespace lgd {
 

@@ -198,6 +198,19 @@ void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
       h.mid[d.joint_index[l]] = 0.5 * (d.limit_lo[l] + d.limit_hi[l]);
     }
   }
+  for (int l = 0; l < d.n_links; ++l) {
+    int path[kMaxLinks + 1], n = 0;
+    for (int x = l; x >= 0 && n <= kMaxLinks; x = d.parent[x]) path[n++] = x;
+    if (n > kMaxDepth) throw std::invalid_argument("device: kinematic chain deeper than 10 links");
+    h.chain_len[l] = n;
+    h.jmask[l] = 0u;
+    for (int i = 0; i < n; ++i) {
+      int x = path[n - 1 - i];
+      h.chain[l][i] = x;
+      if (d.joint_index[x] >= 0) h.jmask[l] |= 1u << d.joint_index[x];
+    }
+    if (d.joint_index[l] >= 0) h.jlink[d.joint_index[l]] = l;
+  }
   for (int p = 0; p < d.n_parts; ++p) {
     int l = d.part_link[p];
     if (p > 0 && d.part_link[p] < d.part_link[p - 1])
@@ -220,6 +233,23 @@ void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
   dupload(ctx->h_part_link, d.part_link, (size_t)d.n_parts, s);
   ctx->n_parts = d.n_parts;
   CK(cudaMemcpyToSymbolAsync(c_hand, &h, sizeof(DHand), 0, cudaMemcpyHostToDevice, s));
+}
+
+// realize_grasp, one warp per problem, 4 warps per CTA.
+void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCfg& P, int rounds,
+                         int fine_iters, const double* tgt, int tgt_stride, const int* tl,
+                         int tl_stride, const double* q_init, double* q_out, double* max_res,
+                         int* finite, unsigned long long* used, int dof) {
+  const int wpb = 4;
+  size_t smem = realize_warp_smem(dof, wpb);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_realize_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_realize_warp<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, P, rounds, fine_iters, tgt,
+                                                             tgt_stride, tl, tl_stride, q_init, q_out,
+                                                             max_res, finite, used);
 }
 
 // Flattened patch data on the device.
@@ -893,9 +923,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_fin = dalloc<int>(b_fin, (size_t)nAct);
       auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nAct);
       tk.start();
-      k_realize<<<grid_for(nAct, 32), 32, 0, s>>>(nAct, k, ikc, cfg.finetune_rounds,
-                                                  cfg.finetune_iterations, d_tgt, d_tl, d_qt, d_res,
-                                                  d_fin, d_used);
+      launch_realize_warp(s, nAct, k, nullptr, ikc, cfg.finetune_rounds, cfg.finetune_iterations,
+                          d_tgt, k * 12, d_tl, k, nullptr, d_qt, d_res, d_fin, d_used, hd.dof);
       LAUNCH(ctx);
       check_launch();
       realize_s += tk.stop();
@@ -1273,8 +1302,8 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
     P.damping_min = 1e-6;
     P.iterations = iterations;
     P.max_backtracks = 10;
-    k_realize_var<<<grid_for(m, 32), 32, 0, s>>>(m, d_k, P, finetune_rounds, finetune_iterations, d_t,
-                                                 d_l, d_q, d_r, d_f, d_u);
+    launch_realize_warp(s, m, 0, d_k, P, finetune_rounds, finetune_iterations, d_t, kMaxK * 12, d_l,
+                        kMaxK, d_q, d_q, d_r, d_f, d_u, hand->dof);
     check_launch();
     auto hq = ddownload(d_q, q0.size(), s);
     for (int i = 0; i < m; ++i)
