@@ -1,0 +1,381 @@
+// dev_copt.cuh — optimize_contacts (reference contact_opt.cpp:45-142) with a
+// register-lean wrench solver (wrench.cpp:124-226).
+//
+// Layout per warp (one warp = one restart):
+//   shared  : incumbent problem, k + s contacts x (p, n, tx, ty, p x n,
+//             p x tx, p x ty) = 21 doubles each; incumbent solution
+//             (alpha, beta_x, beta_y); per-lane best solver state.
+//   registers: the lane's trial slot (21 doubles) and its solver state.
+// The solver never stores the backtracking trial state or the gradient:
+// projection is per contact, so trial_i = project_i(s_i - step g_i) is
+// computed, projected and accumulated contact by contact, and recomputed
+// with identical arithmetic when accepted.  Every sum keeps the oracle's
+// order, so results stay bit-identical.
+#pragma once
+
+#include "dev_stages.cuh"
+
+namespace lgd {
+
+constexpr int kSlot = 21;
+
+// Problem view: contacts from shared memory except slot `tq` (registers).
+struct PV {
+  const double* sp;
+  int n, tq;
+  double lambda, mu;
+  double tv[kSlot];
+  __device__ __forceinline__ double g(int i, int c) const { return i == tq ? tv[c] : sp[kSlot * i + c]; }
+  __device__ __forceinline__ V3 v(int i, int c) const { return v3(g(i, c), g(i, c + 1), g(i, c + 2)); }
+};
+
+// write_slot (contact_opt.cpp:31-35) into a 21-double slot record.
+__device__ __forceinline__ void slot_make(double* o, V3 p, V3 n) {
+  V3 tx, ty;
+  tangent_basis(n, tx, ty);
+  V3 cn = cross(p, n), cx = cross(p, tx), cy = cross(p, ty);
+  v3_store(o, p);
+  v3_store(o + 3, n);
+  v3_store(o + 6, tx);
+  v3_store(o + 9, ty);
+  v3_store(o + 12, cn);
+  v3_store(o + 15, cx);
+  v3_store(o + 18, cy);
+}
+
+__device__ __forceinline__ void proj_one(bool is_anchor, bool fr, double mu, double& a, double& bx,
+                                         double& by) {
+  if (is_anchor) a = 1.0;
+  else if (a < 0.0) a = 0.0;
+  if (!fr) {
+    bx = 0.0;
+    by = 0.0;
+    return;
+  }
+  double cap = mu * a;
+  double r = lgm::xhypot(bx, by);
+  if (r > cap) {
+    if (cap <= 0.0 || r <= 0.0) {
+      bx = 0.0;
+      by = 0.0;
+    } else {
+      double kk = cap / r;
+      bx *= kk;
+      by *= kk;
+    }
+  }
+}
+
+__device__ __forceinline__ void pv_net(const PV& w, const double* a, const double* bx,
+                                       const double* by, V3& f, V3& t) {
+  f = v3(0.0, 0.0, 0.0);
+  t = v3(0.0, 0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i) {
+    if (i < w.n) {
+      f = add(f, add(add(scale(a[i], w.v(i, 3)), scale(bx[i], w.v(i, 6))), scale(by[i], w.v(i, 9))));
+      t = add(t, add(add(scale(a[i], w.v(i, 12)), scale(bx[i], w.v(i, 15))), scale(by[i], w.v(i, 18))));
+    }
+  }
+}
+
+// descend (wrench.cpp:124-177) on state (a, bx, by) in registers.
+__device__ double pv_descend(const PV& w, int anchor, bool fr, int iterations, double step0,
+                             int max_bt, double* a, double* bx, double* by, Ctr& ctr) {
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i)
+    if (i < w.n) proj_one(i == anchor, fr, w.mu, a[i], bx[i], by[i]);
+  V3 f, t;
+  pv_net(w, a, bx, by, f, t);
+  double current = sqnorm(f) + w.lambda * sqnorm(t);
+  ++ctr.weval;
+  for (int it = 0; it < iterations; ++it) {
+    V3 force, torque;
+    pv_net(w, a, bx, by, force, torque);
+    ++ctr.wgrad;
+    torque = v3(torque.x * w.lambda, torque.y * w.lambda, torque.z * w.lambda);
+    double step = step0;
+    bool moved = false;
+    for (int bt = 0; bt <= max_bt; ++bt) {
+      V3 f2 = v3(0.0, 0.0, 0.0), t2 = v3(0.0, 0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < kMaxC; ++i) {
+        if (i < w.n) {
+          double ga = 2.0 * (dot(force, w.v(i, 3)) + dot(torque, w.v(i, 12)));
+          double ta = a[i] - step * ga, tbx = 0.0, tby = 0.0;
+          if (fr) {
+            double gx = 2.0 * (dot(force, w.v(i, 6)) + dot(torque, w.v(i, 15)));
+            double gy = 2.0 * (dot(force, w.v(i, 9)) + dot(torque, w.v(i, 18)));
+            tbx = bx[i] - step * gx;
+            tby = by[i] - step * gy;
+          }
+          proj_one(i == anchor, fr, w.mu, ta, tbx, tby);
+          f2 = add(f2, add(add(scale(ta, w.v(i, 3)), scale(tbx, w.v(i, 6))), scale(tby, w.v(i, 9))));
+          t2 = add(t2, add(add(scale(ta, w.v(i, 12)), scale(tbx, w.v(i, 15))), scale(tby, w.v(i, 18))));
+        }
+      }
+      double next = sqnorm(f2) + w.lambda * sqnorm(t2);
+      ++ctr.weval;
+      if (next <= current) {
+#pragma unroll
+        for (int i = 0; i < kMaxC; ++i) {
+          if (i < w.n) {
+            double ga = 2.0 * (dot(force, w.v(i, 3)) + dot(torque, w.v(i, 12)));
+            double ta = a[i] - step * ga, tbx = 0.0, tby = 0.0;
+            if (fr) {
+              double gx = 2.0 * (dot(force, w.v(i, 6)) + dot(torque, w.v(i, 15)));
+              double gy = 2.0 * (dot(force, w.v(i, 9)) + dot(torque, w.v(i, 18)));
+              tbx = bx[i] - step * gx;
+              tby = by[i] - step * gy;
+            }
+            proj_one(i == anchor, fr, w.mu, ta, tbx, tby);
+            a[i] = ta;
+            bx[i] = tbx;
+            by[i] = tby;
+          }
+        }
+        current = next;
+        moved = true;
+        break;
+      }
+      step *= 0.5;
+    }
+    if (!moved) break;
+  }
+  return current;
+}
+
+// One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
+// warm-started from `warm` ([3][kMaxC], shared memory).
+__device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts& o,
+                                            const double* warm, double* a, double* bx, double* by,
+                                            Ctr& ctr) {
+  const bool fr = w.mu > 0.0;
+  const int iters = warm ? o.warm_iterations : o.iterations;
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i) {
+    a[i] = warm ? warm[i] : 1.0;
+    bx[i] = warm ? warm[kMaxC + i] : 0.0;
+    by[i] = warm ? warm[2 * kMaxC + i] : 0.0;
+  }
+  if (fr) {
+    pv_descend(w, anchor, false, iters, o.step, o.max_bt, a, bx, by, ctr);
+    return pv_descend(w, anchor, true, iters, o.step, o.max_bt, a, bx, by, ctr);
+  }
+  return pv_descend(w, anchor, false, iters, o.step, o.max_bt, a, bx, by, ctr);
+}
+
+// Block per candidate, warp per restart, lanes over the n_inner mutations.
+__global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static,
+                               const double* st_p, const double* st_n, const long long* el_off,
+                               const double* el_p, const double* el_n, const uint64_t* draws,
+                               int* out_ids, double* out_obj, int* out_anchor, double* out_sol,
+                               double eps_stable, int* balanced) {
+  extern __shared__ __align__(16) double s_co[];
+  const int a = blockIdx.x;
+  if (a >= nA) return;
+  const int i = alive_idx[a];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int k = cfg.k;
+  const int s = n_static[i];
+  const int n = k + s;
+  // shared layout per warp: problem [kMaxC][21], incumbent sol [18],
+  // lane states [32][18]; then per-block restart results
+  const int per_warp = kMaxC * kSlot + 6 * kMaxC + 32 * 3 * kMaxC;
+  double* W = s_co + warp * per_warp;
+  double* sp = W;
+  double* inc = W + kMaxC * kSlot;  // incumbent solution (warm start)
+  double* win = inc + 3 * kMaxC;    // best mutation's solution of this step
+  double* lst = win + 3 * kMaxC;    // per-lane solver states
+  const int rstride = 2 + k + 3 * kMaxC;
+  double* res = s_co + nw * per_warp;
+  long long off[kMaxK], cnt[kMaxK];
+  for (int q = 0; q < k; ++q) {
+    off[q] = el_off[a * k + q];
+    cnt[q] = el_off[a * k + q + 1] - off[q];
+  }
+  Ctr ctr = {0, 0, 0, 0, 0};
+  for (int rbase = 0; rbase < cfg.restarts; rbase += nw) {
+    const int r = rbase + warp;
+    if (r < cfg.restarts) {
+      const uint64_t* D = draws + (size_t)a * cfg.per_cand + (size_t)r * cfg.per_restart;
+      int ids[kMaxK];
+      for (int q = 0; q < k; ++q) ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
+      if (lane < k) {
+        long long e = off[lane] + ids[lane];
+        slot_make(sp + kSlot * lane, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+      } else if (lane == k && s) {
+        slot_make(sp + kSlot * k, v3_load(st_p + 3 * i), v3_load(st_n + 3 * i));
+      }
+      __syncwarp();
+      PV w;
+      w.sp = sp;
+      w.n = n;
+      w.tq = -1;
+      w.lambda = cfg.lambda;
+      w.mu = cfg.mu;
+#pragma unroll
+      for (int c = 0; c < kSlot; ++c) w.tv[c] = 0.0;
+      double st_a[kMaxC], st_bx[kMaxC], st_by[kMaxC];
+      // cold solve: lanes over anchors, best anchor by strict '<'
+      double val = kInf;
+      if (lane < n) {
+        val = pv_anchor(w, lane, cfg.o, nullptr, st_a, st_bx, st_by, ctr);
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          lst[3 * kMaxC * lane + c] = st_a[c];
+          lst[3 * kMaxC * lane + kMaxC + c] = st_bx[c];
+          lst[3 * kMaxC * lane + 2 * kMaxC + c] = st_by[c];
+        }
+      }
+      if (!(val < kInf)) val = kInf;
+      double best = val;
+      int bl = val < kInf ? lane : 99;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(kFull, best, o);
+        int ol = __shfl_xor_sync(kFull, bl, o);
+        if (ov < best || (ov == best && ol < bl)) {
+          best = ov;
+          bl = ol;
+        }
+      }
+      int anchor = best < kInf ? bl : -1;
+      double obj = best;
+      __syncwarp();
+      if (lane < 3 * kMaxC) inc[lane] = anchor >= 0 ? lst[3 * kMaxC * anchor + lane] : 0.0;
+      __syncwarp();
+      const uint64_t* M = D + k;
+      for (int outer = 0; outer < cfg.n_outer; ++outer) {
+        for (int q = 0; q < k; ++q) {
+          V3 cur_p = v3(sp[kSlot * q], sp[kSlot * q + 1], sp[kSlot * q + 2]);
+          V3 cur_n = neg(v3(sp[kSlot * q + 3], sp[kSlot * q + 4], sp[kSlot * q + 5]));  // element normal
+          V3 tx, ty;
+          tangent_basis(neg(cur_n), tx, ty);
+          double best_obj = obj;
+          int best_m = 0x7fffffff, best_id = -1, best_anchor = -1;
+          for (int mb = 0; mb < cfg.n_inner; mb += 32) {
+            const int m = mb + lane;
+            double v = kInf;
+            int cand = -1, an = -1;
+            if (m < cfg.n_inner) {
+              const uint64_t* d2 = M + 2 * ((long long)(outer * k + q) * cfg.n_inner + m);
+              double z1, z2;
+              box_muller(d2[0], d2[1], &z1, &z2);
+              V3 cp = axpy(axpy(cur_p, cfg.sigma * z1, tx), cfg.sigma * z2, ty);
+              // project_to_domain (contact_opt.cpp:11-25)
+              const double* P = el_p + 3 * off[q];
+              double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
+              int bi = 0;
+              for (long long e = 1; e < cnt[q]; ++e) {
+                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                if (d2v < bd) {
+                  bd = d2v;
+                  bi = (int)e;
+                }
+              }
+              ctr.proj += (unsigned long long)cnt[q];
+              cand = bi;
+              long long e = off[q] + bi;
+              PV tw = w;
+              tw.tq = q;
+              double tmp[kSlot];
+              slot_make(tmp, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+#pragma unroll
+              for (int c = 0; c < kSlot; ++c) tw.tv[c] = tmp[c];
+              // warm solve over all anchors in this lane (run_solver)
+              double bobj = kInf;
+              for (int anc = 0; anc < n; ++anc) {
+                double va = pv_anchor(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, st_a, st_bx, st_by,
+                                      ctr);
+                if (va < bobj) {
+                  bobj = va;
+                  an = anc;
+#pragma unroll
+                  for (int c = 0; c < kMaxC; ++c) {
+                    lst[3 * kMaxC * lane + c] = st_a[c];
+                    lst[3 * kMaxC * lane + kMaxC + c] = st_bx[c];
+                    lst[3 * kMaxC * lane + 2 * kMaxC + c] = st_by[c];
+                  }
+                }
+              }
+              v = bobj;
+            }
+            double bv = (v < best_obj) ? v : kInf;
+            int bm = (v < best_obj) ? m : 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              double ov = __shfl_xor_sync(kFull, bv, o);
+              int om = __shfl_xor_sync(kFull, bm, o);
+              if (ov < bv || (ov == bv && om < bm)) {
+                bv = ov;
+                bm = om;
+              }
+            }
+            if (bm != 0x7fffffff) {
+              int src = bm - mb;
+              best_obj = bv;
+              best_m = bm;
+              best_id = __shfl_sync(kFull, cand, src);
+              best_anchor = __shfl_sync(kFull, an, src);
+              __syncwarp();
+              // keep the winner's state before the next chunk reuses lst;
+              // the warm start (inc) stays the step's incumbent until the end
+              if (lane < 3 * kMaxC) win[lane] = lst[3 * kMaxC * src + lane];
+              __syncwarp();
+            }
+          }
+          (void)best_m;
+          if (best_id >= 0) {
+            ids[q] = best_id;
+            if (lane == 0) {
+              long long e = off[q] + best_id;
+              slot_make(sp + kSlot * q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+            }
+            if (lane < 3 * kMaxC) inc[lane] = win[lane];
+            __syncwarp();
+            obj = best_obj;
+            anchor = best_anchor;
+          }
+        }
+      }
+      if (lane == 0) {
+        double* R = res + warp * rstride;
+        R[0] = obj;
+        R[1] = (double)anchor;
+        for (int q = 0; q < k; ++q) R[2 + q] = (double)ids[q];
+        for (int c = 0; c < 3 * kMaxC; ++c) R[2 + k + c] = anchor >= 0 ? inc[c] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double* best = res + nw * rstride;
+      for (int w2 = 0; w2 < nw && rbase + w2 < cfg.restarts; ++w2) {
+        double* R = res + w2 * rstride;
+        bool first = (rbase + w2) == 0;
+        if (first || R[0] < best[0])
+          for (int t = 0; t < rstride; ++t) best[t] = R[t];
+        if (first && !(R[0] < kInf)) best[0] = kInf;
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0) ctr_flush(ctr);
+  if (threadIdx.x == 0) {
+    double* best = res + nw * rstride;
+    out_obj[a] = best[0];
+    int an = (int)best[1];
+    if (!(best[0] < kInf)) an = -1;
+    out_anchor[a] = an;
+    for (int q = 0; q < k; ++q) out_ids[a * kMaxK + q] = (int)best[2 + q];
+    for (int c = 0; c < 3 * kMaxC; ++c) out_sol[a * 3 * kMaxC + c] = best[2 + k + c];
+    balanced[a] = (an >= 0 && best[0] < eps_stable) ? 1 : 0;
+  }
+}
+
+__host__ __forceinline__ size_t copt2_smem(int k, int nw) {
+  const int per_warp = kMaxC * kSlot + 6 * kMaxC + 32 * 3 * kMaxC;
+  return ((size_t)nw * per_warp + (size_t)(nw + 1) * (2 + k + 3 * kMaxC)) * sizeof(double);
+}
+
+}  // namespace lgd

@@ -255,9 +255,21 @@ __global__ void k_cell_hash_insert(int n_runs, const int* run_start, const int* 
 }
 
 // --------------------------------------------------------------- queries
-// Hits of one transformed sample: calls visit(patch, box_global, best) for
-// every patch whose box at cell(p) passes the >= theta code test, in patch
-// order (contact_field.cpp:412-432).
+// Does box b pass the hit test max_code(-c.n) >= theta (contact_field.cpp:
+// 417-421)?  The max is >= theta iff some code is, so the scan stops at the
+// first such code: the decision is identical to the full max.
+__device__ __forceinline__ bool box_hit(const DField& f, const double* cb, int b, V3 n,
+                                        double theta) {
+  for (long long q = f.box_code_off[b]; q < f.box_code_off[b + 1]; ++q) {
+    int code = f.codes[q];
+    if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) return true;
+  }
+  return false;
+}
+
+// Hits of one transformed sample: calls visit(patch, box_global) for every
+// patch whose box at cell(p) passes the code test, in patch order
+// (contact_field.cpp:412-432).
 template <typename Visit>
 __device__ __forceinline__ void sample_hits(const DField& f, const double* cb, V3 p, V3 n,
                                             double theta, Visit&& visit) {
@@ -268,13 +280,29 @@ __device__ __forceinline__ void sample_hits(const DField& f, const double* cb, V
   int s = f.run_start[r], e = s + f.run_count[r];
   for (int j = s; j < e; ++j) {
     int b = f.cell_box[j];
-    double best = -2.0;
-    for (long long q = f.box_code_off[b]; q < f.box_code_off[b + 1]; ++q) {
-      int code = f.codes[q];
-      best = dmax(best, -dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n));
-    }
-    if (best >= theta) visit(f.box_patch[b], b, best);
+    if (box_hit(f, cb, b, n, theta)) visit(f.box_patch[b], b, 0.0);
   }
+}
+
+// Reachability mask of one transformed sample: bit g set iff some patch of
+// dependency group g has a hit box.  Boxes of static patches and of groups
+// already in the mask cannot change it and are skipped.
+__device__ __forceinline__ uint32_t sample_mask(const DField& f, const double* cb,
+                                                const int* group_of_patch, V3 p, V3 n,
+                                                double theta) {
+  long long c[3];
+  cell_of(p, f.w, c);
+  int r = find_run(f, c);
+  if (r < 0) return 0u;
+  uint32_t bits = 0u;
+  int s = f.run_start[r], e = s + f.run_count[r];
+  for (int j = s; j < e; ++j) {
+    int b = f.cell_box[j];
+    int g = group_of_patch[f.box_patch[b]];
+    if (g < 0 || ((bits >> g) & 1u)) continue;
+    if (box_hit(f, cb, b, n, theta)) bits |= 1u << g;
+  }
+  return bits;
 }
 
 }  // namespace lgd

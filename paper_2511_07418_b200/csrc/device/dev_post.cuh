@@ -1,0 +1,287 @@
+// dev_post.cuh — realisation attempts and postprocess as whole-batch
+// launches (reference pipeline.cpp:465-604).
+//
+// The reference runs lookup attempt a+1 only while no attempt so far is
+// both converged and collision-free, and redraws the unused joints until a
+// configuration is clean.  Both loops almost always run to exhaustion (most
+// candidates never turn penetration-free), so every attempt is evaluated at
+// once and the reference's in-order selection rule is applied on the device
+// afterwards; the kept attempt, and everything derived from it, is identical.
+#pragma once
+
+#include "dev_stages.cuh"
+
+namespace lgd {
+
+// Reverse lookup for (candidate b, attempt, slot) (contact_field.cpp:450-484).
+__global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int k, int A, int c_lo,
+                              int Bsz, int pass, uint64_t seed, DField f,
+                              const int* group_of_patch, const double* patch_pts,
+                              const double* patch_nrm, const int* patch_link, const int* chosen,
+                              const int* opt_ids, const long long* el_off, const double* el_p,
+                              const double* el_n, double theta, double* tgt, int* tgt_link,
+                              int* err) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)nB * A * k) return;
+  int slot = (int)(t % k);
+  int attempt = (int)((t / k) % A);
+  int b = (int)(t / ((long long)k * A));
+  int a = bal[b];
+  int i = alive_idx[a];
+  int g = chosen[i * kMaxK + slot];
+  long long e = el_off[a * k + slot] + opt_ids[a * kMaxK + slot];
+  V3 p = v3_load(el_p + 3 * e), n = v3_load(el_n + 3 * e);
+  int nh = 0;
+  sample_hits(f, f.codebook, p, n, theta, [&](int patch, int, double) {
+    if (group_of_patch[patch] == g) ++nh;
+  });
+  if (nh == 0) {
+    atomicExch(err, 1);
+    return;
+  }
+  uint64_t gid = (uint64_t)pass * Bsz + (uint64_t)(c_lo + i);
+  DRng rng;
+  rng.seed(mix_seed(seed, kTagReverse, (gid << 6) + ((uint64_t)attempt << 3) + (uint64_t)slot));
+  int pick = (int)rng.index((uint64_t)nh);
+  int box = -1, cnt = 0;
+  sample_hits(f, f.codebook, p, n, theta, [&](int patch, int bx, double) {
+    if (group_of_patch[patch] == g) {
+      if (cnt == pick) box = bx;
+      ++cnt;
+    }
+  });
+  int best = -1;
+  double best_dot = -2.0;
+  long long q0 = f.box_code_off[box], q1 = f.box_code_off[box + 1];
+  for (long long q = q0; q < q1; ++q) {
+    int code = f.codes[q];
+    double d = -dot(v3(f.codebook[3 * code], f.codebook[3 * code + 1], f.codebook[3 * code + 2]), n);
+    if (d > best_dot) {
+      best_dot = d;
+      best = (int)(q - q0);
+    }
+  }
+  int rp = f.rep_point[q0 + best];
+  double* T = tgt + (size_t)t * 12;
+  v3_store(T, p);
+  v3_store(T + 3, neg(n));
+  v3_store(T + 6, v3_load(patch_pts + 3 * rp));
+  v3_store(T + 9, v3_load(patch_nrm + 3 * rp));
+  tgt_link[t] = patch_link[f.box_patch[box]];
+}
+
+__global__ void k_conv_flags(int n, const int* finite, const double* res, double tol, int* on) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) on[t] = (finite[t] && res[t] <= tol) ? 1 : 0;
+}
+
+// pipeline.cpp:476-522: walk the attempts in order, keep the better one
+// (clear first, then lower residual), stop at the first clear keeper.
+__global__ void k_attempt_select(int nB, const int* bal, int k, int A, const double* q_try,
+                                 const double* res, const int* finite,
+                                 const unsigned long long* used, const uint8_t* clean,
+                                 const double* tgt, const int* tgt_link, double contact_tol,
+                                 int* have, int* best_clear, double* best_res, double* best_q,
+                                 unsigned long long* best_used, double* best_tgt, int* best_link,
+                                 int* best_attempt, int* attempts_run) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nB) return;
+  int a = bal[b];
+  bool hv = false, bc = false;
+  double br = 0.0;
+  int ba = -1, runs = 0;
+  for (int att = 0; att < A; ++att) {
+    ++runs;
+    int p = b * A + att;
+    if (!finite[p]) continue;
+    bool conv = res[p] <= contact_tol;
+    bool clear = conv ? (clean[p] != 0) : false;
+    bool better;
+    if (!hv) better = true;
+    else if (clear != bc) better = clear;
+    else better = res[p] < br;
+    if (better) {
+      hv = true;
+      bc = clear;
+      br = res[p];
+      ba = att;
+    }
+    if (bc) break;
+  }
+  have[a] = hv;
+  best_clear[a] = bc;
+  best_attempt[a] = ba;
+  attempts_run[a] = runs;
+  if (!hv) return;
+  int p = b * A + ba;
+  best_res[a] = res[p];
+  best_used[a] = used[p];
+  for (int j = 0; j < kMaxDof; ++j) best_q[(size_t)a * kMaxDof + j] = q_try[(size_t)p * kMaxDof + j];
+  for (int c = 0; c < 12 * k; ++c) best_tgt[(size_t)a * kMaxK * 12 + c] = tgt[(size_t)p * k * 12 + c];
+  for (int q = 0; q < k; ++q) best_link[a * kMaxK + q] = tgt_link[p * k + q];
+}
+
+// pipeline.cpp:535-546: every unused-joint redraw of every attempt; attempt j
+// consumes draws [j*nu, (j+1)*nu) of stream 'unus', g.
+__global__ void k_unused_all(int nR, const int* real, const int* alive_idx, int U, int c_lo,
+                             int Bsz, int pass, uint64_t seed, const double* best_q,
+                             const unsigned long long* best_used, double* q_all) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nR) return;
+  int a = real[r];
+  int i = alive_idx[a];
+  uint64_t gid = (uint64_t)pass * Bsz + (uint64_t)(c_lo + i);
+  Mt64 g;
+  mt_seed(g, mix_seed(seed, kTagUnused, gid));
+  unsigned long long used = best_used[a];
+  const int dof = c_hand.dof;
+  for (int att = 0; att < U; ++att) {
+    double* q = q_all + ((size_t)r * U + att) * kMaxDof;
+    for (int j = 0; j < dof; ++j) {
+      q[j] = best_q[(size_t)a * kMaxDof + j];
+      if ((used >> j) & 1ull) continue;
+      q[j] = c_hand.jlo[j] + (c_hand.jhi[j] - c_hand.jlo[j]) * u01(mt_next(g));
+    }
+  }
+}
+
+// First clean redraw, else the last one (pipeline.cpp:538-551).
+__global__ void k_unused_select(int nR, const int* real, int U, const double* q_all,
+                                const uint8_t* clean, double* final_q, uint8_t* final_clean,
+                                int* uatt) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nR) return;
+  int a = real[r];
+  int sel = U - 1;
+  for (int att = 0; att < U; ++att)
+    if (clean[(size_t)r * U + att]) {
+      sel = att;
+      break;
+    }
+  uatt[a] = sel;
+  final_clean[a] = clean[(size_t)r * U + sel];
+  for (int j = 0; j < kMaxDof; ++j)
+    final_q[(size_t)a * kMaxDof + j] = q_all[((size_t)r * U + sel) * kMaxDof + j];
+}
+
+// Postprocess (pipeline.cpp:553-603), one warp per candidate: lanes < k
+// re-project the targets, all lanes split each nearest-sample scan (argmin
+// with lowest index on ties), lanes < n run one anchor each of the cold
+// stability solve.
+__global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, FinalCfg C,
+                                DSamples fs, const double* pose, const int* n_static,
+                                const int* st_link, const double* st_p, const double* st_n,
+                                const double* q_final, const uint8_t* clean,
+                                const double* best_tgt, const int* best_link, lg_grasp* out,
+                                int* valid, int* dropped) {
+  __shared__ double s_q[4][kMaxDof];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int t = blockIdx.x * (blockDim.x >> 5) + w;
+  if (t >= nT) return;
+  const int a = act[t];
+  const int i = alive_idx[a];
+  const int k = C.k;
+  if (lane < c_hand.dof) s_q[w][lane] = q_final[(size_t)a * kMaxDof + lane];
+  __syncwarp();
+  Xf f = wfk(s_q[w], lane);
+  Xf x = load_xf(pose + 12 * i);
+  // re-projection at the final q: lane s < k
+  int link = lane < k ? best_link[a * kMaxK + lane] : 0;
+  Xf F = shfl_xf(f, link);
+  double d = 0.0;
+  V3 pw = v3(0, 0, 0);
+  if (lane < k) {
+    const double* T = best_tgt + (size_t)a * kMaxK * 12 + 12 * lane;
+    Xf inv = xf_inverse(F);
+    V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
+    d = closest_on_parts(link, xf_apply(inv, v3_load(T)), &sp, &sn);
+    pw = xf_apply(F, sp);
+  }
+  // reference: the first non-finite distance (slot order) drops the candidate
+  bool nonfin = lane < k && !is_finite(d);
+  lg_grasp& g = out[a];
+  if (__any_sync(kFull, nonfin)) {
+    if (lane == 0) {
+      dropped[a] = 1;
+      valid[a] = 0;
+    }
+    return;
+  }
+  double worst = warp_max_d(lane < k ? d : 0.0);
+  for (int s = 0; s < k; ++s) {
+    V3 ps = v3(__shfl_sync(kFull, pw.x, s), __shfl_sync(kFull, pw.y, s), __shfl_sync(kFull, pw.z, s));
+    double bd = kInf;
+    int bi = 0x7fffffff;
+    for (int j = lane; j < fs.n; j += 32) {
+      double d2 = sqnorm(sub(xf_apply(x, fs.p(j)), ps));
+      if (d2 < bd) {
+        bd = d2;
+        bi = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double od = __shfl_xor_sync(kFull, bd, o);
+      int oi = __shfl_xor_sync(kFull, bi, o);
+      if (od < bd || (od == bd && oi < bi)) {
+        bd = od;
+        bi = oi;
+      }
+    }
+    int nearest = bi == 0x7fffffff ? 0 : bi;
+    if (lane == 0) {
+      v3_store(g.contact_p[s], ps);
+      v3_store(g.contact_n[s], neg(xf_rotate(x, fs.nrm(nearest))));
+      g.contact_link[s] = best_link[a * kMaxK + s];
+    }
+  }
+  int nc = k;
+  if (n_static[i]) {
+    if (lane == 0) {
+      v3_store(g.contact_p[k], v3_load(st_p + 3 * i));
+      v3_store(g.contact_n[k], v3_load(st_n + 3 * i));
+      g.contact_link[k] = st_link[i];
+    }
+    nc = k + 1;
+  }
+  __syncwarp();
+  // is_stable (wrench.cpp:260-267): cold GSWO, lanes over anchors
+  WProb wp;
+  wp.n = nc;
+  wp.lambda = C.lambda;
+  wp.mu = C.mu;
+  for (int c = 0; c < nc; ++c) wprob_set(wp, c, v3_load(g.contact_p[c]), v3_load(g.contact_n[c]));
+  Ctr ctr = {0, 0, 0, 0, 0};
+  WState st;
+  double val = kInf;
+  if (lane < nc) val = wsolve_anchor(wp, lane, wp.mu > 0.0, C.o, nullptr, st, ctr);
+  if (!(val < kInf)) val = kInf;
+  double best = val;
+  int bl = val < kInf ? lane : 99;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(kFull, best, o);
+    int ol = __shfl_xor_sync(kFull, bl, o);
+    if (ov < best || (ov == best && ol < bl)) {
+      best = ov;
+      bl = ol;
+    }
+  }
+  ctr_flush(ctr);
+  if (lane == 0) {
+    g.n_contacts = nc;
+    g.ik_converged = worst <= C.contact_tol;
+    g.penetration_free = clean[a] ? 1 : 0;
+    g.objective = best;
+    g.stable = best < C.eps ? 1 : 0;
+    g.g = 0;
+    m3_store(g.pose_R, x.R);
+    v3_store(g.pose_t, x.t);
+    g.dof = c_hand.dof;
+    for (int j = 0; j < c_hand.dof; ++j) g.q[j] = s_q[w][j];
+    dropped[a] = 0;
+    valid[a] = (g.penetration_free && g.stable && g.ik_converged) ? 1 : 0;
+  }
+}
+
+}  // namespace lgd

@@ -251,11 +251,7 @@ __global__ void k_query(int Bl, DField f, const int* group_of_patch, DSamples fs
   for (int j = threadIdx.x; j < fs.n; j += blockDim.x) {
     V3 p = xf_apply(x, fs.p(j));
     V3 n = xf_rotate(x, fs.nrm(j));
-    uint32_t bits = 0u;
-    sample_hits(f, cb, p, n, theta, [&](int patch, int, double) {
-      int g = group_of_patch[patch];
-      if (g >= 0) bits |= 1u << g;
-    });
+    uint32_t bits = sample_mask(f, cb, group_of_patch, p, n, theta);
     m[j] = bits;
     while (bits) {
       int g = __ffs(bits) - 1;

@@ -11,11 +11,14 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
 #include "../capi_common.hpp"
-#include "dev_stages.cuh"
+#include "dev_copt.cuh"
+#include "dev_post.cuh"
 
 using namespace lgd;
 
@@ -29,22 +32,48 @@ namespace {
   } while (0)
 
 // ---------------------------------------------------------------- buffers
+// Stream-ordered allocations from the device's default pool (release
+// threshold raised at context creation), so per-call scratch is recycled
+// without device-wide synchronisation.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+std::mutex g_streams_mu;
+std::set<cudaStream_t> g_live_streams;  // streams of live contexts
+
+void free_on(void* p, cudaStream_t s) {
+  bool live;
+  {
+    std::lock_guard<std::mutex> lk(g_streams_mu);
+    live = g_live_streams.count(s) != 0;
+  }
+  // a buffer that outlives its context (e.g. a field destroyed after the
+  // context) is freed synchronously instead of on the dead stream
+  if (!live || cudaFreeAsync(p, s) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+  }
+}
+
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   Buf() = default;
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
-  ~Buf() {
-    if (p) cudaFree(p);
+  ~Buf() { release(); }
+  void release() {
+    if (p) free_on(p, s);
+    p = nullptr;
+    n = 0;
   }
   void alloc(size_t bytes) {
     if (bytes <= n && p) return;
-    if (p) cudaFree(p);
+    if (p) free_on(p, s);
     p = nullptr;
     n = 0;
     if (bytes == 0) bytes = 8;
-    CK(cudaMalloc(&p, bytes));
+    s = g_alloc_stream;
+    CK(cudaMallocAsync(&p, bytes, s));
     n = bytes;
   }
   template <typename T>
@@ -162,6 +191,11 @@ struct lg_ctx {
 };
 
 namespace {
+
+void use_ctx(lg_ctx* ctx) {
+  CK(cudaSetDevice(ctx->device));
+  g_alloc_stream = ctx->stream;
+}
 
 #define LAUNCH(ctx) ++(ctx)->launches
 
@@ -841,11 +875,16 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     co.per_restart = per_restart;
     co.per_cand = per_cand;
     int nw = std::min(R, 8);
-    size_t co_smem = (size_t)(nw + 1) * (2 + k + 3 * kMaxC) * sizeof(double);
+    size_t co_smem = copt2_smem(k, nw);
+    static bool co_attr = false;
+    if (!co_attr) {
+      CK(cudaFuncSetAttribute(k_contact_opt2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      co_attr = true;
+    }
     tk.start();
-    k_contact_opt<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_els,
-                                               d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan, d_osol,
-                                               cfg.eps_stable, d_bal);
+    k_contact_opt2<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp,
+                                                d_eln, d_draws, d_oid, d_oobj, d_oan, d_osol,
+                                                cfg.eps_stable, d_bal);
     LAUNCH(ctx);
     check_launch();
     copt_s += tk.stop();
@@ -896,62 +935,57 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     CK(cudaMemsetAsync(d_bclear, 0, sizeof(int) * nA, s));
     CK(cudaMemsetAsync(d_bq, 0, sizeof(double) * nA * kMaxDof, s));
     CK(cudaMemsetAsync(d_batt, 0xff, sizeof(int) * nA, s));
-    std::vector<int> searching(nA, 0), attempts_run(nA, 0);
-    for (int a : bal_list) searching[a] = 1;
-    Buf b_act, b_tgt, b_tl, b_qt, b_res, b_fin, b_used, b_clean, b_on, b_cand, b_err;
+    (void)d_search;
+    Buf b_bal_l, b_tgt, b_tl, b_qt, b_res, b_fin, b_used, b_clean, b_on, b_cand, b_err, b_runs_d;
     int* d_err = dalloc<int>(b_err, 1);
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-    for (int attempt = 0; attempt < cfg.lookup_attempts; ++attempt) {
-      std::vector<int> act;
-      for (int a = 0; a < nA; ++a)
-        if (searching[a]) act.push_back(a);
-      if (act.empty()) break;
-      for (int a : act) ++attempts_run[a];
-      const int nAct = (int)act.size();
-      CK(cudaMemcpyAsync(d_search, searching.data(), sizeof(int) * nA, cudaMemcpyHostToDevice, s));
-      int* d_act = dupload(b_act, act.data(), act.size(), s);
-      double* d_tgt = dalloc<double>(b_tgt, (size_t)nAct * k * 12);
-      int* d_tl = dalloc<int>(b_tl, (size_t)nAct * k);
-      k_targets<<<grid_for((long long)nAct * k, 128), 128, 0, s>>>(
-          nAct, d_act, d_aidx, k, attempt, c_lo, B, pass, cfg.seed, F, d_gop, DP.pts.as<double>(),
+    int* d_runs = dalloc<int>(b_runs_d, (size_t)nA);
+    CK(cudaMemsetAsync(d_runs, 0, sizeof(int) * nA, s));
+    const int nB = (int)bal_list.size();
+    const int LA = cfg.lookup_attempts;
+    const long long nP = (long long)nB * LA;  // every (candidate, attempt) problem
+    if (nB > 0) {
+      int* d_bl = dupload(b_bal_l, bal_list.data(), bal_list.size(), s);
+      double* d_tgt = dalloc<double>(b_tgt, (size_t)nP * k * 12);
+      int* d_tl = dalloc<int>(b_tl, (size_t)nP * k);
+      k_targets_all<<<grid_for(nP * k, 128), 128, 0, s>>>(
+          nB, d_bl, d_aidx, k, LA, c_lo, B, pass, cfg.seed, F, d_gop, DP.pts.as<double>(),
           DP.nrm.as<double>(), DP.link.as<int>(), d_chosen, d_oid, d_eloff, d_elp, d_eln,
           cfg.theta_hit, d_tgt, d_tl, d_err);
       LAUNCH(ctx);
       check_launch();
-      double* d_qt = dalloc<double>(b_qt, (size_t)nAct * kMaxDof);
-      double* d_res = dalloc<double>(b_res, (size_t)nAct);
-      int* d_fin = dalloc<int>(b_fin, (size_t)nAct);
-      auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nAct);
+      double* d_qt = dalloc<double>(b_qt, (size_t)nP * kMaxDof);
+      double* d_res = dalloc<double>(b_res, (size_t)nP);
+      int* d_fin = dalloc<int>(b_fin, (size_t)nP);
+      auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nP);
       tk.start();
-      launch_realize_warp(s, nAct, k, nullptr, ikc, cfg.finetune_rounds, cfg.finetune_iterations,
+      launch_realize_warp(s, (int)nP, k, nullptr, ikc, cfg.finetune_rounds, cfg.finetune_iterations,
                           d_tgt, k * 12, d_tl, k, nullptr, d_qt, d_res, d_fin, d_used, hd.dof);
       LAUNCH(ctx);
       check_launch();
       realize_s += tk.stop();
-      out.profile.realize_calls += nAct;
-      auto h_fin = ddownload(d_fin, (size_t)nAct, s);
-      auto h_res = ddownload(d_res, (size_t)nAct, s);
-      std::vector<int> on(nAct), cand(nAct);
-      for (int t = 0; t < nAct; ++t) {
-        on[t] = (h_fin[t] && h_res[t] <= cfg.contact_tol) ? 1 : 0;
-        cand[t] = alive_idx[act[t]];
-      }
-      int* d_on = dupload(b_on, on.data(), on.size(), s);
+      out.profile.realize_calls += nP;
+      int* d_on = dalloc<int>(b_on, (size_t)nP);
+      k_conv_flags<<<grid_for(nP, 256), 256, 0, s>>>((int)nP, d_fin, d_res, cfg.contact_tol, d_on);
+      LAUNCH(ctx);
+      std::vector<int> cand(nP);
+      for (long long p = 0; p < nP; ++p) cand[p] = alive_idx[bal_list[p / LA]];
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
-      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
-      CK(cudaMemsetAsync(d_clean, 0, nAct, s));
-      for (int t = 0; t < nAct; ++t) out.profile.collision_calls += on[t];
-      k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, d_on, d_qt, d_pose, d_aabb, d_clean, nullptr);
+      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nP);
+      CK(cudaMemsetAsync(d_clean, 0, nP, s));
+      k_collision<<<(int)nP, 128, 0, s>>>((int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, d_clean,
+                                           nullptr);
       LAUNCH(ctx);
       check_launch();
-      k_attempt_update<<<grid_for(nAct, 128), 128, 0, s>>>(
-          nAct, d_act, k, attempt, d_qt, d_res, d_fin, d_used, d_clean, d_on, d_tgt, d_tl,
-          cfg.contact_tol, d_have, d_bclear, d_bres, d_bq, d_bused, d_btgt, d_blink, d_batt, d_search);
+      k_attempt_select<<<grid_for(nB, 128), 128, 0, s>>>(
+          nB, d_bl, k, LA, d_qt, d_res, d_fin, d_used, d_clean, d_tgt, d_tl, cfg.contact_tol, d_have,
+          d_bclear, d_bres, d_bq, d_bused, d_btgt, d_blink, d_batt, d_runs);
       LAUNCH(ctx);
       check_launch();
-      auto h_search = ddownload(d_search, (size_t)nA, s);
-      for (int a = 0; a < nA; ++a) searching[a] = h_search[a];
+      auto h_on = ddownload(d_on, (size_t)nP, s);
+      for (long long p = 0; p < nP; ++p) out.profile.collision_calls += h_on[p];
     }
+    std::vector<int> attempts_run = ddownload(d_runs, (size_t)nA, s);
     int herr = 0;
     CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     auto h_have = ddownload(d_have, (size_t)nA, s);
@@ -995,50 +1029,42 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
 
     // -------- stage 4: unused-joint redraws + postprocess
     tm.start();
-    Buf b_fq, b_fclean, b_uatt, b_grasp, b_valid, b_drop;
+    Buf b_fq, b_fclean, b_uatt, b_grasp, b_valid, b_drop, b_act_r, b_qall;
     double* d_fq = dalloc<double>(b_fq, (size_t)nA * kMaxDof);
     uint8_t* d_fclean = dalloc<uint8_t>(b_fclean, (size_t)nA);
-    std::vector<int> uatt(nA, -1), uclean(nA, 0);
-    std::vector<int> pending = real_list;
-    std::vector<double> fq_h((size_t)nA * kMaxDof, 0.0);
-    for (int attempt = 0; attempt < cfg.unused_attempts && !pending.empty(); ++attempt) {
-      const int nAct = (int)pending.size();
-      int* d_act = dupload(b_act, pending.data(), pending.size(), s);
-      double* d_qt = dalloc<double>(b_qt, (size_t)nAct * kMaxDof);
-      k_unused_q<<<grid_for(nAct, 64), 64, 0, s>>>(nAct, d_act, d_aidx, attempt, c_lo, B, pass,
-                                                   cfg.seed, d_bq, d_bused, d_qt);
-      LAUNCH(ctx);
-      check_launch();
-      std::vector<int> cand(nAct);
-      for (int t = 0; t < nAct; ++t) cand[t] = alive_idx[pending[t]];
+    const int nR = (int)real_list.size();
+    const int UA = cfg.unused_attempts;
+    const long long nU = (long long)nR * UA;  // every (candidate, redraw) configuration
+    int* d_real = dupload(b_act_r, real_list.data(), real_list.size(), s);
+    double* d_qall = dalloc<double>(b_qall, (size_t)nU * kMaxDof);
+    k_unused_all<<<grid_for(nR, 64), 64, 0, s>>>(nR, d_real, d_aidx, UA, c_lo, B, pass, cfg.seed, d_bq,
+                                                 d_bused, d_qall);
+    LAUNCH(ctx);
+    check_launch();
+    {
+      std::vector<int> cand(nU);
+      for (long long u = 0; u < nU; ++u) cand[u] = alive_idx[real_list[u / UA]];
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
-      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nAct);
-      out.profile.collision_calls += nAct;
-      k_collision<<<nAct, 128, 0, s>>>(nAct, cc, d_cand, nullptr, d_qt, d_pose, d_aabb, d_clean, nullptr);
+      uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nU);
+      out.profile.collision_calls += nU;
+      k_collision<<<(int)nU, 128, 0, s>>>((int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, d_clean,
+                                           nullptr);
       LAUNCH(ctx);
       check_launch();
-      auto h_clean = ddownload(d_clean, (size_t)nAct, s);
-      auto h_qt = ddownload(d_qt, (size_t)nAct * kMaxDof, s);
-      std::vector<int> next;
-      for (int t = 0; t < nAct; ++t) {
-        int a = pending[t];
-        uatt[a] = attempt;
-        uclean[a] = h_clean[t];
-        std::memcpy(&fq_h[(size_t)a * kMaxDof], &h_qt[(size_t)t * kMaxDof], kMaxDof * sizeof(double));
-        if (!h_clean[t]) next.push_back(a);
-      }
-      pending.swap(next);
+      int* d_uatt_d = dalloc<int>(b_uatt, (size_t)nA);
+      CK(cudaMemsetAsync(d_uatt_d, 0xff, sizeof(int) * nA, s));
+      CK(cudaMemsetAsync(d_fclean, 0, nA, s));
+      k_unused_select<<<grid_for(nR, 128), 128, 0, s>>>(nR, d_real, UA, d_qall, d_clean, d_fq, d_fclean,
+                                                        d_uatt_d);
+      LAUNCH(ctx);
+      check_launch();
     }
-    dupload(b_fq, fq_h.data(), fq_h.size(), s);
-    std::vector<uint8_t> ucl8(nA);
-    for (int a = 0; a < nA; ++a) ucl8[a] = (uint8_t)uclean[a];
-    dupload(b_fclean, ucl8.data(), ucl8.size(), s);
     lg_grasp* d_grasp = dalloc<lg_grasp>(b_grasp, (size_t)nA);
     int* d_valid = dalloc<int>(b_valid, (size_t)nA);
     int* d_drop = dalloc<int>(b_drop, (size_t)nA);
     CK(cudaMemsetAsync(d_grasp, 0, sizeof(lg_grasp) * nA, s));
     CK(cudaMemsetAsync(d_valid, 0, sizeof(int) * nA, s));
-    int* d_act = dupload(b_act, real_list.data(), real_list.size(), s);
+    CK(cudaMemsetAsync(d_drop, 0, sizeof(int) * nA, s));
     FinalCfg fc;
     fc.k = k;
     fc.contact_tol = cfg.contact_tol;
@@ -1046,11 +1072,14 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     fc.mu = cfg.mu;
     fc.eps = cfg.eps_stable;
     fc.o = wo;
-    k_finalize<<<grid_for((long long)real_list.size(), 32), 32, 0, s>>>(
-        (int)real_list.size(), d_act, d_aidx, fc, FS, d_pose, d_nst, d_stl, d_stp, d_stn, b_fq.as<double>(),
-        b_fclean.as<uint8_t>(), d_btgt, d_blink, d_grasp, d_valid, d_drop);
+    k_finalize_warp<<<(nR + 3) / 4, 128, 0, s>>>(nR, d_real, d_aidx, fc, FS, d_pose, d_nst, d_stl, d_stp,
+                                                 d_stn, d_fq, d_fclean, d_btgt, d_blink, d_grasp,
+                                                 d_valid, d_drop);
     LAUNCH(ctx);
     check_launch();
+    std::vector<int> uatt = ddownload(b_uatt.as<int>(), (size_t)nA, s);
+    std::vector<double> fq_h;
+    if (cfg.want_trace) fq_h = ddownload(d_fq, (size_t)nA * kMaxDof, s);
     auto h_grasp = ddownload(d_grasp, (size_t)nA, s);
     auto h_valid = ddownload(d_valid, (size_t)nA, s);
     auto h_drop = ddownload(d_drop, (size_t)nA, s);
@@ -1176,7 +1205,7 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
     for (int i = 0; i < m; ++i)
       if (n[i] < 1 || n[i] > kMaxC) throw std::invalid_argument("wrench solve: 1..6 contacts");
     if (m == 0) return;
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     Buf bn, bp, bq, bo, ba, bs;
     int* d_n = dupload(bn, n, (size_t)m, s);
@@ -1211,7 +1240,7 @@ int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const doubl
     if (!ctx || !hand || m < 0) throw std::invalid_argument("lg_collision_batch: bad argument");
     if (margin < 0.0) throw std::invalid_argument("broad_phase: negative margin");
     if (m == 0) return;
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     bind_hand(ctx, *hand);
     std::vector<double> col(std::max(n, 1));
@@ -1262,7 +1291,7 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
     if (!ctx || !hand || m < 0) throw std::invalid_argument("lg_realize_batch: bad argument");
     if (beta <= 0.0) throw std::invalid_argument("solve_contact_ik: beta must be > 0");
     if (m == 0) return;
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     bind_hand(ctx, *hand);
     std::vector<double> tg((size_t)m * kMaxK * 12, 0.0);
@@ -1346,6 +1375,15 @@ int lg_ctx_create(int device, lg_ctx** out) {
       delete c;
       throw lgc::cuda_error(std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
     }
+    {
+      std::lock_guard<std::mutex> lk(g_streams_mu);
+      g_live_streams.insert(c->stream);
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;  // keep freed blocks cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     *out = c;
   });
 }
@@ -1353,8 +1391,19 @@ int lg_ctx_create(int device, lg_ctx** out) {
 void lg_ctx_destroy(lg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (Buf* b : {&ctx->h_vert_off, &ctx->h_verts, &ctx->h_tri_off, &ctx->h_tris, &ctx->h_plane_off,
+                 &ctx->h_planes, &ctx->h_bounds, &ctx->h_part_link})
+    b->release();
   if (ctx->cub_tmp) cudaFree(ctx->cub_tmp);
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    {
+      std::lock_guard<std::mutex> lk(g_streams_mu);
+      g_live_streams.erase(ctx->stream);
+    }
+    cudaStreamDestroy(ctx->stream);
+  }
   delete ctx;
 }
 
@@ -1362,7 +1411,7 @@ int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc*
                    double w, uint64_t seed, int C, lg_field** out) {
   return lgc::guard([&] {
     if (!ctx || !hand || !patches || !out) throw std::invalid_argument("lg_field_build: null argument");
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     auto f = std::make_unique<lg_field>();
     f->ctx = ctx;
     build_field_device(ctx, *hand, *patches, N, w, seed, C, f.get());
@@ -1420,7 +1469,7 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
                            uint32_t* masks, double* scores) {
   return lgc::guard([&] {
     if (!ctx || !f || !samples || !poses || !masks) throw std::invalid_argument("lg_query_domains_batch: null argument");
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     std::vector<double> col(n);
     Buf sc[6];
@@ -1452,7 +1501,7 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
 int lg_preprocess(lg_ctx* ctx, const double* samples, int n, double h, double d, uint8_t* keep) {
   return lgc::guard([&] {
     if (h <= 0.0 || d < 0.0) throw std::invalid_argument("preprocess_object: bad probe dimensions");
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     std::vector<double> col(n);
     Buf sc[6], bk;
@@ -1474,7 +1523,7 @@ int lg_run_batch_field(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_d
                        lg_result** out) {
   return lgc::guard([&] {
     if (!ctx || !hand || !patches || !raw || !p || !out) throw std::invalid_argument("lg_run_batch: null argument");
-    CK(cudaSetDevice(ctx->device));
+    use_ctx(ctx);
     auto r = std::make_unique<lg_result>();
     run_batch_device(ctx, *hand, *patches, field, raw, n_raw, *p, r->r);
     *out = r.release();
