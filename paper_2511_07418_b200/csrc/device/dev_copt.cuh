@@ -1,16 +1,18 @@
 // dev_copt.cuh — optimize_contacts (reference contact_opt.cpp:45-142) with a
 // register-lean wrench solver (wrench.cpp:124-226).
 //
-// Layout per warp (one warp = one restart):
-//   shared  : incumbent problem, k + s contacts x (p, n, tx, ty, p x n,
-//             p x tx, p x ty) = 21 doubles each; incumbent solution
-//             (alpha, beta_x, beta_y); per-lane best solver state.
-//   registers: the lane's trial slot (21 doubles) and its solver state.
+// Layout per warp (one warp = one restart), all in shared memory:
+//   incumbent problem  k + s contacts x (p, n, tx, ty, p x n, p x tx, p x ty)
+//                      = 21 doubles each;
+//   each lane's trial slot (21 doubles) and solver state (alpha, beta_x,
+//   beta_y); the incumbent solution (warm start) and the step's winner.
 // The solver never stores the backtracking trial state or the gradient:
 // projection is per contact, so trial_i = project_i(s_i - step g_i) is
 // computed, projected and accumulated contact by contact, and recomputed
-// with identical arithmetic when accepted.  Every sum keeps the oracle's
-// order, so results stay bit-identical.
+// with identical arithmetic when accepted.  In the frictionless descent the
+// beta terms are exactly zero and are skipped: force/torque accumulators
+// start at +0 and x + (+-0) == x, so every sum is unchanged bit for bit.
+// Every other sum keeps the oracle's order (bit-identical results).
 #pragma once
 
 #include "dev_stages.cuh"
@@ -19,15 +21,17 @@ namespace lgd {
 
 constexpr int kSlot = 21;
 
-// Problem view: contacts from shared memory except slot `tq` (registers).
+// Problem view: contacts from shared memory, slot `tq` from the lane's own
+// trial record.
 struct PV {
   const double* sp;
+  const double* ts;
   int n, tq;
   double lambda, mu;
-  double tv[kSlot];
-  __device__ __forceinline__ double g(int i, int c) const { return i == tq ? tv[c] : sp[kSlot * i + c]; }
-  __device__ __forceinline__ V3 v(int i, int c) const { return v3(g(i, c), g(i, c + 1), g(i, c + 2)); }
+  __device__ __forceinline__ const double* slot(int i) const { return i == tq ? ts : sp + kSlot * i; }
 };
+
+__device__ __forceinline__ V3 ld3(const double* p) { return v3(p[0], p[1], p[2]); }
 
 // write_slot (contact_opt.cpp:31-35) into a 21-double slot record.
 __device__ __forceinline__ void slot_make(double* o, V3 p, V3 n) {
@@ -43,11 +47,12 @@ __device__ __forceinline__ void slot_make(double* o, V3 p, V3 n) {
   v3_store(o + 18, cy);
 }
 
-__device__ __forceinline__ void proj_one(bool is_anchor, bool fr, double mu, double& a, double& bx,
+template <bool FR>
+__device__ __forceinline__ void proj_one(bool is_anchor, double mu, double& a, double& bx,
                                          double& by) {
   if (is_anchor) a = 1.0;
   else if (a < 0.0) a = 0.0;
-  if (!fr) {
+  if (!FR) {
     bx = 0.0;
     by = 0.0;
     return;
@@ -66,73 +71,63 @@ __device__ __forceinline__ void proj_one(bool is_anchor, bool fr, double mu, dou
   }
 }
 
-__device__ __forceinline__ void pv_net(const PV& w, const double* a, const double* bx,
-                                       const double* by, V3& f, V3& t) {
-  f = v3(0.0, 0.0, 0.0);
-  t = v3(0.0, 0.0, 0.0);
-#pragma unroll
-  for (int i = 0; i < kMaxC; ++i) {
-    if (i < w.n) {
-      f = add(f, add(add(scale(a[i], w.v(i, 3)), scale(bx[i], w.v(i, 6))), scale(by[i], w.v(i, 9))));
-      t = add(t, add(add(scale(a[i], w.v(i, 12)), scale(bx[i], w.v(i, 15))), scale(by[i], w.v(i, 18))));
-    }
+// force += a n + bx tx + by ty ; torque += a cn + bx cx + by cy
+template <bool FR>
+__device__ __forceinline__ void acc_contact(const double* s, double a, double bx, double by, V3& f,
+                                            V3& t) {
+  if (FR) {
+    f = add(f, add(add(scale(a, ld3(s + 3)), scale(bx, ld3(s + 6))), scale(by, ld3(s + 9))));
+    t = add(t, add(add(scale(a, ld3(s + 12)), scale(bx, ld3(s + 15))), scale(by, ld3(s + 18))));
+  } else {
+    f = add(f, scale(a, ld3(s + 3)));
+    t = add(t, scale(a, ld3(s + 12)));
   }
 }
 
-// descend (wrench.cpp:124-177) on state (a, bx, by) in registers.
-__device__ double pv_descend(const PV& w, int anchor, bool fr, int iterations, double step0,
-                             int max_bt, double* a, double* bx, double* by, Ctr& ctr) {
-#pragma unroll
-  for (int i = 0; i < kMaxC; ++i)
-    if (i < w.n) proj_one(i == anchor, fr, w.mu, a[i], bx[i], by[i]);
-  V3 f, t;
-  pv_net(w, a, bx, by, f, t);
+// descend (wrench.cpp:124-177) on state (a, bx, by) in shared memory.
+template <bool FR>
+__device__ double pv_descend(const PV& w, int anchor, int iterations, double step0, int max_bt,
+                             double* a, double* bx, double* by, Ctr& ctr) {
+  for (int i = 0; i < w.n; ++i) proj_one<FR>(i == anchor, w.mu, a[i], bx[i], by[i]);
+  V3 f = v3(0.0, 0.0, 0.0), t = v3(0.0, 0.0, 0.0);
+  for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], f, t);
   double current = sqnorm(f) + w.lambda * sqnorm(t);
   ++ctr.weval;
   for (int it = 0; it < iterations; ++it) {
-    V3 force, torque;
-    pv_net(w, a, bx, by, force, torque);
+    V3 force = v3(0.0, 0.0, 0.0), torque = v3(0.0, 0.0, 0.0);
+    for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], force, torque);
     ++ctr.wgrad;
     torque = v3(torque.x * w.lambda, torque.y * w.lambda, torque.z * w.lambda);
     double step = step0;
     bool moved = false;
     for (int bt = 0; bt <= max_bt; ++bt) {
       V3 f2 = v3(0.0, 0.0, 0.0), t2 = v3(0.0, 0.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < kMaxC; ++i) {
-        if (i < w.n) {
-          double ga = 2.0 * (dot(force, w.v(i, 3)) + dot(torque, w.v(i, 12)));
-          double ta = a[i] - step * ga, tbx = 0.0, tby = 0.0;
-          if (fr) {
-            double gx = 2.0 * (dot(force, w.v(i, 6)) + dot(torque, w.v(i, 15)));
-            double gy = 2.0 * (dot(force, w.v(i, 9)) + dot(torque, w.v(i, 18)));
-            tbx = bx[i] - step * gx;
-            tby = by[i] - step * gy;
-          }
-          proj_one(i == anchor, fr, w.mu, ta, tbx, tby);
-          f2 = add(f2, add(add(scale(ta, w.v(i, 3)), scale(tbx, w.v(i, 6))), scale(tby, w.v(i, 9))));
-          t2 = add(t2, add(add(scale(ta, w.v(i, 12)), scale(tbx, w.v(i, 15))), scale(tby, w.v(i, 18))));
+      for (int i = 0; i < w.n; ++i) {
+        const double* s = w.slot(i);
+        double ta = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
+        double tbx = 0.0, tby = 0.0;
+        if (FR) {
+          tbx = bx[i] - step * (2.0 * (dot(force, ld3(s + 6)) + dot(torque, ld3(s + 15))));
+          tby = by[i] - step * (2.0 * (dot(force, ld3(s + 9)) + dot(torque, ld3(s + 18))));
         }
+        proj_one<FR>(i == anchor, w.mu, ta, tbx, tby);
+        acc_contact<FR>(s, ta, tbx, tby, f2, t2);
       }
       double next = sqnorm(f2) + w.lambda * sqnorm(t2);
       ++ctr.weval;
       if (next <= current) {
-#pragma unroll
-        for (int i = 0; i < kMaxC; ++i) {
-          if (i < w.n) {
-            double ga = 2.0 * (dot(force, w.v(i, 3)) + dot(torque, w.v(i, 12)));
-            double ta = a[i] - step * ga, tbx = 0.0, tby = 0.0;
-            if (fr) {
-              double gx = 2.0 * (dot(force, w.v(i, 6)) + dot(torque, w.v(i, 15)));
-              double gy = 2.0 * (dot(force, w.v(i, 9)) + dot(torque, w.v(i, 18)));
-              tbx = bx[i] - step * gx;
-              tby = by[i] - step * gy;
-            }
-            proj_one(i == anchor, fr, w.mu, ta, tbx, tby);
-            a[i] = ta;
-            bx[i] = tbx;
-            by[i] = tby;
+        for (int i = 0; i < w.n; ++i) {
+          const double* s = w.slot(i);
+          double ta = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
+          double tbx = 0.0, tby = 0.0;
+          if (FR) {
+            tbx = bx[i] - step * (2.0 * (dot(force, ld3(s + 6)) + dot(torque, ld3(s + 15))));
+            tby = by[i] - step * (2.0 * (dot(force, ld3(s + 9)) + dot(torque, ld3(s + 18))));
           }
+          proj_one<FR>(i == anchor, w.mu, ta, tbx, tby);
+          a[i] = ta;
+          bx[i] = tbx;
+          by[i] = tby;
         }
         current = next;
         moved = true;
@@ -146,31 +141,33 @@ __device__ double pv_descend(const PV& w, int anchor, bool fr, int iterations, d
 }
 
 // One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
-// warm-started from `warm` ([3][kMaxC], shared memory).
+// warm-started from `warm` ([3][kMaxC]); state st = [3][kMaxC].
 __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts& o,
-                                            const double* warm, double* a, double* bx, double* by,
-                                            Ctr& ctr) {
-  const bool fr = w.mu > 0.0;
+                                            const double* warm, double* st, Ctr& ctr) {
   const int iters = warm ? o.warm_iterations : o.iterations;
-#pragma unroll
-  for (int i = 0; i < kMaxC; ++i) {
+  double* a = st;
+  double* bx = st + kMaxC;
+  double* by = st + 2 * kMaxC;
+  for (int i = 0; i < w.n; ++i) {
     a[i] = warm ? warm[i] : 1.0;
     bx[i] = warm ? warm[kMaxC + i] : 0.0;
     by[i] = warm ? warm[2 * kMaxC + i] : 0.0;
   }
-  if (fr) {
-    pv_descend(w, anchor, false, iters, o.step, o.max_bt, a, bx, by, ctr);
-    return pv_descend(w, anchor, true, iters, o.step, o.max_bt, a, bx, by, ctr);
+  if (w.mu > 0.0) {
+    pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
+    return pv_descend<true>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
   }
-  return pv_descend(w, anchor, false, iters, o.step, o.max_bt, a, bx, by, ctr);
+  return pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
 }
 
+constexpr int kCoptPerWarp = kMaxC * kSlot + 6 * kMaxC + 32 * (kSlot + 6 * kMaxC);
+
 // Block per candidate, warp per restart, lanes over the n_inner mutations.
-__global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static,
-                               const double* st_p, const double* st_n, const long long* el_off,
-                               const double* el_p, const double* el_n, const uint64_t* draws,
-                               int* out_ids, double* out_obj, int* out_anchor, double* out_sol,
-                               double eps_stable, int* balanced) {
+__global__ void __launch_bounds__(128, 4)
+k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
+               const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
+               const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
+               double* out_sol, double eps_stable, int* balanced) {
   extern __shared__ __align__(16) double s_co[];
   const int a = blockIdx.x;
   if (a >= nA) return;
@@ -179,16 +176,16 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
   const int k = cfg.k;
   const int s = n_static[i];
   const int n = k + s;
-  // shared layout per warp: problem [kMaxC][21], incumbent sol [18],
-  // lane states [32][18]; then per-block restart results
-  const int per_warp = kMaxC * kSlot + 6 * kMaxC + 32 * 3 * kMaxC;
-  double* W = s_co + warp * per_warp;
-  double* sp = W;
-  double* inc = W + kMaxC * kSlot;  // incumbent solution (warm start)
-  double* win = inc + 3 * kMaxC;    // best mutation's solution of this step
-  double* lst = win + 3 * kMaxC;    // per-lane solver states
+  double* W = s_co + warp * kCoptPerWarp;
+  double* sp = W;                        // incumbent problem
+  double* inc = W + kMaxC * kSlot;       // incumbent solution (warm start)
+  double* win = inc + 3 * kMaxC;         // best mutation's solution of this step
+  double* lane_base = win + 3 * kMaxC;   // per lane: trial slot, working state, best state
+  double* tslot = lane_base + lane * (kSlot + 6 * kMaxC);
+  double* wst = tslot + kSlot;
+  double* bst = wst + 3 * kMaxC;
   const int rstride = 2 + k + 3 * kMaxC;
-  double* res = s_co + nw * per_warp;
+  double* res = s_co + nw * kCoptPerWarp;
   long long off[kMaxK], cnt[kMaxK];
   for (int q = 0; q < k; ++q) {
     off[q] = el_off[a * k + q];
@@ -210,24 +207,14 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
       __syncwarp();
       PV w;
       w.sp = sp;
+      w.ts = tslot;
       w.n = n;
       w.tq = -1;
       w.lambda = cfg.lambda;
       w.mu = cfg.mu;
-#pragma unroll
-      for (int c = 0; c < kSlot; ++c) w.tv[c] = 0.0;
-      double st_a[kMaxC], st_bx[kMaxC], st_by[kMaxC];
       // cold solve: lanes over anchors, best anchor by strict '<'
       double val = kInf;
-      if (lane < n) {
-        val = pv_anchor(w, lane, cfg.o, nullptr, st_a, st_bx, st_by, ctr);
-#pragma unroll
-        for (int c = 0; c < kMaxC; ++c) {
-          lst[3 * kMaxC * lane + c] = st_a[c];
-          lst[3 * kMaxC * lane + kMaxC + c] = st_bx[c];
-          lst[3 * kMaxC * lane + 2 * kMaxC + c] = st_by[c];
-        }
-      }
+      if (lane < n) val = pv_anchor(w, lane, cfg.o, nullptr, wst, ctr);
       if (!(val < kInf)) val = kInf;
       double best = val;
       int bl = val < kInf ? lane : 99;
@@ -243,17 +230,18 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
       int anchor = best < kInf ? bl : -1;
       double obj = best;
       __syncwarp();
-      if (lane < 3 * kMaxC) inc[lane] = anchor >= 0 ? lst[3 * kMaxC * anchor + lane] : 0.0;
+      if (lane < 3 * kMaxC)
+        inc[lane] = anchor >= 0 ? lane_base[anchor * (kSlot + 6 * kMaxC) + kSlot + lane] : 0.0;
       __syncwarp();
       const uint64_t* M = D + k;
       for (int outer = 0; outer < cfg.n_outer; ++outer) {
         for (int q = 0; q < k; ++q) {
-          V3 cur_p = v3(sp[kSlot * q], sp[kSlot * q + 1], sp[kSlot * q + 2]);
-          V3 cur_n = neg(v3(sp[kSlot * q + 3], sp[kSlot * q + 4], sp[kSlot * q + 5]));  // element normal
+          const double* cs = sp + kSlot * q;
+          V3 cur_p = ld3(cs);
           V3 tx, ty;
-          tangent_basis(neg(cur_n), tx, ty);
+          tangent_basis(ld3(cs + 3), tx, ty);  // slot normal = -element normal
           double best_obj = obj;
-          int best_m = 0x7fffffff, best_id = -1, best_anchor = -1;
+          int best_id = -1, best_anchor = -1;
           for (int mb = 0; mb < cfg.n_inner; mb += 32) {
             const int m = mb + lane;
             double v = kInf;
@@ -277,26 +265,17 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
               ctr.proj += (unsigned long long)cnt[q];
               cand = bi;
               long long e = off[q] + bi;
+              slot_make(tslot, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
               PV tw = w;
               tw.tq = q;
-              double tmp[kSlot];
-              slot_make(tmp, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
-#pragma unroll
-              for (int c = 0; c < kSlot; ++c) tw.tv[c] = tmp[c];
               // warm solve over all anchors in this lane (run_solver)
               double bobj = kInf;
               for (int anc = 0; anc < n; ++anc) {
-                double va = pv_anchor(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, st_a, st_bx, st_by,
-                                      ctr);
+                double va = pv_anchor(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, wst, ctr);
                 if (va < bobj) {
                   bobj = va;
                   an = anc;
-#pragma unroll
-                  for (int c = 0; c < kMaxC; ++c) {
-                    lst[3 * kMaxC * lane + c] = st_a[c];
-                    lst[3 * kMaxC * lane + kMaxC + c] = st_bx[c];
-                    lst[3 * kMaxC * lane + 2 * kMaxC + c] = st_by[c];
-                  }
+                  for (int c = 0; c < 3 * kMaxC; ++c) bst[c] = wst[c];
                 }
               }
               v = bobj;
@@ -315,17 +294,15 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
             if (bm != 0x7fffffff) {
               int src = bm - mb;
               best_obj = bv;
-              best_m = bm;
               best_id = __shfl_sync(kFull, cand, src);
               best_anchor = __shfl_sync(kFull, an, src);
               __syncwarp();
-              // keep the winner's state before the next chunk reuses lst;
-              // the warm start (inc) stays the step's incumbent until the end
-              if (lane < 3 * kMaxC) win[lane] = lst[3 * kMaxC * src + lane];
+              // keep the winner's state before the next chunk reuses it; the
+              // warm start (inc) stays the step's incumbent until the end
+              if (lane < 3 * kMaxC) win[lane] = lane_base[src * (kSlot + 6 * kMaxC) + kSlot + 3 * kMaxC + lane];
               __syncwarp();
             }
           }
-          (void)best_m;
           if (best_id >= 0) {
             ids[q] = best_id;
             if (lane == 0) {
@@ -360,7 +337,7 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
     }
     __syncthreads();
   }
-  if (lane == 0) ctr_flush(ctr);
+  ctr_flush(ctr);
   if (threadIdx.x == 0) {
     double* best = res + nw * rstride;
     out_obj[a] = best[0];
@@ -374,8 +351,7 @@ __global__ void k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const 
 }
 
 __host__ __forceinline__ size_t copt2_smem(int k, int nw) {
-  const int per_warp = kMaxC * kSlot + 6 * kMaxC + 32 * 3 * kMaxC;
-  return ((size_t)nw * per_warp + (size_t)(nw + 1) * (2 + k + 3 * kMaxC)) * sizeof(double);
+  return ((size_t)nw * kCoptPerWarp + (size_t)(nw + 1) * (2 + k + 3 * kMaxC)) * sizeof(double);
 }
 
 }  // namespace lgd

@@ -40,6 +40,14 @@ struct DField {
   const int* run_start;
   const int* run_count;
   const int* cell_box;  // box ids ordered by (cell, patch)
+  // dense query path (when the field's cell range is small): grid cell ->
+  // (start, count) into rec; rec[j] = (dependency group of the box's patch,
+  // first code, code count, box id) in (cell, patch) order.
+  int grid_ok;
+  long long gbase[3];
+  int gdim[3];
+  const int2* grid;
+  const int4* rec;
 };
 
 __device__ __forceinline__ uint64_t cell_hash(long long x, long long y, long long z) {
@@ -241,6 +249,27 @@ __global__ void k_cell_runs(long long B, const int* head, const int* run_id, int
   (void)n_runs;
 }
 
+// Dense grid of runs + run-ordered packed box records.
+__global__ void k_grid_fill(int n_runs, const int* run_start, const int* run_count,
+                            const int* cell_box, const long long* box_cell, long long bx,
+                            long long by, long long bz, int dy, int dz, int2* grid) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_runs) return;
+  const long long* c = box_cell + 3 * cell_box[run_start[r]];
+  long long idx = ((c[0] - bx) * dy + (c[1] - by)) * dz + (c[2] - bz);
+  grid[idx] = make_int2(run_start[r], run_count[r]);
+}
+
+__global__ void k_rec_fill(long long B, const int* cell_box, const int* box_patch,
+                           const int* group_of_patch, const long long* box_code_off, int4* rec) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < B;
+       j += (long long)gridDim.x * blockDim.x) {
+    int b = cell_box[j];
+    rec[j] = make_int4(group_of_patch[box_patch[b]], (int)box_code_off[b],
+                       (int)(box_code_off[b + 1] - box_code_off[b]), b);
+  }
+}
+
 __global__ void k_cell_hash_insert(int n_runs, const int* run_start, const int* cell_box,
                                    const long long* box_cell, int mask, int* hash_run) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -292,6 +321,24 @@ __device__ __forceinline__ uint32_t sample_mask(const DField& f, const double* c
                                                 double theta) {
   long long c[3];
   cell_of(p, f.w, c);
+  if (f.grid_ok) {
+    long long x = c[0] - f.gbase[0], y = c[1] - f.gbase[1], z = c[2] - f.gbase[2];
+    if (x < 0 || y < 0 || z < 0 || x >= f.gdim[0] || y >= f.gdim[1] || z >= f.gdim[2]) return 0u;
+    int2 se = f.grid[(x * f.gdim[1] + y) * f.gdim[2] + z];
+    uint32_t bits = 0u;
+    for (int j = se.x; j < se.x + se.y; ++j) {
+      int4 r = f.rec[j];
+      if (r.x < 0 || ((bits >> r.x) & 1u)) continue;
+      for (int q = r.y; q < r.y + r.z; ++q) {
+        int code = f.codes[q];
+        if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) {
+          bits |= 1u << r.x;
+          break;
+        }
+      }
+    }
+    return bits;
+  }
   int r = find_run(f, c);
   if (r < 0) return 0u;
   uint32_t bits = 0u;

@@ -36,6 +36,8 @@ struct DHand {
   int chain[kMaxLinks][kMaxDepth];
   unsigned jmask[kMaxLinks];  // bit j: joint j drives link l
   int jlink[kMaxDof];         // link carrying joint j
+  int level[kMaxLinks];       // depth in the kinematic tree (root = 0)
+  int n_levels;
   // convex parts (global memory)
   const int* vert_off;
   const double* verts;

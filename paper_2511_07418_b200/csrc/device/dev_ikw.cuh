@@ -3,9 +3,9 @@
 //
 // Lane roles (all summations keep the oracle's exact order, so results are
 // bit-identical to the serial restatement):
-//   - FK: lane l holds the frame of link l in registers and composes its own
-//     root -> l chain; that is the same sequence of compose() calls the
-//     topological-order FK performs for link l (hand.cpp:275-295).
+//   - FK: lane l computes link l's local transform, then frames are composed
+//     level by level in shared memory, frames[l] = frames[parent] * local_l,
+//     the same operations as the topological-order FK (hand.cpp:275-295).
 //   - Jacobian: lane j owns joint column j; rows are streamed per target point.
 //   - J^T J: lanes own entries (a <= b), each a row-ordered sum; mirrored.
 //   - LDLT (Eigen, diagonal pivoting): lane i owns row i of the trailing
@@ -21,39 +21,51 @@ namespace lgd {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ Xf shfl_xf(const Xf& x, int src) {
-  Xf o;
-#pragma unroll
-  for (int a = 0; a < 9; ++a) o.R.m[a] = __shfl_sync(kFull, x.R.m[a], src);
-  o.t.x = __shfl_sync(kFull, x.t.x, src);
-  o.t.y = __shfl_sync(kFull, x.t.y, src);
-  o.t.z = __shfl_sync(kFull, x.t.z, src);
-  return o;
+__device__ __forceinline__ Xf ld_xf(const double* p) {
+  Xf x;
+  x.R = m3_load(p);
+  x.t = v3_load(p + 9);
+  return x;
+}
+__device__ __forceinline__ void st_xf(double* p, const Xf& x) {
+  m3_store(p, x.R);
+  v3_store(p + 9, x.t);
 }
 
-// Frame of link `lane` at q (q in shared memory, read by all lanes).
-__device__ __forceinline__ Xf wfk(const double* q, int lane) {
-  Xf f = xf_identity();
-  if (lane < c_hand.n_links) {
-    const int n = c_hand.chain_len[lane];
-    for (int d = 0; d < n; ++d) {
-      int l = c_hand.chain[lane][d];
-      Xf local;
-      local.R = m3_load(c_hand.R[l]);
-      local.t = v3_load(c_hand.t[l]);
-      int jt = c_hand.jtype[l];
-      if (jt == 1) {
-        Xf m;
-        m.R = angle_axis(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]));
-        m.t = v3(0.0, 0.0, 0.0);
-        local = xf_compose(local, m);
-      } else if (jt == 2) {
-        local.t = add(local.t, mul(local.R, scale(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]))));
-      }
-      f = d == 0 ? local : xf_compose(f, local);
-    }
+// Pre-motion origin composed with the joint motion at q (hand.cpp:281-290).
+__device__ __forceinline__ Xf link_local(int l, const double* q) {
+  Xf local;
+  local.R = m3_load(c_hand.R[l]);
+  local.t = v3_load(c_hand.t[l]);
+  int jt = c_hand.jtype[l];
+  if (jt == 1) {
+    Xf m;
+    m.R = angle_axis(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]));
+    m.t = v3(0.0, 0.0, 0.0);
+    local = xf_compose(local, m);
+  } else if (jt == 2) {
+    local.t = add(local.t, mul(local.R, scale(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]))));
   }
-  return f;
+  return local;
+}
+
+// forward_kinematics into shared memory F[n_links][12], q in shared memory.
+__device__ __forceinline__ void wfk_s(const double* q, double* F, int lane) {
+  const int nl = c_hand.n_links;
+  Xf loc = xf_identity();
+  if (lane < nl) loc = link_local(lane, q);
+  for (int d = 0; d < c_hand.n_levels; ++d) {
+    if (lane < nl && c_hand.level[lane] == d) {
+      int p = c_hand.parent[lane];
+      st_xf(F + 12 * lane, p < 0 ? loc : xf_compose(ld_xf(F + 12 * p), loc));
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ void copy_frames(double* dst, const double* src, int lane) {
+  for (int a = lane; a < 12 * c_hand.n_links; a += 32) dst[a] = src[a];
+  __syncwarp();
 }
 
 // Target layout in shared memory: [k][12] = op(3) on(3) hp(3) hn(3); links [k].
@@ -70,15 +82,14 @@ __device__ __forceinline__ double warp_max_d(double v) {
 
 // stacked_residual (ik.cpp:13-27): lanes < k fill r[6i..6i+5]; returns the
 // row-ordered sum of squares (computed by lane 0, broadcast).
-__device__ __forceinline__ double wresidual(const Xf& f, const WTargets& T, int k, double beta,
+__device__ __forceinline__ double wresidual(const double* F, const WTargets& T, int k, double beta,
                                             double* r, int lane) {
-  int src = lane < k ? T.link[lane] : 0;
-  Xf F = shfl_xf(f, src);
   if (lane < k) {
+    Xf Fl = ld_xf(F + 12 * T.link[lane]);
     const double* t = T.t + 12 * lane;
     V3 op = v3_load(t), on = v3_load(t + 3);
-    V3 hp = xf_apply(F, v3_load(t + 6));
-    V3 hn = xf_rotate(F, v3_load(t + 9));
+    V3 hp = xf_apply(Fl, v3_load(t + 6));
+    V3 hn = xf_rotate(Fl, v3_load(t + 9));
     V3 a = sub(op, hp);
     V3 b = sub(axpy(op, beta, on), axpy(hp, beta, hn));
     double* o = r + 6 * lane;
@@ -219,61 +230,55 @@ __device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
   __syncwarp();
 }
 
-// solve_contact_ik (ik.cpp:31-139).  q (smem) in/out; f = lane frame at q on
-// exit.  Returns finite; used = OR of joints with a nonzero column.
+// solve_contact_ik (ik.cpp:31-139).  q (smem) in/out; F (smem) receives the
+// frames at the final q; Ft is trial scratch.  Returns finite; used = OR of
+// joints with a nonzero column.
 __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
-                    unsigned long long& used, WarpWs& ws, Xf& f, Ctr& ctr, int lane) {
+                    unsigned long long& used, WarpWs& ws, double* F, double* Ft, Ctr& ctr,
+                    int lane) {
   const int dof = c_hand.dof;
   const int rows = 6 * k;
   if (lane < dof) q[lane] = dclamp(q[lane], c_hand.jlo[lane], c_hand.jhi[lane]);
   __syncwarp();
   used = 0ull;
-  if (k == 0) {
-    f = wfk(q, lane);
-    return true;
-  }
-  bool finite = true;
-  f = wfk(q, lane);
+  wfk_s(q, F, lane);
   ++ctr.fk;
+  if (k == 0) return true;
+  bool finite = true;
   double* r = ws.r;
   double* rt = ws.rt;
-  double objective = wresidual(f, T, k, P.beta, r, lane);
+  double objective = wresidual(F, T, k, P.beta, r, lane);
   for (int it = 0; it < iterations; ++it) {
     ++ctr.ik_it;
     // Jacobian points: lane p < 2k -> target p/2, half p%2
-    {
+    if (lane < 2 * k) {
       int i = lane >> 1;
-      int src = lane < 2 * k ? T.link[i] : 0;
-      Xf F = shfl_xf(f, src);
-      if (lane < 2 * k) {
-        const double* t = T.t + 12 * i;
-        V3 lp = (lane & 1) ? axpy(v3_load(t + 6), P.beta, v3_load(t + 9)) : v3_load(t + 6);
-        v3_store(ws.pts + 3 * lane, xf_apply(F, lp));
-      }
+      Xf Fl = ld_xf(F + 12 * T.link[i]);
+      const double* t = T.t + 12 * i;
+      V3 lp = (lane & 1) ? axpy(v3_load(t + 6), P.beta, v3_load(t + 9)) : v3_load(t + 6);
+      v3_store(ws.pts + 3 * lane, xf_apply(Fl, lp));
     }
+    __syncwarp();
     // joint columns
-    {
-      int lj = lane < dof ? c_hand.jlink[lane] : 0;
-      Xf Fj = shfl_xf(f, lj);
-      __syncwarp();
-      if (lane < dof) {
-        V3 axis = mul(Fj.R, v3_load(c_hand.axis[lj]));
-        bool rev = c_hand.jtype[lj] == 1;
-        double cm = 0.0;
-        for (int p = 0; p < 2 * k; ++p) {
-          bool on = (c_hand.jmask[T.link[p >> 1]] >> lane) & 1u;
-          V3 col = v3(0.0, 0.0, 0.0);
-          if (on) col = rev ? cross(axis, sub(v3_load(ws.pts + 3 * p), Fj.t)) : axis;
-          int row = 3 * p;  // 6i + 3h
-          ws.J[(row + 0) * dof + lane] = col.x;
-          ws.J[(row + 1) * dof + lane] = col.y;
-          ws.J[(row + 2) * dof + lane] = col.z;
-          cm = dmax(cm, dabs(col.x));
-          cm = dmax(cm, dabs(col.y));
-          cm = dmax(cm, dabs(col.z));
-        }
-        if (cm > 1e-12) used |= 1ull << lane;
+    if (lane < dof) {
+      int lj = c_hand.jlink[lane];
+      Xf Fj = ld_xf(F + 12 * lj);
+      V3 axis = mul(Fj.R, v3_load(c_hand.axis[lj]));
+      bool rev = c_hand.jtype[lj] == 1;
+      double cm = 0.0;
+      for (int p = 0; p < 2 * k; ++p) {
+        bool on = (c_hand.jmask[T.link[p >> 1]] >> lane) & 1u;
+        V3 col = v3(0.0, 0.0, 0.0);
+        if (on) col = rev ? cross(axis, sub(v3_load(ws.pts + 3 * p), Fj.t)) : axis;
+        int row = 3 * p;  // 6i + 3h
+        ws.J[(row + 0) * dof + lane] = col.x;
+        ws.J[(row + 1) * dof + lane] = col.y;
+        ws.J[(row + 2) * dof + lane] = col.z;
+        cm = dmax(cm, dabs(col.x));
+        cm = dmax(cm, dabs(col.y));
+        cm = dmax(cm, dabs(col.z));
       }
+      if (cm > 1e-12) used |= 1ull << lane;
     }
     {
       unsigned long long u = used;
@@ -322,18 +327,17 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
         ws.qt[lane] = dclamp(q[lane] + dmin(dmax(dq, -P.step_clamp), P.step_clamp), c_hand.jlo[lane],
                              c_hand.jhi[lane]);
       __syncwarp();
-      Xf ft = wfk(ws.qt, lane);
+      wfk_s(ws.qt, Ft, lane);
       ++ctr.fk;
-      double obj_try = wresidual(ft, T, k, P.beta, rt, lane);
+      double obj_try = wresidual(Ft, T, k, P.beta, rt, lane);
       if (obj_try <= objective) {
         if (lane < dof) q[lane] = ws.qt[lane];
-        f = ft;
+        copy_frames(F, Ft, lane);
         double* sw = r;
         r = rt;
         rt = sw;
         objective = obj_try;
         moved = true;
-        __syncwarp();
         break;
       }
       dq *= 0.5;
@@ -346,23 +350,16 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
   }
   bool nonfin = lane < dof && !is_finite(q[lane]);
   if (__any_sync(kFull, nonfin)) finite = false;
-  // keep the caller's r buffer in place (ws.r) for residual reads
-  if (r != ws.r) {
-    if (lane < rows) ws.r[lane] = r[lane];
-    __syncwarp();
-  }
   return finite;
 }
 
-// realize_grasp's project (pipeline.cpp:196-220) at lane frames f: worst
+// realize_grasp's project (pipeline.cpp:196-220) at frames F: worst
 // distance (all lanes), optionally refreshing hand points into R.
-__device__ __forceinline__ double wproject(const Xf& f, const WTargets& T, int k, WTargets* R,
+__device__ __forceinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
                                            int lane) {
-  int src = lane < k ? T.link[lane] : 0;
-  Xf F = shfl_xf(f, src);
   double d = 0.0;
   if (lane < k) {
-    Xf inv = xf_inverse(F);
+    Xf inv = xf_inverse(ld_xf(F + 12 * T.link[lane]));
     V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
     d = closest_on_parts(T.link[lane], xf_apply(inv, v3_load(T.t + 12 * lane)), &sp, &sn);
     if (R) {
@@ -375,59 +372,59 @@ __device__ __forceinline__ double wproject(const Xf& f, const WTargets& T, int k
 }
 
 // realize_grasp (pipeline.cpp:185-253) for one warp; q (smem) starts at q0.
+// F, Fs, Ft: frame buffers for q, the finetune candidate and trial steps.
 __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref, int k,
                          const IkCfg& P, int rounds, int fine_iters, double* max_res,
-                         unsigned long long* used_out, WarpWs& ws, Ctr& ctr, int lane) {
+                         unsigned long long* used_out, WarpWs& ws, double* F, double* Fs,
+                         double* Ft, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   double q0 = lane < dof ? q[lane] : 0.0;
   unsigned long long used = 0ull;
-  Xf f;
-  if (!wik(q, T, k, P, P.iterations, used, ws, f, ctr, lane)) {
+  if (!wik(q, T, k, P, P.iterations, used, ws, F, Ft, ctr, lane)) {
     if (lane < dof) q[lane] = q0;
     __syncwarp();
     *max_res = kInf;
     *used_out = 0ull;
     return false;
   }
-  double worst = wproject(f, T, k, nullptr, lane);
+  double worst = wproject(F, T, k, nullptr, lane);
   for (int round = 0; round < rounds; ++round) {
     for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
     if (lane < k) Ref.link[lane] = T.link[lane];
     __syncwarp();
-    wproject(f, T, k, &Ref, lane);
+    wproject(F, T, k, &Ref, lane);
     if (lane < dof) qs[lane] = q[lane];
     __syncwarp();
     unsigned long long su = 0ull;
-    Xf fs;
-    if (!wik(qs, Ref, k, P, fine_iters, su, ws, fs, ctr, lane)) break;
-    double w2 = wproject(fs, T, k, nullptr, lane);
+    if (!wik(qs, Ref, k, P, fine_iters, su, ws, Fs, Ft, ctr, lane)) break;
+    double w2 = wproject(Fs, T, k, nullptr, lane);
     if (w2 > worst + 1e-6) break;
     if (lane < dof) q[lane] = qs[lane];
-    __syncwarp();
-    f = fs;
+    copy_frames(F, Fs, lane);
     worst = w2;
     used |= su;
   }
-  *max_res = wproject(f, T, k, nullptr, lane);
+  *max_res = wproject(F, T, k, nullptr, lane);
   *used_out = used;
   bool nonfin = lane < dof && !is_finite(q[lane]);
   return !__any_sync(kFull, nonfin);
 }
 
-// Per-warp shared bytes: workspace + targets, refreshed targets, q, qs, links
-// (16-byte aligned so every warp's double arrays stay aligned).
+// Per-warp shared bytes: workspace + targets, refreshed targets, q, qs,
+// three frame buffers, links (16-byte aligned).
 __host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof) {
-  size_t b = warp_ws_bytes(kMaxK, dof) + (size_t)(24 * kMaxK + 2 * kMaxDof) * sizeof(double) +
+  size_t b = warp_ws_bytes(kMaxK, dof) + (size_t)(24 * kMaxK + 2 * kMaxDof + 3 * 12 * kMaxLinks) * sizeof(double) +
              2 * kMaxK * sizeof(int);
   return (b + 15) & ~(size_t)15;
 }
 
 // One warp per problem; targets [t][kMaxK][12] + links [t][kMaxK]; q_out
 // [t][kMaxDof] holds q0 on entry (mid_config when q_init == nullptr).
-__global__ void k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_iters,
-                               const double* tgt, int tgt_stride, const int* tl, int tl_stride,
-                               const double* q_init, double* q_out, double* max_res, int* finite,
-                               unsigned long long* used) {
+__global__ void __launch_bounds__(128, 4)
+k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_iters,
+               const double* tgt, int tgt_stride, const int* tl, int tl_stride,
+               const double* q_init, double* q_out, double* max_res, int* finite,
+               unsigned long long* used) {
   extern __shared__ __align__(16) char s_ik[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -442,7 +439,10 @@ __global__ void k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int roun
   Ref.t = extra + 12 * kMaxK;
   double* q = extra + 24 * kMaxK;
   double* qs = q + kMaxDof;
-  T.link = (int*)(qs + kMaxDof);
+  double* F = qs + kMaxDof;
+  double* Fs = F + 12 * kMaxLinks;
+  double* Ft = Fs + 12 * kMaxLinks;
+  T.link = (int*)(Ft + 12 * kMaxLinks);
   Ref.link = T.link + kMaxK;
   const double* src = tgt + (size_t)t * tgt_stride;
   for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
@@ -452,7 +452,7 @@ __global__ void k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int roun
   Ctr ctr = {0, 0, 0, 0, 0};
   double mr;
   unsigned long long u;
-  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, ctr, lane);
+  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, Fs, Ft, ctr, lane);
   if (lane == 0) ctr_flush(ctr);
   if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
   if (lane == 0) {

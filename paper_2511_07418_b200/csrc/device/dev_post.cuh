@@ -175,6 +175,7 @@ __global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, Fi
                                 const double* best_tgt, const int* best_link, lg_grasp* out,
                                 int* valid, int* dropped) {
   __shared__ double s_q[4][kMaxDof];
+  __shared__ double s_F[4][12 * kMaxLinks];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t = blockIdx.x * (blockDim.x >> 5) + w;
   if (t >= nT) return;
@@ -183,14 +184,14 @@ __global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, Fi
   const int k = C.k;
   if (lane < c_hand.dof) s_q[w][lane] = q_final[(size_t)a * kMaxDof + lane];
   __syncwarp();
-  Xf f = wfk(s_q[w], lane);
+  wfk_s(s_q[w], s_F[w], lane);
   Xf x = load_xf(pose + 12 * i);
   // re-projection at the final q: lane s < k
   int link = lane < k ? best_link[a * kMaxK + lane] : 0;
-  Xf F = shfl_xf(f, link);
   double d = 0.0;
   V3 pw = v3(0, 0, 0);
   if (lane < k) {
+    Xf F = ld_xf(s_F[w] + 12 * link);
     const double* T = best_tgt + (size_t)a * kMaxK * 12 + 12 * lane;
     Xf inv = xf_inverse(F);
     V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);

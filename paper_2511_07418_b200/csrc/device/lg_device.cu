@@ -8,6 +8,8 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -237,6 +239,8 @@ void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
     for (int x = l; x >= 0 && n <= kMaxLinks; x = d.parent[x]) path[n++] = x;
     if (n > kMaxDepth) throw std::invalid_argument("device: kinematic chain deeper than 10 links");
     h.chain_len[l] = n;
+    h.level[l] = n - 1;
+    h.n_levels = std::max(h.n_levels, n);
     h.jmask[l] = 0u;
     for (int i = 0; i < n; ++i) {
       int x = path[n - 1 - i];
@@ -333,7 +337,8 @@ struct lg_field {
   DField f;
   DevPatches patches;
   Buf codebook, patch_link, patch_box_off, box_cell, box_patch, box_code_off, codes, rep_point,
-      hash_run, run_start, run_count, cell_box;
+      hash_run, run_start, run_count, cell_box, grid, rec, gop;
+  std::vector<int> h_gop;  // dependency group per patch baked into rec
   long long n_vectors = 0, n_codes = 0;
   int n_runs = 0;
   double build_ms = 0.0;
@@ -377,11 +382,21 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   if (pd.n_patches < 1) throw std::invalid_argument("index build: no patches");
   if (w <= 0.0 || N < 1) throw std::invalid_argument("index build: bad box width or N");
   cudaStream_t s = ctx->stream;
+  const bool timing = std::getenv("LG_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto fmark = [&](const char* name) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[lg timing]   field %-14s %9.3f ms\n", name,
+                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  };
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   bind_hand(ctx, hd);
+  fmark("bind_hand");
   upload_patches(ctx, pd, out->patches);
+  fmark("patches");
   DevPatches& P = out->patches;
   auto cb = make_codebook(C);
   out->x_codebook = cb;
@@ -444,6 +459,7 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   k_field_heads<<<grid_for(V, 256), 256, 0, s>>>(V, d_keys2, KL.sh_z, d_ch, d_bh);
   LAUNCH(ctx);
   check_launch();
+  fmark("sorted");
   long long n_codes = exclusive_scan_count(ctx, d_ch, d_cid, V);
   long long n_boxes = exclusive_scan_count(ctx, d_bh, d_bid, V);
   auto* o_codes = dalloc<uint16_t>(out->codes, (size_t)n_codes);
@@ -463,6 +479,7 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   CK(cudaMemcpyAsync(o_bco + n_boxes, &nc_ll, sizeof(long long), cudaMemcpyHostToDevice, s));
   dupload(out->patch_link, P.h_link.data(), P.h_link.size(), s);
 
+  fmark("emitted");
   // cell hash: boxes keyed by (cell, patch)
   KeyLayout K2;
   K2.sh_patch = 0;
@@ -502,6 +519,39 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
                                                              o_hash);
   LAUNCH(ctx);
   check_launch();
+  fmark("hashed");
+  // dense grid + packed run-ordered records for the query kernel
+  {
+    int G = 0;
+    std::vector<int> gol = groups_of(hd, &G);
+    out->h_gop.resize(P.P);
+    for (int p = 0; p < P.P; ++p) out->h_gop[p] = gol[P.h_link[p]];
+    int* d_gop = dupload(out->gop, out->h_gop.data(), out->h_gop.size(), s);
+    long long dx = cmm_h[3] - cmm_h[0] + 1, dy = cmm_h[4] - cmm_h[1] + 1, dz = cmm_h[5] - cmm_h[2] + 1;
+    out->f.grid_ok = 0;
+    if (dx > 0 && dy > 0 && dz > 0 && dx * dy * dz <= (64ll << 20)) {
+      int2* g = dalloc<int2>(out->grid, (size_t)(dx * dy * dz));
+      CK(cudaMemsetAsync(g, 0, sizeof(int2) * (size_t)(dx * dy * dz), s));
+      k_grid_fill<<<grid_for(n_runs, 256), 256, 0, s>>>(n_runs, o_rs, o_rc, o_cellbox, o_cell, cmm_h[0],
+                                                         cmm_h[1], cmm_h[2], (int)dy, (int)dz, g);
+      LAUNCH(ctx);
+      check_launch();
+      int4* rec = dalloc<int4>(out->rec, (size_t)n_boxes);
+      k_rec_fill<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, o_cellbox, o_bpatch, d_gop, o_bco, rec);
+      LAUNCH(ctx);
+      check_launch();
+      out->f.grid_ok = 1;
+      out->f.gbase[0] = cmm_h[0];
+      out->f.gbase[1] = cmm_h[1];
+      out->f.gbase[2] = cmm_h[2];
+      out->f.gdim[0] = (int)dx;
+      out->f.gdim[1] = (int)dy;
+      out->f.gdim[2] = (int)dz;
+      out->f.grid = g;
+      out->f.rec = rec;
+    }
+  }
+  fmark("grid");
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
@@ -616,6 +666,15 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     CK(cudaStreamSynchronize(s));
   }
   DSamples RS = make_samples(rawc, n_raw);
+  // LG_TIMING=1: host-clock marks after stream syncs, printed at the end
+  const bool timing = std::getenv("LG_TIMING") != nullptr;
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* name) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    marks.push_back({name, std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count()});
+  };
+  mark("inputs_uploaded");
   tdev.start();
   Buf keepb;
   uint8_t* d_keep = dalloc<uint8_t>(keepb, (size_t)n_raw);
@@ -688,6 +747,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   const int Bl = c_hi - c_lo;
   const int k = cfg.k_contacts;
   out.profile.candidates = (long long)cfg.passes * Bl;
+  mark("preprocess_statics");
   double t_pre = tm.stop();
 
   // ---- per-candidate placement state (pass 0, reused by later passes)
@@ -731,6 +791,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   cc.raw = RS;
   cc.part_link = ctx->h_part_link.as<int>();
 
+  mark("candidate_state");
   for (int pass = 0; pass < cfg.passes && Bl > 0; ++pass) {
     // -------- stage 1: placement + domains (pass 0) + group pick
     tm.start();
@@ -833,6 +894,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       continue;
     }
 
+    mark("stage1");
     // -------- stage 2: contact optimisation
     tm.start();
     Buf b_aidx, b_eloff, b_els, b_elp, b_eln;
@@ -919,6 +981,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       }
     }
 
+    mark("stage2");
     // -------- stage 3: lookup attempts (reverse lookup + realize + filter)
     tm.start();
     Buf b_have, b_bclear, b_bres, b_bq, b_bused, b_btgt, b_blink, b_batt, b_search, b_runs;
@@ -1027,6 +1090,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       continue;
     }
 
+    mark("stage3");
     // -------- stage 4: unused-joint redraws + postprocess
     tm.start();
     Buf b_fq, b_fclean, b_uatt, b_grasp, b_valid, b_drop, b_act_r, b_qall;
@@ -1116,6 +1180,9 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       out.traces.insert(out.traces.end(), pass_tr.begin(), pass_tr.end());
     }
   }
+  mark("passes_done");
+  if (timing)
+    for (auto& m : marks) std::fprintf(stderr, "[lg timing] %-20s %9.3f ms\n", m.first, 1e3 * m.second);
   out.profile.valid = (long long)out.grasps.size();
   out.profile.device_seconds = tdev.stop() + out.profile.field_build;
   {
@@ -1490,7 +1557,9 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
     int* d_cnt = dalloc<int>(bc, (size_t)m * std::max(G, 1));
     int cb_smem = 3 * f->f.C <= 6144 ? 1 : 0;
     size_t qsm = cb_smem ? 3 * (size_t)f->f.C * sizeof(double) : 0;
-    k_query<<<m, 256, qsm, s>>>(m, f->f, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
+    DField fq = f->f;  // the dense path bakes the field's own groups into rec
+    if (!std::equal(f->h_gop.begin(), f->h_gop.end(), group_of_patch)) fq.grid_ok = 0;
+    k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
     check_launch();
     CK(cudaMemcpyAsync(masks, d_mask, sizeof(uint32_t) * m * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
