@@ -13,6 +13,105 @@
 
 namespace lgd {
 
+// validate_grasp_collisions (collision.cpp:230-288), block per configuration:
+// warp 0 runs the level-synchronous FK, threads share the broad phase and
+// one GJK per link-link candidate pair, then all threads sweep the object
+// samples per object-overlapping part.  clean() is an OR of violations and
+// max_penetration a max, both order independent.  With clean_only (the
+// pipeline consumes only clean()), the sweep stops at the first violation.
+__global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const int* call_on,
+                             const double* q_all, const double* pose, const double* obj_aabb,
+                             int clean_only, uint8_t* clean_out, double* maxpen_out) {
+  __shared__ double s_q[kMaxDof];
+  __shared__ double s_fr[kMaxLinks * 12];
+  __shared__ double s_box[64 * 6];
+  __shared__ int s_obj[64];
+  __shared__ int s_nobj;
+  __shared__ int s_viol;
+  __shared__ double scratch[32];
+  const int call = blockIdx.x;
+  if (call >= n_calls) return;
+  if (call_on && !call_on[call]) return;
+  const int i = call_cand[call];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int np = c_hand.n_parts;
+  if (tid < c_hand.dof) s_q[tid] = q_all[(size_t)call * kMaxDof + tid];
+  if (tid == 0) {
+    s_nobj = 0;
+    s_viol = 0;
+  }
+  __syncthreads();
+  if (tid < 32) wfk_s(s_q, s_fr, lane);
+  __syncthreads();
+  for (int p = tid; p < np; p += blockDim.x) {
+    V3 mn, mx;
+    world_bounds(p, ld_xf(s_fr + 12 * C.part_link[p]), &mn, &mx);
+    s_box[6 * p + 0] = mn.x - C.margin;
+    s_box[6 * p + 1] = mn.y - C.margin;
+    s_box[6 * p + 2] = mn.z - C.margin;
+    s_box[6 * p + 3] = mx.x + C.margin;
+    s_box[6 * p + 4] = mx.y + C.margin;
+    s_box[6 * p + 5] = mx.z + C.margin;
+  }
+  __syncthreads();
+  const double* ob = obj_aabb + 6 * i;
+  const double oi[6] = {ob[0] - C.margin, ob[1] - C.margin, ob[2] - C.margin,
+                        ob[3] + C.margin, ob[4] + C.margin, ob[5] + C.margin};
+  auto ovl = [](const double* a, const double* b) {
+    return a[0] <= b[3] && a[1] <= b[4] && a[2] <= b[5] && a[3] >= b[0] && a[4] >= b[1] &&
+           a[5] >= b[2];
+  };
+  // broad phase (collision.cpp:22-45) + GJK narrow phase, pairs in parallel
+  for (int e = tid; e < np * np; e += blockDim.x) {
+    int pa = e / np, pb = e % np;
+    if (pb == pa) {
+      if (C.raw.n > 0 && ovl(s_box + 6 * pa, oi)) s_obj[atomicAdd(&s_nobj, 1)] = pa;
+      continue;
+    }
+    if (pb < pa || !ovl(s_box + 6 * pa, s_box + 6 * pb)) continue;
+    int la = C.part_link[pa], lb = C.part_link[pb];
+    if (la == lb || c_hand.parent[la] == lb || c_hand.parent[lb] == la) continue;
+    if (clean_only && *(volatile int*)&s_viol) continue;
+    if (gjk_distance(pa, ld_xf(s_fr + 12 * la), pb, ld_xf(s_fr + 12 * lb)) == 0.0)
+      atomicOr(&s_viol, 1);
+  }
+  __syncthreads();
+  bool stop = clean_only && s_viol;
+  double maxpen = 0.0;
+  if (!stop) {
+    Xf x = load_xf(pose + 12 * i);
+    const int nobj = s_nobj;
+    for (int o = 0; o < nobj; ++o) {
+      int pa = s_obj[o];
+      Xf inv = xf_inverse(ld_xf(s_fr + 12 * C.part_link[pa]));
+      const double* b = c_hand.bounds + 6 * pa;
+      double mx = 0.0;
+      bool off = false;
+      for (int j = tid; j < C.raw.n; j += blockDim.x) {
+        V3 local = xf_apply(inv, xf_apply(x, C.raw.p(j)));
+        if (!(local.x >= b[0] - 1e-9 && local.y >= b[1] - 1e-9 && local.z >= b[2] - 1e-9 &&
+              local.x <= b[3] + 1e-9 && local.y <= b[4] + 1e-9 && local.z <= b[5] + 1e-9))
+          continue;
+        double depth = part_interior_depth(pa, local);
+        if (depth > C.margin) {
+          off = true;
+          mx = dmax(mx, depth);
+          if (clean_only) break;
+        }
+      }
+      if (off) atomicOr(&s_viol, 1);
+      mx = block_max(mx, scratch);  // synchronises the block
+      maxpen = dmax(maxpen, mx);
+      if (clean_only && s_viol) break;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    clean_out[call] = s_viol ? 0 : 1;
+    if (maxpen_out) maxpen_out[call] = maxpen;
+  }
+}
+
 // Reverse lookup for (candidate b, attempt, slot) (contact_field.cpp:450-484).
 __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int k, int A, int c_lo,
                               int Bsz, int pass, uint64_t seed, DField f,

@@ -1036,8 +1036,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nP);
       CK(cudaMemsetAsync(d_clean, 0, nP, s));
-      k_collision<<<(int)nP, 128, 0, s>>>((int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, d_clean,
-                                           nullptr);
+      k_collision2<<<(int)nP, 128, 0, s>>>((int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, 1,
+                                            d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
       k_attempt_select<<<grid_for(nB, 128), 128, 0, s>>>(
@@ -1111,8 +1111,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nU);
       out.profile.collision_calls += nU;
-      k_collision<<<(int)nU, 128, 0, s>>>((int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, d_clean,
-                                           nullptr);
+      k_collision2<<<(int)nU, 128, 0, s>>>((int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, 1,
+                                            d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
       int* d_uatt_d = dalloc<int>(b_uatt, (size_t)nA);
@@ -1339,7 +1339,7 @@ int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const doubl
     cc.margin = margin;
     cc.raw = S;
     cc.part_link = ctx->h_part_link.as<int>();
-    k_collision<<<m, 128, 0, s>>>(m, cc, d_i, nullptr, d_q, d_p, d_b, d_c, d_m);
+    k_collision2<<<m, 128, 0, s>>>(m, cc, d_i, nullptr, d_q, d_p, d_b, 0, d_c, d_m);
     check_launch();
     CK(cudaMemcpyAsync(clean, d_c, (size_t)m, cudaMemcpyDeviceToHost, s));
     if (max_penetration)
