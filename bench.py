@@ -201,7 +201,10 @@ def run_b200(args):
 
     for _ in range(args.warmup):
         step()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local) if not args.no_clocks else None
+    if clocks:
+        time.sleep(1.0)  # let nvidia-smi finish NVML start-up before the timed steps
+        step()
     e2e_ms, dev_s, valid, launches, h2d, d2h, profs = [], [], [], [], [], [], []
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 (126 MB) between timed steps
@@ -222,7 +225,9 @@ def run_b200(args):
         h2d.append(r.profile["h2d_bytes"])
         d2h.append(r.profile["d2h_bytes"])
         profs.append(r.profile)
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled"]}
+    if args.verbose:
+        print("per-step device ms:", [round(1e3 * x, 1) for x in dev_s], file=sys.stderr)
 
     def reduce(x, op):
         t = torch.tensor(x, dtype=torch.float64, device=dev)
@@ -308,6 +313,8 @@ def main():
     ap.add_argument("--sample-frac", type=int, default=40,
                     help="CPU legs time one 1/N shard of the batch")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

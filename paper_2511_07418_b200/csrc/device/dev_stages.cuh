@@ -263,6 +263,98 @@ __global__ void k_query(int Bl, DField f, const int* group_of_patch, DSamples fs
   for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = s_cnt[g];
 }
 
+// Load-balanced query over the dense cell grid: a warp takes 32 samples,
+// prefix-sums their per-cell box counts and spreads the (sample, box) items
+// evenly over its lanes; a hit ORs the box's group bit into the sample's
+// mask (OR is order independent, so the mask equals the per-sample scan).
+__global__ void __launch_bounds__(256)
+k_query2(int Bl, DField f, DSamples fs, const double* pose, const int* accepted, double theta,
+         int G, int cb_in_smem, uint32_t* mask, int* dom_count) {
+  extern __shared__ double s_cb[];
+  __shared__ int s_cnt[LG_MAX_GROUPS];
+  __shared__ int s_ex[8][33];
+  __shared__ int s_st[8][32];
+  __shared__ double s_n[8][32][3];
+  __shared__ unsigned s_bits[8][32];
+  const int i = blockIdx.x;
+  if (i >= Bl) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t* m = mask + (size_t)i * fs.n;
+  if (!accepted[i]) {
+    for (int j = threadIdx.x; j < fs.n; j += blockDim.x) m[j] = 0u;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = 0;
+    return;
+  }
+  if (cb_in_smem)
+    for (int a = threadIdx.x; a < 3 * f.C; a += blockDim.x) s_cb[a] = f.codebook[a];
+  for (int g = threadIdx.x; g < LG_MAX_GROUPS; g += blockDim.x) s_cnt[g] = 0;
+  __syncthreads();
+  const double* cb = cb_in_smem ? s_cb : f.codebook;
+  const Xf x = load_xf(pose + 12 * i);
+  for (int base = warp * 32; base < fs.n; base += nw * 32) {
+    const int j = base + lane;
+    int start = 0, count = 0;
+    if (j < fs.n) {
+      V3 p = xf_apply(x, fs.p(j));
+      V3 n = xf_rotate(x, fs.nrm(j));
+      s_n[warp][lane][0] = n.x;
+      s_n[warp][lane][1] = n.y;
+      s_n[warp][lane][2] = n.z;
+      long long c[3];
+      cell_of(p, f.w, c);
+      long long cx = c[0] - f.gbase[0], cy = c[1] - f.gbase[1], cz = c[2] - f.gbase[2];
+      if (cx >= 0 && cy >= 0 && cz >= 0 && cx < f.gdim[0] && cy < f.gdim[1] && cz < f.gdim[2]) {
+        int2 se = f.grid[(cx * f.gdim[1] + cy) * f.gdim[2] + cz];
+        start = se.x;
+        count = se.y;
+      }
+    }
+    int incl = count;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    s_ex[warp][lane] = incl - count;
+    if (lane == 31) s_ex[warp][32] = incl;
+    s_st[warp][lane] = start;
+    s_bits[warp][lane] = 0u;
+    __syncwarp();
+    for (int it = lane; it < total; it += 32) {
+      int lo = 0, hi = 31;  // owner = last lane with ex <= it
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (s_ex[warp][mid] <= it) lo = mid;
+        else hi = mid - 1;
+      }
+      int4 r = f.rec[s_st[warp][lo] + (it - s_ex[warp][lo])];
+      if (r.x < 0) continue;
+      V3 n = v3(s_n[warp][lo][0], s_n[warp][lo][1], s_n[warp][lo][2]);
+      for (int q = r.y; q < r.y + r.z; ++q) {
+        int code = f.codes[q];
+        if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) {
+          atomicOr(&s_bits[warp][lo], 1u << r.x);
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (j < fs.n) {
+      uint32_t bits = s_bits[warp][lane];
+      m[j] = bits;
+      while (bits) {
+        int g = __ffs(bits) - 1;
+        bits &= bits - 1;
+        atomicAdd(&s_cnt[g], 1);
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = s_cnt[g];
+}
+
 // Per-candidate world AABB of the raw object samples (the broad-phase
 // object box of validate_grasp_collisions, collision.cpp:243-245).
 __global__ void k_obj_aabb(int Bl, DSamples raw, const double* pose, const int* accepted,

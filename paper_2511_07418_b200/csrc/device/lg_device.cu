@@ -41,18 +41,49 @@ thread_local cudaStream_t g_alloc_stream = nullptr;
 std::mutex g_streams_mu;
 std::set<cudaStream_t> g_live_streams;  // streams of live contexts
 
-void free_on(void* p, cudaStream_t s) {
-  bool live;
+// Per-stream block cache: a pass allocates the same buffer sizes every call,
+// so released blocks are kept and handed back (stream order makes reuse on
+// the same stream safe); nothing is returned to the driver until the
+// context goes away.
+std::map<cudaStream_t, std::multimap<size_t, void*>> g_cache;
+
+void* cached_alloc(size_t bytes, cudaStream_t s) {
   {
     std::lock_guard<std::mutex> lk(g_streams_mu);
-    live = g_live_streams.count(s) != 0;
+    if (g_live_streams.count(s)) {
+      auto& c = g_cache[s];
+      auto it = c.lower_bound(bytes);
+      if (it != c.end() && it->first <= 2 * bytes + 4096) {
+        void* p = it->second;
+        c.erase(it);
+        return p;
+      }
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, bytes));
+  return p;
+}
+
+void free_on(void* p, size_t bytes, cudaStream_t s) {
+  {
+    std::lock_guard<std::mutex> lk(g_streams_mu);
+    if (g_live_streams.count(s)) {
+      g_cache[s].emplace(bytes, p);
+      return;
+    }
   }
   // a buffer that outlives its context (e.g. a field destroyed after the
-  // context) is freed synchronously instead of on the dead stream
-  if (!live || cudaFreeAsync(p, s) != cudaSuccess) {
-    cudaGetLastError();
-    cudaFree(p);
-  }
+  // context) is freed synchronously
+  cudaFree(p);
+}
+
+void drop_cache(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_streams_mu);
+  auto it = g_cache.find(s);
+  if (it == g_cache.end()) return;
+  for (auto& kv : it->second) cudaFree(kv.second);
+  g_cache.erase(it);
 }
 
 struct Buf {
@@ -64,18 +95,19 @@ struct Buf {
   Buf& operator=(const Buf&) = delete;
   ~Buf() { release(); }
   void release() {
-    if (p) free_on(p, s);
+    if (p) free_on(p, n, s);
     p = nullptr;
     n = 0;
   }
   void alloc(size_t bytes) {
     if (bytes <= n && p) return;
-    if (p) free_on(p, s);
+    if (p) free_on(p, n, s);
     p = nullptr;
     n = 0;
-    if (bytes == 0) bytes = 8;
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (bytes == 0) bytes = 256;
     s = g_alloc_stream;
-    CK(cudaMallocAsync(&p, bytes, s));
+    p = cached_alloc(bytes, s);
     n = bytes;
   }
   template <typename T>
@@ -827,8 +859,12 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       check_launch();
       int cb_smem = 3 * F.C <= 6144 ? 1 : 0;
       size_t qsm = cb_smem ? 3 * (size_t)F.C * sizeof(double) : 0;
-      k_query<<<Bl, 256, qsm, s>>>(Bl, F, d_gop, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
-                                   d_mask, d_cnt);
+      if (F.grid_ok)
+        k_query2<<<Bl, 256, qsm, s>>>(Bl, F, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem, d_mask,
+                                      d_cnt);
+      else
+        k_query<<<Bl, 256, qsm, s>>>(Bl, F, d_gop, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
+                                     d_mask, d_cnt);
       LAUNCH(ctx);
       check_launch();
       k_obj_aabb<<<Bl, 256, 0, s>>>(Bl, RS, d_pose, d_acc, d_aabb);
@@ -1465,6 +1501,7 @@ void lg_ctx_destroy(lg_ctx* ctx) {
   if (ctx->cub_tmp) cudaFree(ctx->cub_tmp);
   if (ctx->stream) {
     cudaStreamSynchronize(ctx->stream);
+    drop_cache(ctx->stream);
     {
       std::lock_guard<std::mutex> lk(g_streams_mu);
       g_live_streams.erase(ctx->stream);
