@@ -189,6 +189,7 @@ typedef struct lg_profile {
   long long ik_iterations, fk_evals, wrench_evals, wrench_grads, proj_evals;
   long long realize_calls, collision_calls;
   double realize_seconds, contact_opt_seconds;
+  long long index_from_cache; /* RunResult.index.from_cache */
 } lg_profile;
 
 /* Per-candidate record of every stage decision, used by the stage parity
@@ -302,6 +303,13 @@ int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand,
 /* Copies the index to host CSR (pointers valid until lg_field_destroy). */
 int lg_field_export(lg_field* f, lg_field_csr* out);
 void lg_field_destroy(lg_field* f);
+/* ContactFieldIndex::save / load (contact_field.cpp:570-655): the GGCF v1
+ * file, byte-identical to the reference's. load sets *out = NULL (and returns
+ * LG_OK) when the file is missing, malformed, or keyed differently — the
+ * reference's std::nullopt. */
+int lg_field_save(lg_field* f, const char* path, uint64_t key);
+int lg_field_load(lg_ctx* ctx, const lg_hand_desc* hand, const char* path,
+                  uint64_t key, lg_field** out);
 
 /* query_domains (contact_field.cpp:380-448) for m poses at once: writes the
  * reachability mask masks[m][n] (bit g set iff sample i is an element of group

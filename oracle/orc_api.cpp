@@ -1,6 +1,7 @@
 // oracle/orc_api.cpp — flat C entry points over the CPU oracle, loaded with
 // ctypes by tests/ and bench.py (checker / cpu_baseline only).
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -272,6 +273,64 @@ long long orc_field_nodes(void* fp) {
   return n;
 }
 void orc_field_destroy(void* f) { delete (OrcField*)f; }
+
+// ContactFieldIndex::save (contact_field.cpp:570-600): the GGCF v1 stream,
+// field by field, from the oracle's map-built index and its BVHs.
+extern "C++" {
+namespace {
+template <typename T>
+void fput(FILE* f, const T& v) { std::fwrite(&v, sizeof(T), 1, f); }
+void fput_v3(FILE* f, const V3& v) { fput(f, v.x); fput(f, v.y); fput(f, v.z); }
+void fput_nodes(FILE* f, const std::vector<BvhNode>& nodes, int32_t root) {
+  fput(f, (uint64_t)nodes.size());
+  for (const BvhNode& n : nodes) {
+    fput_v3(f, n.bounds.min);
+    fput_v3(f, n.bounds.max);
+    fput(f, n.left);
+    fput(f, n.right);
+    fput(f, n.leaf);
+  }
+  fput(f, root);
+}
+}  // namespace
+}  // extern "C++"
+int orc_field_save(void* fp, const char* path, uint64_t key) {
+  return guard([&] {
+    const FieldIndex& idx = ((OrcField*)fp)->idx;
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw std::runtime_error(std::string("cannot write index file: ") + path);
+    fput(f, (uint32_t)0x47474346u);
+    fput(f, (uint32_t)1u);
+    fput(f, key);
+    fput(f, idx.box_width);
+    fput(f, (uint32_t)idx.codebook.size());
+    for (const V3& d : idx.codebook) fput_v3(f, d);
+    fput(f, (uint64_t)idx.patches.size());
+    for (const PatchIndex& p : idx.patches) {
+      fput(f, (int32_t)p.patch_id);
+      fput(f, (int32_t)p.link);
+      fput(f, (uint64_t)p.boxes.size());
+      for (const IndexBox& b : p.boxes) {
+        fput(f, b.cell[0]);
+        fput(f, b.cell[1]);
+        fput(f, b.cell[2]);
+        fput(f, (uint32_t)b.codes.size());
+        for (size_t i = 0; i < b.codes.size(); ++i) {
+          fput(f, b.codes[i]);
+          fput(f, (int32_t)b.reps[i].link);
+          fput_v3(f, b.reps[i].point);
+          fput_v3(f, b.reps[i].normal);
+        }
+      }
+      fput_nodes(f, p.nodes, p.root);
+    }
+    fput_nodes(f, idx.top_nodes, idx.top_root);
+    bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) throw std::runtime_error(std::string("short write on index file: ") + path);
+  });
+}
+
 
 // query_domains for one pose: masks[n] bitmask of groups whose domain holds
 // an element for sample i, scores[n] element score (0 when no element).

@@ -53,6 +53,7 @@ def lib():
                                           P(vp)]),
             "orc_field_export": (C.c_int, [vp, P(A.FieldCsr)]),
             "orc_field_nodes": (C.c_longlong, [vp]),
+            "orc_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
             "orc_field_destroy": (None, [vp]),
             "orc_query": (C.c_int, [vp, HD, dp, C.c_int, dp, C.c_double, P(C.c_uint32), dp, ip]),
             "orc_reverse_lookup": (C.c_int, [vp, HD, dp, C.c_int, dp, C.c_double, C.c_int,
@@ -254,6 +255,10 @@ class OrcField:
 
     def nodes(self):
         return int(lib().orc_field_nodes(self._h))
+
+    def save(self, path, key):
+        """ContactFieldIndex::save (contact_field.cpp:570-600)."""
+        check(lib().orc_field_save(self._h, str(path).encode(), C.c_uint64(key)))
 
     def query(self, hand_desc, samples, pose12, theta):
         s = _d(samples).reshape(-1, 6)

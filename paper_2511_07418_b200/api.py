@@ -77,6 +77,8 @@ def lib():
         "lg_field_build": (C.c_int, [vp, P(A.HandDesc), P(A.PatchesDesc), C.c_int, C.c_double,
                                      C.c_uint64, C.c_int, P(vp)]),
         "lg_field_export": (C.c_int, [vp, P(A.FieldCsr)]),
+        "lg_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+        "lg_field_load": (C.c_int, [vp, P(A.HandDesc), C.c_char_p, C.c_uint64, P(vp)]),
         "lg_field_destroy": (None, [vp]),
         "lg_query_domains_batch": (C.c_int, [vp, vp, A.ip, A.dp, C.c_int, A.dp, C.c_int,
                                              C.c_double, P(C.c_uint32), A.dp]),
@@ -376,6 +378,19 @@ class ContactFieldIndex:
                                    float(box_width), C.c_uint64(seed), int(codebook_size),
                                    C.byref(h)))
         return cls(h, ctx)
+
+    def save(self, path, key):
+        """ContactFieldIndex::save (contact_field.cpp:570-600): GGCF v1 file."""
+        check(lib().lg_field_save(self._h, os.fsencode(str(path)), C.c_uint64(key)))
+
+    @classmethod
+    def load(cls, ctx, hand, path, expected_key):
+        """ContactFieldIndex::load (contact_field.cpp:602-655): None when the
+        file is missing, malformed or keyed differently."""
+        h = C.c_void_p()
+        check(lib().lg_field_load(ctx._h, C.byref(hand.desc), os.fsencode(str(path)),
+                                  C.c_uint64(expected_key), C.byref(h)))
+        return cls(h, ctx) if h.value else None
 
     def export(self):
         """Host CSR copy: patches -> boxes (lexicographic cells) -> codes/reps."""

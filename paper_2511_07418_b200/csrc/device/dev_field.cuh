@@ -33,7 +33,8 @@ struct DField {
   const int* box_patch;           // [B]
   const long long* box_code_off;  // [B+1]
   const uint16_t* codes;          // [n_codes]
-  const int* rep_point;           // [n_codes] global patch-point index
+  const double* rep_pn;           // [n_codes][6] representative point, normal (link frame)
+  const int* rep_link;            // [n_codes] representative link
   // cell hash: run r covers cell_box[run_start[r] .. run_start[r]+run_count[r])
   int hash_mask;
   const int* hash_run;  // [mask+1] run id or -1
@@ -190,8 +191,10 @@ __global__ void k_field_heads(long long V, const unsigned long long* keys, int s
 __global__ void k_field_emit(long long V, int F, const unsigned long long* keys,
                              const uint32_t* vals, const int* code_head, const int* box_head,
                              const int* code_id, const int* box_id, const long long* cells,
-                             const int* fp_patch, const int* fp_point, KeyLayout L,
-                             uint16_t* out_codes, int* out_rep, long long* box_cell,
+                             const int* fp_patch, const int* fp_point, const int* fp_link,
+                             const double* pts, const double* nrm, KeyLayout L,
+                             uint16_t* out_codes, double* out_rep, int* out_rlink,
+                             long long* box_cell,
                              int* box_patch, long long* box_code_off, int* patch_box_off) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < V;
        i += (long long)gridDim.x * blockDim.x) {
@@ -200,7 +203,12 @@ __global__ void k_field_emit(long long V, int F, const unsigned long long* keys,
     int f = (int)(v % (uint32_t)F);
     int ce = code_id[i];
     out_codes[ce] = (uint16_t)((keys[i] >> L.sh_code) & ((1ull << (L.sh_z - L.sh_code)) - 1ull));
-    out_rep[ce] = fp_point[f];
+    int pi = fp_point[f];
+    for (int a = 0; a < 3; ++a) {
+      out_rep[6 * (long long)ce + a] = pts[3 * pi + a];
+      out_rep[6 * (long long)ce + 3 + a] = nrm[3 * pi + a];
+    }
+    out_rlink[ce] = fp_link[f];
     if (box_head[i]) {
       int b = box_id[i];
       box_cell[3 * b] = cells[3 * (long long)v];

@@ -160,13 +160,13 @@ __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int 
       best = (int)(q - q0);
     }
   }
-  int rp = f.rep_point[q0 + best];
+  const double* rp = f.rep_pn + 6 * (q0 + best);
   double* T = tgt + (size_t)t * 12;
   v3_store(T, p);
   v3_store(T + 3, neg(n));
-  v3_store(T + 6, v3_load(patch_pts + 3 * rp));
-  v3_store(T + 9, v3_load(patch_nrm + 3 * rp));
-  tgt_link[t] = patch_link[f.box_patch[box]];
+  v3_store(T + 6, v3_load(rp));
+  v3_store(T + 9, v3_load(rp + 3));
+  tgt_link[t] = f.rep_link[q0 + best];
 }
 
 __global__ void k_conv_flags(int n, const int* finite, const double* res, double tol, int* on) {

@@ -711,12 +711,12 @@ __global__ void k_targets(int nAct, const int* act, const int* alive_idx, int k,
       best = (int)(q - q0);
     }
   }
-  int rp = f.rep_point[q0 + best];
+  const double* rp = f.rep_pn + 6 * (q0 + best);
   double* T = tgt + (size_t)(ai * k + slot) * 12;
   v3_store(T, p);
   v3_store(T + 3, neg(n));
-  v3_store(T + 6, v3_load(patch_pts + 3 * rp));
-  v3_store(T + 9, v3_load(patch_nrm + 3 * rp));
+  v3_store(T + 6, v3_load(rp));
+  v3_store(T + 9, v3_load(rp + 3));
   tgt_link[ai * k + slot] = patch_link[f.box_patch[box]];
 }
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <filesystem>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -363,256 +364,10 @@ void upload_patches(lg_ctx* ctx, const lg_patches_desc& d, DevPatches& o) {
 
 }  // namespace
 
-// ---------------------------------------------------------------- field
-struct lg_field {
-  lg_ctx* ctx = nullptr;
-  DField f;
-  DevPatches patches;
-  Buf codebook, patch_link, patch_box_off, box_cell, box_patch, box_code_off, codes, rep_point,
-      hash_run, run_start, run_count, cell_box, grid, rec, gop;
-  std::vector<int> h_gop;  // dependency group per patch baked into rec
-  long long n_vectors = 0, n_codes = 0;
-  int n_runs = 0;
-  double build_ms = 0.0;
-  // host export storage
-  std::vector<double> x_codebook, x_rep_point, x_rep_normal;
-  std::vector<int> x_patch_link, x_patch_box_off, x_rep_link;
-  std::vector<long long> x_box_cell, x_box_code_off;
-  std::vector<uint16_t> x_codes;
-};
+#include "dev_fieldbuild.cuh"
 
 namespace {
 
-template <typename K, typename V>
-void radix_sort_pairs(lg_ctx* ctx, const K* kin, K* kout, const V* vin, V* vout, long long n,
-                      int end_bit) {
-  size_t bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit,
-                                     ctx->stream));
-  void* tmp = ctx->tmp(bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kin, kout, vin, vout, (int)n, 0, end_bit,
-                                     ctx->stream));
-  LAUNCH(ctx);
-}
-
-int exclusive_scan_count(lg_ctx* ctx, const int* flags, int* ids, long long n) {
-  size_t bytes = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, ids, (int)n, ctx->stream));
-  void* tmp = ctx->tmp(bytes);
-  CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, flags, ids, (int)n, ctx->stream));
-  LAUNCH(ctx);
-  int last_id = 0, last_flag = 0;
-  CK(cudaMemcpyAsync(&last_id, ids + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(&last_flag, flags + n - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  return last_id + last_flag;
-}
-
-// ContactFieldIndex::build on the device (see dev_field.cuh).
-void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc& pd, int N,
-                        double w, uint64_t seed, int C, lg_field* out) {
-  if (pd.n_patches < 1) throw std::invalid_argument("index build: no patches");
-  if (w <= 0.0 || N < 1) throw std::invalid_argument("index build: bad box width or N");
-  cudaStream_t s = ctx->stream;
-  const bool timing = std::getenv("LG_TIMING") != nullptr;
-  auto t0 = std::chrono::steady_clock::now();
-  auto fmark = [&](const char* name) {
-    if (!timing) return;
-    cudaStreamSynchronize(s);
-    std::fprintf(stderr, "[lg timing]   field %-14s %9.3f ms\n", name,
-                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
-  };
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  bind_hand(ctx, hd);
-  fmark("bind_hand");
-  upload_patches(ctx, pd, out->patches);
-  fmark("patches");
-  DevPatches& P = out->patches;
-  auto cb = make_codebook(C);
-  out->x_codebook = cb;
-  const double* d_cb = dupload(out->codebook, cb.data(), cb.size(), s);
-  CK(cudaEventRecord(e0, s));
-  const int L = hd.n_links;
-  const long long V = (long long)N * P.F;
-  if (V > 0xffffffffll) throw std::invalid_argument("index build: too many contact vectors");
-  Buf frames, cells, codes16, cmm;
-  double* d_frames = dalloc<double>(frames, (size_t)N * L * 12);
-  k_field_frames<<<grid_for(N, 128), 128, 0, s>>>(N, seed, d_frames);
-  LAUNCH(ctx);
-  check_launch();
-  long long* d_cells = dalloc<long long>(cells, 3 * (size_t)V);
-  uint16_t* d_codes = dalloc<uint16_t>(codes16, (size_t)V);
-  long long* d_cmm = dalloc<long long>(cmm, 6);
-  long long init[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
-  CK(cudaMemcpyAsync(d_cmm, init, sizeof(init), cudaMemcpyHostToDevice, s));
-  size_t cb_smem = 3 * (size_t)C * sizeof(double);
-  if (cb_smem > 200 * 1024) throw std::invalid_argument("index build: codebook too large for the device build");
-  CK(cudaFuncSetAttribute(k_field_vectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb_smem));
-  k_field_vectors<<<grid_for(V, 256), 256, cb_smem, s>>>(
-      N, P.F, P.fp_link.as<int>(), P.fp_point.as<int>(), P.pts.as<double>(), P.nrm.as<double>(),
-      d_frames, d_cb, C, w, d_cells, d_codes, d_cmm, d_cmm + 3);
-  LAUNCH(ctx);
-  check_launch();
-  long long cmm_h[6];
-  CK(cudaMemcpyAsync(cmm_h, d_cmm, sizeof(cmm_h), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  KeyLayout KL;
-  int bc = bits_for((unsigned long long)(C - 1));
-  int bz = bits_for((unsigned long long)(cmm_h[5] - cmm_h[2]));
-  int by = bits_for((unsigned long long)(cmm_h[4] - cmm_h[1]));
-  int bx = bits_for((unsigned long long)(cmm_h[3] - cmm_h[0]));
-  int bp = bits_for((unsigned long long)(P.P - 1));
-  KL.sh_code = 0;
-  KL.sh_z = bc;
-  KL.sh_y = bc + bz;
-  KL.sh_x = bc + bz + by;
-  KL.sh_patch = bc + bz + by + bx;
-  KL.bits_total = KL.sh_patch + bp;
-  KL.base[0] = cmm_h[0];
-  KL.base[1] = cmm_h[1];
-  KL.base[2] = cmm_h[2];
-  if (KL.bits_total > 64) throw std::runtime_error("index build: packed field key exceeds 64 bits");
-  Buf keys, keys2, vals, vals2, chead, bhead, cid, bid;
-  auto* d_keys = dalloc<unsigned long long>(keys, (size_t)V);
-  auto* d_keys2 = dalloc<unsigned long long>(keys2, (size_t)V);
-  auto* d_vals = dalloc<uint32_t>(vals, (size_t)V);
-  auto* d_vals2 = dalloc<uint32_t>(vals2, (size_t)V);
-  k_field_keys<<<grid_for(V, 256), 256, 0, s>>>(V, P.F, P.fp_patch.as<int>(), d_cells, d_codes, KL,
-                                                 d_keys, d_vals);
-  LAUNCH(ctx);
-  check_launch();
-  radix_sort_pairs(ctx, d_keys, d_keys2, d_vals, d_vals2, V, std::max(1, KL.bits_total));
-  int* d_ch = dalloc<int>(chead, (size_t)V);
-  int* d_bh = dalloc<int>(bhead, (size_t)V);
-  int* d_cid = dalloc<int>(cid, (size_t)V);
-  int* d_bid = dalloc<int>(bid, (size_t)V);
-  k_field_heads<<<grid_for(V, 256), 256, 0, s>>>(V, d_keys2, KL.sh_z, d_ch, d_bh);
-  LAUNCH(ctx);
-  check_launch();
-  fmark("sorted");
-  long long n_codes = exclusive_scan_count(ctx, d_ch, d_cid, V);
-  long long n_boxes = exclusive_scan_count(ctx, d_bh, d_bid, V);
-  auto* o_codes = dalloc<uint16_t>(out->codes, (size_t)n_codes);
-  auto* o_rep = dalloc<int>(out->rep_point, (size_t)n_codes);
-  auto* o_cell = dalloc<long long>(out->box_cell, 3 * (size_t)n_boxes);
-  auto* o_bpatch = dalloc<int>(out->box_patch, (size_t)n_boxes);
-  auto* o_bco = dalloc<long long>(out->box_code_off, (size_t)n_boxes + 1);
-  auto* o_pbo = dalloc<int>(out->patch_box_off, (size_t)P.P + 1);
-  k_field_emit<<<grid_for(V, 256), 256, 0, s>>>(V, P.F, d_keys2, d_vals2, d_ch, d_bh, d_cid, d_bid,
-                                                 d_cells, P.fp_patch.as<int>(), P.fp_point.as<int>(),
-                                                 KL, o_codes, o_rep, o_cell, o_bpatch, o_bco, o_pbo);
-  LAUNCH(ctx);
-  check_launch();
-  int nb_i = (int)n_boxes;
-  long long nc_ll = n_codes;
-  CK(cudaMemcpyAsync(o_pbo + P.P, &nb_i, sizeof(int), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(o_bco + n_boxes, &nc_ll, sizeof(long long), cudaMemcpyHostToDevice, s));
-  dupload(out->patch_link, P.h_link.data(), P.h_link.size(), s);
-
-  fmark("emitted");
-  // cell hash: boxes keyed by (cell, patch)
-  KeyLayout K2;
-  K2.sh_patch = 0;
-  K2.sh_z = bp;
-  K2.sh_y = bp + bz;
-  K2.sh_x = bp + bz + by;
-  K2.sh_code = 0;
-  K2.bits_total = bp + bz + by + bx;
-  K2.base[0] = KL.base[0];
-  K2.base[1] = KL.base[1];
-  K2.base[2] = KL.base[2];
-  Buf ck, ck2, cv, cv2, chd, crid;
-  auto* d_ck = dalloc<unsigned long long>(ck, (size_t)n_boxes);
-  auto* d_ck2 = dalloc<unsigned long long>(ck2, (size_t)n_boxes);
-  auto* d_cv = dalloc<uint32_t>(cv, (size_t)n_boxes);
-  auto* o_cellbox = dalloc<int>(out->cell_box, (size_t)n_boxes);
-  k_cell_keys<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, o_cell, o_bpatch, K2, d_ck, d_cv);
-  LAUNCH(ctx);
-  check_launch();
-  radix_sort_pairs(ctx, d_ck, d_ck2, d_cv, (uint32_t*)o_cellbox, n_boxes, std::max(1, K2.bits_total));
-  int* d_chd = dalloc<int>(chd, (size_t)n_boxes);
-  int* d_crid = dalloc<int>(crid, (size_t)n_boxes);
-  k_cell_heads<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, d_ck2, K2.sh_z, d_chd);
-  LAUNCH(ctx);
-  check_launch();
-  int n_runs = exclusive_scan_count(ctx, d_chd, d_crid, n_boxes);
-  auto* o_rs = dalloc<int>(out->run_start, (size_t)n_runs);
-  auto* o_rc = dalloc<int>(out->run_count, (size_t)n_runs);
-  k_cell_runs<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, d_chd, d_crid, o_rs, o_rc, n_runs);
-  LAUNCH(ctx);
-  check_launch();
-  int cap = 1024;
-  while (cap < 2 * n_runs) cap <<= 1;
-  auto* o_hash = dalloc<int>(out->hash_run, (size_t)cap);
-  CK(cudaMemsetAsync(o_hash, 0xff, (size_t)cap * sizeof(int), s));
-  k_cell_hash_insert<<<grid_for(n_runs, 256), 256, 0, s>>>(n_runs, o_rs, o_cellbox, o_cell, cap - 1,
-                                                             o_hash);
-  LAUNCH(ctx);
-  check_launch();
-  fmark("hashed");
-  // dense grid + packed run-ordered records for the query kernel
-  {
-    int G = 0;
-    std::vector<int> gol = groups_of(hd, &G);
-    out->h_gop.resize(P.P);
-    for (int p = 0; p < P.P; ++p) out->h_gop[p] = gol[P.h_link[p]];
-    int* d_gop = dupload(out->gop, out->h_gop.data(), out->h_gop.size(), s);
-    long long dx = cmm_h[3] - cmm_h[0] + 1, dy = cmm_h[4] - cmm_h[1] + 1, dz = cmm_h[5] - cmm_h[2] + 1;
-    out->f.grid_ok = 0;
-    if (dx > 0 && dy > 0 && dz > 0 && dx * dy * dz <= (64ll << 20)) {
-      int2* g = dalloc<int2>(out->grid, (size_t)(dx * dy * dz));
-      CK(cudaMemsetAsync(g, 0, sizeof(int2) * (size_t)(dx * dy * dz), s));
-      k_grid_fill<<<grid_for(n_runs, 256), 256, 0, s>>>(n_runs, o_rs, o_rc, o_cellbox, o_cell, cmm_h[0],
-                                                         cmm_h[1], cmm_h[2], (int)dy, (int)dz, g);
-      LAUNCH(ctx);
-      check_launch();
-      int4* rec = dalloc<int4>(out->rec, (size_t)n_boxes);
-      k_rec_fill<<<grid_for(n_boxes, 256), 256, 0, s>>>(n_boxes, o_cellbox, o_bpatch, d_gop, o_bco, rec);
-      LAUNCH(ctx);
-      check_launch();
-      out->f.grid_ok = 1;
-      out->f.gbase[0] = cmm_h[0];
-      out->f.gbase[1] = cmm_h[1];
-      out->f.gbase[2] = cmm_h[2];
-      out->f.gdim[0] = (int)dx;
-      out->f.gdim[1] = (int)dy;
-      out->f.gdim[2] = (int)dz;
-      out->f.grid = g;
-      out->f.rec = rec;
-    }
-  }
-  fmark("grid");
-  CK(cudaEventRecord(e1, s));
-  CK(cudaStreamSynchronize(s));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  out->build_ms = ms;
-  out->n_vectors = V;
-  out->n_codes = n_codes;
-  out->n_runs = n_runs;
-  DField& f = out->f;
-  f.w = w;
-  f.C = C;
-  f.codebook = d_cb;
-  f.P = P.P;
-  f.patch_link = out->patch_link.as<int>();
-  f.patch_box_off = o_pbo;
-  f.B = n_boxes;
-  f.box_cell = o_cell;
-  f.box_patch = o_bpatch;
-  f.box_code_off = o_bco;
-  f.codes = o_codes;
-  f.rep_point = o_rep;
-  f.hash_mask = cap - 1;
-  f.hash_run = o_hash;
-  f.run_start = o_rs;
-  f.run_count = o_rc;
-  f.cell_box = o_cellbox;
-}
 
 // ------------------------------------------------------------- run_batch
 struct RunOut {
@@ -669,20 +424,47 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   Timer tk(s);     // per-kernel spans (realize, contact search)
   double realize_s = 0.0, copt_s = 0.0;
   // ---- field (ContactFieldIndex::build) or reuse
+  // build_field (pipeline.cpp:286-304): with cfg.cache the index is read
+  // from <out>/index_cache.bin when its key matches, else built and saved.
   std::unique_ptr<lg_field> own;
   lg_field* field = field_in;
   if (!field) {
     own.reset(new lg_field);
     own->ctx = ctx;
-    build_field_device(ctx, hd, pd, cfg.field_configs, cfg.box_width, cfg.seed, cfg.codebook_size,
-                       own.get());
+    uint64_t key = 0;
+    std::string cache_path = std::string(cfg.out) + "/index_cache.bin";
+    if (cfg.cache) {
+      if (lg_index_cache_key(&cfg, &key) != LG_OK) {
+        char msg[512];
+        lg_last_error(msg, sizeof(msg));
+        throw std::invalid_argument(msg);
+      }
+      if (!load_field(ctx, hd, cache_path.c_str(), key, own.get())) {
+        own.reset(new lg_field);
+        own->ctx = ctx;
+      }
+    }
+    if (!own->from_cache) {
+      build_field_device(ctx, hd, pd, cfg.field_configs, cfg.box_width, cfg.seed, cfg.codebook_size,
+                         own.get());
+      out.profile.field_build = own->build_ms * 1e-3;
+      if (cfg.cache) {
+        std::filesystem::create_directories(cfg.out);
+        save_field(own.get(), cache_path.c_str(), key);
+      }
+    }
     field = own.get();
-    out.profile.field_build = field->build_ms * 1e-3;
   } else {
     bind_hand(ctx, hd);
   }
+  out.profile.index_from_cache = field->from_cache ? 1 : 0;
   const DField& F = field->f;
-  const DevPatches& DP = field->patches;
+  DevPatches cache_patches;
+  if (field->from_cache) {
+    if (F.P != pd.n_patches) throw std::invalid_argument("run_batch: cached index does not match the hand's patches");
+    upload_patches(ctx, pd, cache_patches);
+  }
+  const DevPatches& DP = field->from_cache ? cache_patches : field->patches;
   out.profile.patches = F.P;
   out.profile.boxes = F.B;
   out.profile.field_vectors = field->n_vectors;
@@ -1525,29 +1307,10 @@ int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc*
 
 int lg_field_export(lg_field* f, lg_field_csr* o) {
   return lgc::guard([&] {
-    cudaStream_t s = f->ctx->stream;
+    if (!f || !o) throw std::invalid_argument("lg_field_export: null argument");
+    use_ctx(f->ctx);
+    export_field(f);
     const DField& F = f->f;
-    f->x_patch_link = f->patches.h_link;
-    f->x_patch_box_off = ddownload(F.patch_box_off, (size_t)F.P + 1, s);
-    f->x_box_cell = ddownload(F.box_cell, 3 * (size_t)F.B, s);
-    f->x_box_code_off = ddownload(F.box_code_off, (size_t)F.B + 1, s);
-    f->x_codes = ddownload(F.codes, (size_t)f->n_codes, s);
-    auto rp = ddownload(F.rep_point, (size_t)f->n_codes, s);
-    std::vector<int> point_link(f->patches.npts);
-    for (int p = 0; p < F.P; ++p)
-      for (int i = f->patches.h_point_off[p]; i < f->patches.h_point_off[p + 1]; ++i)
-        point_link[i] = f->patches.h_link[p];
-    f->x_rep_link.resize(f->n_codes);
-    f->x_rep_point.resize(3 * f->n_codes);
-    f->x_rep_normal.resize(3 * f->n_codes);
-    for (long long c = 0; c < f->n_codes; ++c) {
-      int i = rp[c];
-      f->x_rep_link[c] = point_link[i];
-      for (int a = 0; a < 3; ++a) {
-        f->x_rep_point[3 * c + a] = f->patches.h_pts[3 * i + a];
-        f->x_rep_normal[3 * c + a] = f->patches.h_nrm[3 * i + a];
-      }
-    }
     o->box_width = F.w;
     o->codebook_size = F.C;
     o->codebook = f->x_codebook.data();
@@ -1563,6 +1326,26 @@ int lg_field_export(lg_field* f, lg_field_csr* o) {
     o->rep_point = f->x_rep_point.data();
     o->rep_normal = f->x_rep_normal.data();
     o->n_vectors = f->n_vectors;
+  });
+}
+
+int lg_field_save(lg_field* f, const char* path, uint64_t key) {
+  return lgc::guard([&] {
+    if (!f || !path) throw std::invalid_argument("lg_field_save: null argument");
+    use_ctx(f->ctx);
+    save_field(f, path, key);
+  });
+}
+
+int lg_field_load(lg_ctx* ctx, const lg_hand_desc* hand, const char* path, uint64_t key,
+                  lg_field** out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !path || !out) throw std::invalid_argument("lg_field_load: null argument");
+    use_ctx(ctx);
+    *out = nullptr;
+    auto f = std::make_unique<lg_field>();
+    f->ctx = ctx;
+    if (load_field(ctx, *hand, path, key, f.get())) *out = f.release();
   });
 }
 

@@ -104,7 +104,8 @@ class Profile(C.Structure):
         ("d2h_bytes", C.c_longlong)] + [(n, C.c_longlong) for n in (
         "ik_iterations", "fk_evals", "wrench_evals", "wrench_grads", "proj_evals",
         "realize_calls", "collision_calls")] + [
-        ("realize_seconds", C.c_double), ("contact_opt_seconds", C.c_double)]
+        ("realize_seconds", C.c_double), ("contact_opt_seconds", C.c_double),
+        ("index_from_cache", C.c_longlong)]
 
 
 class Trace(C.Structure):
