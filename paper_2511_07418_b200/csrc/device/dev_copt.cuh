@@ -142,16 +142,17 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
 
 // One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
 // warm-started from `warm` ([3][kMaxC]); state st = [3][kMaxC].
+template <int NC>
 __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts& o,
                                             const double* warm, double* st, Ctr& ctr) {
   const int iters = warm ? o.warm_iterations : o.iterations;
   double* a = st;
-  double* bx = st + kMaxC;
-  double* by = st + 2 * kMaxC;
+  double* bx = st + NC;
+  double* by = st + 2 * NC;
   for (int i = 0; i < w.n; ++i) {
     a[i] = warm ? warm[i] : 1.0;
-    bx[i] = warm ? warm[kMaxC + i] : 0.0;
-    by[i] = warm ? warm[2 * kMaxC + i] : 0.0;
+    bx[i] = warm ? warm[NC + i] : 0.0;
+    by[i] = warm ? warm[2 * NC + i] : 0.0;
   }
   if (w.mu > 0.0) {
     pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
@@ -160,9 +161,13 @@ __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts
   return pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
 }
 
-constexpr int kCoptPerWarp = kMaxC * kSlot + 6 * kMaxC + 32 * (kSlot + 6 * kMaxC);
+// Per-warp shared doubles for problems of at most NC contacts.
+template <int NC>
+constexpr int copt_per_warp() { return NC * kSlot + 6 * NC + 32 * (kSlot + 6 * NC); }
 
 // Block per candidate, warp per restart, lanes over the n_inner mutations.
+// NC = compile-time bound on k + statics (sizes the shared-memory layout).
+template <int NC>
 __global__ void __launch_bounds__(128, 4)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
@@ -176,16 +181,16 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
   const int k = cfg.k;
   const int s = n_static[i];
   const int n = k + s;
-  double* W = s_co + warp * kCoptPerWarp;
+  double* W = s_co + warp * copt_per_warp<NC>();
   double* sp = W;                        // incumbent problem
-  double* inc = W + kMaxC * kSlot;       // incumbent solution (warm start)
-  double* win = inc + 3 * kMaxC;         // best mutation's solution of this step
-  double* lane_base = win + 3 * kMaxC;   // per lane: trial slot, working state, best state
-  double* tslot = lane_base + lane * (kSlot + 6 * kMaxC);
+  double* inc = W + NC * kSlot;       // incumbent solution (warm start)
+  double* win = inc + 3 * NC;         // best mutation's solution of this step
+  double* lane_base = win + 3 * NC;   // per lane: trial slot, working state, best state
+  double* tslot = lane_base + lane * (kSlot + 6 * NC);
   double* wst = tslot + kSlot;
-  double* bst = wst + 3 * kMaxC;
-  const int rstride = 2 + k + 3 * kMaxC;
-  double* res = s_co + nw * kCoptPerWarp;
+  double* bst = wst + 3 * NC;
+  const int rstride = 2 + k + 3 * NC;
+  double* res = s_co + nw * copt_per_warp<NC>();
   long long off[kMaxK], cnt[kMaxK];
   for (int q = 0; q < k; ++q) {
     off[q] = el_off[a * k + q];
@@ -214,7 +219,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       w.mu = cfg.mu;
       // cold solve: lanes over anchors, best anchor by strict '<'
       double val = kInf;
-      if (lane < n) val = pv_anchor(w, lane, cfg.o, nullptr, wst, ctr);
+      if (lane < n) val = pv_anchor<NC>(w, lane, cfg.o, nullptr, wst, ctr);
       if (!(val < kInf)) val = kInf;
       double best = val;
       int bl = val < kInf ? lane : 99;
@@ -230,8 +235,8 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       int anchor = best < kInf ? bl : -1;
       double obj = best;
       __syncwarp();
-      if (lane < 3 * kMaxC)
-        inc[lane] = anchor >= 0 ? lane_base[anchor * (kSlot + 6 * kMaxC) + kSlot + lane] : 0.0;
+      if (lane < 3 * NC)
+        inc[lane] = anchor >= 0 ? lane_base[anchor * (kSlot + 6 * NC) + kSlot + lane] : 0.0;
       __syncwarp();
       const uint64_t* M = D + k;
       for (int outer = 0; outer < cfg.n_outer; ++outer) {
@@ -255,27 +260,40 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               const double* P = el_p + 3 * off[q];
               double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
               int bi = 0;
-              for (long long e = 1; e < cnt[q]; ++e) {
+              const int ne = (int)cnt[q];
+              int e = 1;
+              // four independent distances in flight, compared in index order
+              for (; e + 4 <= ne; e += 4) {
+                double d0 = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                double d1 = sqnorm(sub(v3(P[3 * e + 3], P[3 * e + 4], P[3 * e + 5]), cp));
+                double d2 = sqnorm(sub(v3(P[3 * e + 6], P[3 * e + 7], P[3 * e + 8]), cp));
+                double d3 = sqnorm(sub(v3(P[3 * e + 9], P[3 * e + 10], P[3 * e + 11]), cp));
+                if (d0 < bd) { bd = d0; bi = e; }
+                if (d1 < bd) { bd = d1; bi = e + 1; }
+                if (d2 < bd) { bd = d2; bi = e + 2; }
+                if (d3 < bd) { bd = d3; bi = e + 3; }
+              }
+              for (; e < ne; ++e) {
                 double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
                 if (d2v < bd) {
                   bd = d2v;
-                  bi = (int)e;
+                  bi = e;
                 }
               }
               ctr.proj += (unsigned long long)cnt[q];
               cand = bi;
-              long long e = off[q] + bi;
-              slot_make(tslot, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+              const long long eg = off[q] + bi;
+              slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));
               PV tw = w;
               tw.tq = q;
               // warm solve over all anchors in this lane (run_solver)
               double bobj = kInf;
               for (int anc = 0; anc < n; ++anc) {
-                double va = pv_anchor(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, wst, ctr);
+                double va = pv_anchor<NC>(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, wst, ctr);
                 if (va < bobj) {
                   bobj = va;
                   an = anc;
-                  for (int c = 0; c < 3 * kMaxC; ++c) bst[c] = wst[c];
+                  for (int c = 0; c < 3 * NC; ++c) bst[c] = wst[c];
                 }
               }
               v = bobj;
@@ -299,7 +317,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               __syncwarp();
               // keep the winner's state before the next chunk reuses it; the
               // warm start (inc) stays the step's incumbent until the end
-              if (lane < 3 * kMaxC) win[lane] = lane_base[src * (kSlot + 6 * kMaxC) + kSlot + 3 * kMaxC + lane];
+              if (lane < 3 * NC) win[lane] = lane_base[src * (kSlot + 6 * NC) + kSlot + 3 * NC + lane];
               __syncwarp();
             }
           }
@@ -309,7 +327,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               long long e = off[q] + best_id;
               slot_make(sp + kSlot * q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
             }
-            if (lane < 3 * kMaxC) inc[lane] = win[lane];
+            if (lane < 3 * NC) inc[lane] = win[lane];
             __syncwarp();
             obj = best_obj;
             anchor = best_anchor;
@@ -321,7 +339,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
         R[0] = obj;
         R[1] = (double)anchor;
         for (int q = 0; q < k; ++q) R[2 + q] = (double)ids[q];
-        for (int c = 0; c < 3 * kMaxC; ++c) R[2 + k + c] = anchor >= 0 ? inc[c] : 0.0;
+        for (int c = 0; c < 3 * NC; ++c) R[2 + k + c] = anchor >= 0 ? inc[c] : 0.0;
       }
     }
     __syncthreads();
@@ -345,13 +363,17 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
     if (!(best[0] < kInf)) an = -1;
     out_anchor[a] = an;
     for (int q = 0; q < k; ++q) out_ids[a * kMaxK + q] = (int)best[2 + q];
-    for (int c = 0; c < 3 * kMaxC; ++c) out_sol[a * 3 * kMaxC + c] = best[2 + k + c];
+    for (int c = 0; c < 3 * kMaxC; ++c) {
+      int comp = c / kMaxC, ci = c % kMaxC;  // output keeps the [3][kMaxC] layout
+      out_sol[a * 3 * kMaxC + c] = ci < NC ? best[2 + k + comp * NC + ci] : 0.0;
+    }
     balanced[a] = (an >= 0 && best[0] < eps_stable) ? 1 : 0;
   }
 }
 
+template <int NC>
 __host__ __forceinline__ size_t copt2_smem(int k, int nw) {
-  return ((size_t)nw * kCoptPerWarp + (size_t)(nw + 1) * (2 + k + 3 * kMaxC)) * sizeof(double);
+  return ((size_t)nw * copt_per_warp<NC>() + (size_t)(nw + 1) * (2 + k + 3 * NC)) * sizeof(double);
 }
 
 }  // namespace lgd

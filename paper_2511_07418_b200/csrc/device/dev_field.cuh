@@ -49,6 +49,16 @@ struct DField {
   int gdim[3];
   const int2* grid;
   const int4* rec;
+  // code-major query path: grun = run id per grid cell (-1 empty);
+  // cmask[run][code] = OR of group bits of the cell's boxes holding code;
+  // dl_* = codes that can pass the theta test for directions in each cell
+  // of a cube map over the sphere (count -1: test every code).
+  const int* grun;
+  const uint32_t* cmask;
+  int cm_ok;
+  int dl_R;
+  const int2* dl_rng;
+  const uint16_t* dl_codes;
 };
 
 __device__ __forceinline__ uint64_t cell_hash(long long x, long long y, long long z) {
@@ -260,12 +270,111 @@ __global__ void k_cell_runs(long long B, const int* head, const int* run_id, int
 // Dense grid of runs + run-ordered packed box records.
 __global__ void k_grid_fill(int n_runs, const int* run_start, const int* run_count,
                             const int* cell_box, const long long* box_cell, long long bx,
-                            long long by, long long bz, int dy, int dz, int2* grid) {
+                            long long by, long long bz, int dy, int dz, int2* grid, int* grun) {
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_runs) return;
   const long long* c = box_cell + 3 * cell_box[run_start[r]];
   long long idx = ((c[0] - bx) * dy + (c[1] - by)) * dz + (c[2] - bz);
   grid[idx] = make_int2(run_start[r], run_count[r]);
+  grun[idx] = r;
+}
+
+// cmask[r][code] |= bit(group) for every (box, code) of run r; static
+// patches (group -1) never enter a mask.
+__global__ void k_cmask_fill(int n_runs, const int* run_start, const int* run_count,
+                             const int4* rec, const uint16_t* codes, int C, uint32_t* cmask) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_runs) return;
+  uint32_t* row = cmask + (size_t)r * C;
+  for (int j = run_start[r]; j < run_start[r] + run_count[r]; ++j) {
+    int4 b = rec[j];
+    if (b.x < 0) continue;
+    for (int q = b.y; q < b.y + b.z; ++q) row[codes[q]] |= 1u << b.x;
+  }
+}
+
+// Cube map over directions: face f in 0..5 = +x,-x,+y,-y,+z,-z, (u, v) in
+// [-1, 1]^2 on the face, R x R cells.  Returns -1 for a zero / non-finite m.
+__host__ __device__ __forceinline__ V3 cube_dir(int face, double u, double v) {
+  switch (face) {
+    case 0: return v3(1.0, u, v);
+    case 1: return v3(-1.0, u, v);
+    case 2: return v3(u, 1.0, v);
+    case 3: return v3(u, -1.0, v);
+    case 4: return v3(u, v, 1.0);
+    default: return v3(u, v, -1.0);
+  }
+}
+__device__ __forceinline__ int cube_cell(V3 m, int R) {
+  double ax = fabs(m.x), ay = fabs(m.y), az = fabs(m.z);
+  int face;
+  double u, v, d;
+  if (ax >= ay && ax >= az) {
+    face = m.x > 0.0 ? 0 : 1;
+    d = ax;
+    u = m.y;
+    v = m.z;
+  } else if (ay >= az) {
+    face = m.y > 0.0 ? 2 : 3;
+    d = ay;
+    u = m.x;
+    v = m.z;
+  } else {
+    face = m.z > 0.0 ? 4 : 5;
+    d = az;
+    u = m.x;
+    v = m.y;
+  }
+  if (!(d > 0.0) || !(d <= 1.7976931348623157e308)) return -1;
+  u /= d;
+  v /= d;
+  double fi = (u + 1.0) * 0.5 * R, fj = (v + 1.0) * 0.5 * R;
+  if (!(fi >= -1.0 && fi <= R + 1.0 && fj >= -1.0 && fj <= R + 1.0)) return -1;
+  int i = (int)fi, j = (int)fj;
+  i = i < 0 ? 0 : (i >= R ? R - 1 : i);
+  j = j < 0 ? 0 : (j >= R ? R - 1 : j);
+  return (face * R + i) * R + j;
+}
+
+// One block per cube cell: the codes whose direction lies within
+// acos(theta) + (cell angular radius) + 1e-6 rad of the cell centre — a
+// superset of the codes that can pass -dot(code, n) >= theta for any unit n
+// mapped to the cell.  The exact FP64 test is still applied per code.
+__global__ void k_dirlist(int R, int lmax, const double* cb, int C, double theta, int2* rng,
+                          uint16_t* out) {
+  __shared__ int cnt;
+  __shared__ double s_cos;
+  __shared__ double s_c[3];
+  const int cell = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int face = cell / (R * R), i = (cell / R) % R, j = cell % R;
+    double u0 = -1.0 + 2.0 * i / R, u1 = -1.0 + 2.0 * (i + 1) / R;
+    double v0 = -1.0 + 2.0 * j / R, v1 = -1.0 + 2.0 * (j + 1) / R;
+    V3 c = normalized(cube_dir(face, 0.5 * (u0 + u1), 0.5 * (v0 + v1)));
+    double rho = 0.0;
+    double us[2] = {u0, u1}, vs[2] = {v0, v1};
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        double d = dot(c, normalized(cube_dir(face, us[a], vs[b])));
+        rho = fmax(rho, acos(fmin(1.0, fmax(-1.0, d))));
+      }
+    double lim = acos(fmin(1.0, fmax(-1.0, theta))) + rho + 1e-6;
+    s_cos = lim >= 3.141592653589793 ? -2.0 : cos(lim);
+    s_c[0] = c.x;
+    s_c[1] = c.y;
+    s_c[2] = c.z;
+    cnt = 0;
+  }
+  __syncthreads();
+  for (int code = threadIdx.x; code < C; code += blockDim.x) {
+    double d = cb[3 * code] * s_c[0] + cb[3 * code + 1] * s_c[1] + cb[3 * code + 2] * s_c[2];
+    if (d >= s_cos) {
+      int k = atomicAdd(&cnt, 1);
+      if (k < lmax) out[(size_t)cell * lmax + k] = (uint16_t)code;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) rng[cell] = make_int2(cell * lmax, cnt <= lmax ? cnt : -1);
 }
 
 __global__ void k_rec_fill(long long B, const int* cell_box, const int* box_patch,
@@ -319,6 +428,35 @@ __device__ __forceinline__ void sample_hits(const DField& f, const double* cb, V
     int b = f.cell_box[j];
     if (box_hit(f, cb, b, n, theta)) visit(f.box_patch[b], b, 0.0);
   }
+}
+
+// Code-major reachability mask: bit g set iff some code c passes
+// -dot(c, n) >= theta and some group-g box of the cell holds c — the same
+// predicate as sample_mask with the two existentials swapped.  Only codes
+// of n's cube-map cell are tested (exact test; cell lists are supersets).
+__device__ __forceinline__ uint32_t sample_mask_cm(const DField& f, const double* cb, V3 p, V3 n,
+                                                   double theta) {
+  long long c[3];
+  cell_of(p, f.w, c);
+  long long x = c[0] - f.gbase[0], y = c[1] - f.gbase[1], z = c[2] - f.gbase[2];
+  if (x < 0 || y < 0 || z < 0 || x >= f.gdim[0] || y >= f.gdim[1] || z >= f.gdim[2]) return 0u;
+  int r = f.grun[(x * f.gdim[1] + y) * f.gdim[2] + z];
+  if (r < 0) return 0u;
+  const uint32_t* row = f.cmask + (size_t)r * f.C;
+  double n2 = dot(n, n);
+  int cell = (n2 >= 1.0 - 1e-9 && n2 <= 1.0 + 1e-9) ? cube_cell(neg(n), f.dl_R) : -1;
+  int2 rg = cell >= 0 ? f.dl_rng[cell] : make_int2(0, -1);
+  uint32_t bits = 0u;
+  if (rg.y >= 0) {
+    for (int t = 0; t < rg.y; ++t) {
+      int code = f.dl_codes[rg.x + t];
+      if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) bits |= row[code];
+    }
+  } else {
+    for (int code = 0; code < f.C; ++code)
+      if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) bits |= row[code];
+  }
+  return bits;
 }
 
 // Reachability mask of one transformed sample: bit g set iff some patch of

@@ -11,7 +11,9 @@ struct lg_field {
   DField f;
   DevPatches patches;
   Buf codebook, patch_link, patch_box_off, box_cell, box_patch, box_code_off, codes, rep_pn,
-      rep_link, hash_run, run_start, run_count, cell_box, grid, rec, gop;
+      rep_link, hash_run, run_start, run_count, cell_box, grid, rec, gop, grun, cmask, dl_rng,
+      dl_codes;
+  double dl_theta = NAN;  // theta the direction lists were built for
   std::vector<int> h_gop;  // dependency group per patch baked into rec
   long long n_vectors = 0, n_codes = 0;
   int n_runs = 0;
@@ -118,9 +120,11 @@ void finalize_field(lg_ctx* ctx, const lg_hand_desc& hd, const long long* cmin,
   out->f.grid_ok = 0;
   if (dx > 0 && dy > 0 && dz > 0 && dx * dy * dz <= (64ll << 20)) {
     int2* g = dalloc<int2>(out->grid, (size_t)(dx * dy * dz));
+    int* gr = dalloc<int>(out->grun, (size_t)(dx * dy * dz));
     CK(cudaMemsetAsync(g, 0, sizeof(int2) * (size_t)(dx * dy * dz), s));
+    CK(cudaMemsetAsync(gr, 0xff, sizeof(int) * (size_t)(dx * dy * dz), s));
     k_grid_fill<<<grid_for(n_runs, 256), 256, 0, s>>>(n_runs, o_rs, o_rc, o_cellbox, o_cell, cmin[0],
-                                                       cmin[1], cmin[2], (int)dy, (int)dz, g);
+                                                       cmin[1], cmin[2], (int)dy, (int)dz, g, gr);
     LAUNCH(ctx);
     check_launch();
     int4* rec = dalloc<int4>(out->rec, (size_t)n_boxes);
@@ -134,6 +138,20 @@ void finalize_field(lg_ctx* ctx, const lg_hand_desc& hd, const long long* cmin,
     out->f.gdim[2] = (int)dz;
     out->f.grid = g;
     out->f.rec = rec;
+    out->f.grun = gr;
+    // code-major masks (sample_mask_cm) when they fit in 1 GiB
+    const int C = out->f.C > 0 ? out->f.C : 0;
+    out->f.cm_ok = 0;
+    if (C > 0 && (size_t)n_runs * C * sizeof(uint32_t) <= (1ull << 30)) {
+      uint32_t* cm = dalloc<uint32_t>(out->cmask, (size_t)n_runs * C);
+      CK(cudaMemsetAsync(cm, 0, sizeof(uint32_t) * (size_t)n_runs * C, s));
+      k_cmask_fill<<<grid_for(n_runs, 128), 128, 0, s>>>(n_runs, o_rs, o_rc, rec,
+                                                          out->codes.as<uint16_t>(), C, cm);
+      LAUNCH(ctx);
+      check_launch();
+      out->f.cmask = cm;
+      out->f.cm_ok = 1;
+    }
   }
   out->n_runs = n_runs;
   DField& f = out->f;
@@ -249,6 +267,7 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   CK(cudaMemcpyAsync(o_bco + n_boxes, &nc_ll, sizeof(long long), cudaMemcpyHostToDevice, s));
   dupload(out->patch_link, P.h_link.data(), P.h_link.size(), s);
   CK(cudaStreamSynchronize(s));
+  out->f.C = C;
   finalize_field(ctx, hd, cmm_h, cmm_h + 3, P.P, n_boxes, out);
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
@@ -262,6 +281,26 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   out->f.w = w;
   out->f.C = C;
   out->f.codebook = d_cb;
+}
+
+// Direction lists for the code-major query at this theta (built once per
+// (field, theta) on the device).  Returns false when the path is off.
+bool ensure_dirlists(lg_field* fl, double theta) {
+  DField& f = fl->f;
+  if (!f.grid_ok || !f.cm_ok || !(theta <= 0.99999)) return false;
+  if (fl->dl_theta == theta) return true;
+  constexpr int R = 32, LMAX = 96;
+  cudaStream_t s = fl->ctx->stream;
+  int2* rng = dalloc<int2>(fl->dl_rng, 6 * R * R);
+  uint16_t* codes = dalloc<uint16_t>(fl->dl_codes, (size_t)6 * R * R * LMAX);
+  k_dirlist<<<6 * R * R, 128, 0, s>>>(R, LMAX, f.codebook, f.C, theta, rng, codes);
+  LAUNCH(fl->ctx);
+  check_launch();
+  f.dl_R = R;
+  f.dl_rng = rng;
+  f.dl_codes = codes;
+  fl->dl_theta = theta;
+  return true;
 }
 
 // Host CSR copy of a device field (lg_field_export).
@@ -525,6 +564,7 @@ bool load_field(lg_ctx* ctx, const lg_hand_desc& hd, const char* path, uint64_t 
   dupload(out->rep_link, rlink.data(), rlink.size(), s);
   dupload(out->rep_pn, rpn.data(), rpn.size(), s);
   CK(cudaStreamSynchronize(s));
+  out->f.C = (int)cb;
   finalize_field(ctx, hd, cmin, cmax, P, B, out);
   CK(cudaStreamSynchronize(s));
   out->n_codes = (long long)codes.size();

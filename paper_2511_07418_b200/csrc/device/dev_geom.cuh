@@ -49,6 +49,9 @@ struct DHand {
 };
 
 __constant__ DHand c_hand;
+// Global mirror for lane-indexed reads: the constant cache serialises a warp's
+// distinct addresses, L1 serves them in one wavefront.
+__device__ DHand g_hand;
 
 // Algorithmic work counters (per thread in registers, folded into g_cnt with
 // one atomic per thread at kernel exit); feed the roofline's FLOP counts.

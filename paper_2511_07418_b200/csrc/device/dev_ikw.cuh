@@ -35,16 +35,16 @@ __device__ __forceinline__ void st_xf(double* p, const Xf& x) {
 // Pre-motion origin composed with the joint motion at q (hand.cpp:281-290).
 __device__ __forceinline__ Xf link_local(int l, const double* q) {
   Xf local;
-  local.R = m3_load(c_hand.R[l]);
-  local.t = v3_load(c_hand.t[l]);
-  int jt = c_hand.jtype[l];
+  local.R = m3_load(g_hand.R[l]);
+  local.t = v3_load(g_hand.t[l]);
+  int jt = g_hand.jtype[l];
   if (jt == 1) {
     Xf m;
-    m.R = angle_axis(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]));
+    m.R = angle_axis(q[g_hand.jidx[l]], v3_load(g_hand.axis[l]));
     m.t = v3(0.0, 0.0, 0.0);
     local = xf_compose(local, m);
   } else if (jt == 2) {
-    local.t = add(local.t, mul(local.R, scale(q[c_hand.jidx[l]], v3_load(c_hand.axis[l]))));
+    local.t = add(local.t, mul(local.R, scale(q[g_hand.jidx[l]], v3_load(g_hand.axis[l]))));
   }
   return local;
 }
@@ -53,12 +53,14 @@ __device__ __forceinline__ Xf link_local(int l, const double* q) {
 __device__ __forceinline__ void wfk_s(const double* q, double* F, int lane) {
   const int nl = c_hand.n_links;
   Xf loc = xf_identity();
-  if (lane < nl) loc = link_local(lane, q);
+  int lvl = -1, p = -1;
+  if (lane < nl) {
+    loc = link_local(lane, q);
+    lvl = g_hand.level[lane];
+    p = g_hand.parent[lane];
+  }
   for (int d = 0; d < c_hand.n_levels; ++d) {
-    if (lane < nl && c_hand.level[lane] == d) {
-      int p = c_hand.parent[lane];
-      st_xf(F + 12 * lane, p < 0 ? loc : xf_compose(ld_xf(F + 12 * p), loc));
-    }
+    if (lvl == d) st_xf(F + 12 * lane, p < 0 ? loc : xf_compose(ld_xf(F + 12 * p), loc));
     __syncwarp();
   }
 }
@@ -233,12 +235,12 @@ __device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
 // solve_contact_ik (ik.cpp:31-139).  q (smem) in/out; F (smem) receives the
 // frames at the final q; Ft is trial scratch.  Returns finite; used = OR of
 // joints with a nonzero column.
-__device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
+__device__ __noinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
                     unsigned long long& used, WarpWs& ws, double* F, double* Ft, Ctr& ctr,
                     int lane) {
   const int dof = c_hand.dof;
   const int rows = 6 * k;
-  if (lane < dof) q[lane] = dclamp(q[lane], c_hand.jlo[lane], c_hand.jhi[lane]);
+  if (lane < dof) q[lane] = dclamp(q[lane], g_hand.jlo[lane], g_hand.jhi[lane]);
   __syncwarp();
   used = 0ull;
   wfk_s(q, F, lane);
@@ -261,10 +263,10 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
     __syncwarp();
     // joint columns
     if (lane < dof) {
-      int lj = c_hand.jlink[lane];
+      int lj = g_hand.jlink[lane];
       Xf Fj = ld_xf(F + 12 * lj);
-      V3 axis = mul(Fj.R, v3_load(c_hand.axis[lj]));
-      bool rev = c_hand.jtype[lj] == 1;
+      V3 axis = mul(Fj.R, v3_load(g_hand.axis[lj]));
+      bool rev = g_hand.jtype[lj] == 1;
       double cm = 0.0;
       for (int p = 0; p < 2 * k; ++p) {
         bool on = (c_hand.jmask[T.link[p >> 1]] >> lane) & 1u;
@@ -289,9 +291,8 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
     __syncwarp();
     // J^T J (upper triangle, mirrored) and J^T r
     const int ne = dof * (dof + 1) / 2;
-    for (int e = lane; e < ne; e += 32) {
-      int a = 0, rem = e;
-      while (rem >= dof - a) {
+    for (int e = lane, a = 0, rem = lane; e < ne; e += 32, rem += 32) {
+      while (rem >= dof - a) {  // row-major upper-triangle index -> (a, b)
         rem -= dof - a;
         ++a;
       }
@@ -324,8 +325,8 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
     double dq = lane < dof ? ws.x[lane] : 0.0;
     for (int bt = 0; bt <= P.max_backtracks; ++bt) {
       if (lane < dof)
-        ws.qt[lane] = dclamp(q[lane] + dmin(dmax(dq, -P.step_clamp), P.step_clamp), c_hand.jlo[lane],
-                             c_hand.jhi[lane]);
+        ws.qt[lane] = dclamp(q[lane] + dmin(dmax(dq, -P.step_clamp), P.step_clamp), g_hand.jlo[lane],
+                             g_hand.jhi[lane]);
       __syncwarp();
       wfk_s(ws.qt, Ft, lane);
       ++ctr.fk;
@@ -355,7 +356,7 @@ __device__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int ite
 
 // realize_grasp's project (pipeline.cpp:196-220) at frames F: worst
 // distance (all lanes), optionally refreshing hand points into R.
-__device__ __forceinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
+__device__ __noinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
                                            int lane) {
   double d = 0.0;
   if (lane < k) {
@@ -412,16 +413,16 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
 
 // Per-warp shared bytes: workspace + targets, refreshed targets, q, qs,
 // three frame buffers, links (16-byte aligned).
-__host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof) {
-  size_t b = warp_ws_bytes(kMaxK, dof) + (size_t)(24 * kMaxK + 2 * kMaxDof + 3 * 12 * kMaxLinks) * sizeof(double) +
-             2 * kMaxK * sizeof(int);
+__host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof, int kmax, int nl) {
+  size_t b = warp_ws_bytes(kmax, dof) + (size_t)(24 * kmax + 2 * dof + 3 * 12 * nl) * sizeof(double) +
+             2 * kmax * sizeof(int);
   return (b + 15) & ~(size_t)15;
 }
 
 // One warp per problem; targets [t][kMaxK][12] + links [t][kMaxK]; q_out
 // [t][kMaxDof] holds q0 on entry (mid_config when q_init == nullptr).
 __global__ void __launch_bounds__(128, 4)
-k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_iters,
+k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, int fine_iters,
                const double* tgt, int tgt_stride, const int* tl, int tl_stride,
                const double* q_init, double* q_out, double* max_res, int* finite,
                unsigned long long* used) {
@@ -431,23 +432,24 @@ k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_ite
   if (t >= nAct) return;  // warp-uniform
   const int kt = kk ? kk[t] : k;
   const int dof = c_hand.dof;
-  char* base = s_ik + (size_t)warp * realize_warp_bytes(dof);
+  const int nl = c_hand.n_links;
+  char* base = s_ik + (size_t)warp * realize_warp_bytes(dof, kmax, nl);
   WarpWs ws = warp_ws(base, kt, dof);
-  double* extra = (double*)(base + warp_ws_bytes(kMaxK, dof));
+  double* extra = (double*)(base + warp_ws_bytes(kmax, dof));
   WTargets T, Ref;
   T.t = extra;
-  Ref.t = extra + 12 * kMaxK;
-  double* q = extra + 24 * kMaxK;
-  double* qs = q + kMaxDof;
-  double* F = qs + kMaxDof;
-  double* Fs = F + 12 * kMaxLinks;
-  double* Ft = Fs + 12 * kMaxLinks;
-  T.link = (int*)(Ft + 12 * kMaxLinks);
-  Ref.link = T.link + kMaxK;
+  Ref.t = extra + 12 * kmax;
+  double* q = extra + 24 * kmax;
+  double* qs = q + dof;
+  double* F = qs + dof;
+  double* Fs = F + 12 * nl;
+  double* Ft = Fs + 12 * nl;
+  T.link = (int*)(Ft + 12 * nl);
+  Ref.link = T.link + kmax;
   const double* src = tgt + (size_t)t * tgt_stride;
   for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
   if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
-  if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : c_hand.mid[lane];
+  if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
   __syncwarp();
   Ctr ctr = {0, 0, 0, 0, 0};
   double mr;
@@ -462,8 +464,8 @@ k_realize_warp(int nAct, int k, const int* kk, IkCfg P, int rounds, int fine_ite
   }
 }
 
-__host__ __forceinline__ size_t realize_warp_smem(int dof, int warps) {
-  return realize_warp_bytes(dof) * warps;
+__host__ __forceinline__ size_t realize_warp_smem(int dof, int kmax, int nl, int warps) {
+  return realize_warp_bytes(dof, kmax, nl) * warps;
 }
 
 }  // namespace lgd

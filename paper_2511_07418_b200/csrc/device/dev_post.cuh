@@ -70,7 +70,7 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
     }
     if (pb < pa || !ovl(s_box + 6 * pa, s_box + 6 * pb)) continue;
     int la = C.part_link[pa], lb = C.part_link[pb];
-    if (la == lb || c_hand.parent[la] == lb || c_hand.parent[lb] == la) continue;
+    if (la == lb || g_hand.parent[la] == lb || g_hand.parent[lb] == la) continue;
     if (clean_only && *(volatile int*)&s_viol) continue;
     if (gjk_distance(pa, ld_xf(s_fr + 12 * la), pb, ld_xf(s_fr + 12 * lb)) == 0.0)
       atomicOr(&s_viol, 1);

@@ -355,6 +355,42 @@ k_query2(int Bl, DField f, DSamples fs, const double* pose, const int* accepted,
   for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = s_cnt[g];
 }
 
+// Code-major query (sample_mask_cm): block per candidate, thread per field
+// sample; a sample costs one grid read plus ~10 code tests.
+__global__ void __launch_bounds__(256)
+k_query3(int Bl, DField f, DSamples fs, const double* pose, const int* accepted, double theta,
+         int G, int cb_in_smem, uint32_t* mask, int* dom_count) {
+  extern __shared__ double s_cb[];
+  __shared__ int s_cnt[LG_MAX_GROUPS];
+  const int i = blockIdx.x;
+  if (i >= Bl) return;
+  uint32_t* m = mask + (size_t)i * fs.n;
+  if (!accepted[i]) {
+    for (int j = threadIdx.x; j < fs.n; j += blockDim.x) m[j] = 0u;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = 0;
+    return;
+  }
+  if (cb_in_smem)
+    for (int a = threadIdx.x; a < 3 * f.C; a += blockDim.x) s_cb[a] = f.codebook[a];
+  for (int g = threadIdx.x; g < LG_MAX_GROUPS; g += blockDim.x) s_cnt[g] = 0;
+  __syncthreads();
+  const Xf x = load_xf(pose + 12 * i);
+  for (int j = threadIdx.x; j < fs.n; j += blockDim.x) {
+    V3 p = xf_apply(x, fs.p(j));
+    V3 n = xf_rotate(x, fs.nrm(j));
+    uint32_t bits = cb_in_smem ? sample_mask_cm(f, s_cb, p, n, theta)
+                               : sample_mask_cm(f, f.codebook, p, n, theta);
+    m[j] = bits;
+    while (bits) {
+      int g = __ffs(bits) - 1;
+      bits &= bits - 1;
+      atomicAdd(&s_cnt[g], 1);
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = s_cnt[g];
+}
+
 // Per-candidate world AABB of the raw object samples (the broad-phase
 // object box of validate_grasp_collisions, collision.cpp:243-245).
 __global__ void k_obj_aabb(int Bl, DSamples raw, const double* pose, const int* accepted,
@@ -476,282 +512,6 @@ struct CoptCfg {
   long long per_restart, per_cand;
 };
 
-// contact_opt.cpp:45-142: block per candidate, one warp per restart, lanes
-// over the n_inner mutations of a (outer, slot) step.  Every mutation is
-// projected and warm-solved independently from the same incumbent; the
-// winner is argmin (objective, m) among objectives strictly below the
-// incumbent, identical to the sequential first-strict-improvement rule.
-__global__ void k_contact_opt(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static,
-                              const double* st_p, const double* st_n, const long long* el_off,
-                              const int* el_s, const double* el_p, const double* el_n,
-                              const uint64_t* draws, int* out_ids, double* out_obj,
-                              int* out_anchor, double* out_sol, double eps_stable, int* balanced) {
-  extern __shared__ double s_res[];  // per warp: objective, ids[k], anchor, sol[3*6]
-  const int a = blockIdx.x;
-  if (a >= nA) return;
-  const int i = alive_idx[a];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int k = cfg.k;
-  const int s = n_static[i];
-  const int n = k + s;
-  const int stride = 2 + k + 3 * kMaxC;
-  long long off[kMaxK], cnt[kMaxK];
-  for (int q = 0; q < k; ++q) {
-    off[q] = el_off[a * k + q];
-    cnt[q] = el_off[a * k + q + 1] - off[q];
-  }
-  Ctr ctr = {0, 0, 0, 0, 0};
-  for (int rbase = 0; rbase < cfg.restarts; rbase += nw) {
-    const int r = rbase + warp;
-    if (r < cfg.restarts) {
-    const uint64_t* D = draws + (size_t)a * cfg.per_cand + (size_t)r * cfg.per_restart;
-    WProb prob;
-    prob.n = n;
-    prob.lambda = cfg.lambda;
-    prob.mu = cfg.mu;
-    if (s) wprob_set(prob, k, v3_load(st_p + 3 * i), v3_load(st_n + 3 * i));
-    int ids[kMaxK];
-    for (int q = 0; q < k; ++q) {
-      ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
-      long long e = off[q] + ids[q];
-      wprob_set(prob, q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
-    }
-    // cold solve: lanes over anchors, best anchor by strict '<'
-    WState sol;
-    double obj;
-    int anchor;
-    {
-      WState st;
-      double val = kInf;
-      if (lane < n) val = wsolve_anchor(prob, lane, prob.mu > 0.0, cfg.o, nullptr, st, ctr);
-      if (!(val < kInf)) val = kInf;  // NaN / inf anchors never win (strict '<')
-      double best = val;
-      int bl = val < kInf ? lane : 99;
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        if (ov < best || (ov == best && ol < bl)) {
-          best = ov;
-          bl = ol;
-        }
-      }
-      // anchors whose value is not < inf never win (reference: strict '<')
-      anchor = (best < kInf) ? bl : -1;
-      obj = best;
-      int src = anchor >= 0 ? anchor : 0;
-      for (int c = 0; c < kMaxC; ++c) {
-        sol.a[c] = __shfl_sync(0xffffffffu, st.a[c], src);
-        sol.bx[c] = __shfl_sync(0xffffffffu, st.bx[c], src);
-        sol.by[c] = __shfl_sync(0xffffffffu, st.by[c], src);
-      }
-    }
-    const uint64_t* M = D + k;
-    for (int outer = 0; outer < cfg.n_outer; ++outer) {
-      for (int q = 0; q < k; ++q) {
-        long long ce = off[q] + ids[q];
-        V3 cur_p = v3_load(el_p + 3 * ce);
-        V3 tx, ty;
-        tangent_basis(neg(v3_load(el_n + 3 * ce)), tx, ty);
-        double best_obj = obj;
-        int best_m = 0x7fffffff, best_id = -1;
-        WState best_sol = sol;
-        int best_anchor = -1;
-        for (int mb = 0; mb < cfg.n_inner; mb += 32) {
-          int m = mb + lane;
-          double val = kInf;
-          int cand = -1, an = -1;
-          WState ws;
-          if (m < cfg.n_inner) {
-            const uint64_t* d2 = M + 2 * ((long long)(outer * k + q) * cfg.n_inner + m);
-            double z1, z2;
-            box_muller(d2[0], d2[1], &z1, &z2);
-            double u = cfg.sigma * z1;
-            double v = cfg.sigma * z2;
-            V3 cp = axpy(axpy(cur_p, u, tx), v, ty);
-            // project_to_domain (contact_opt.cpp:11-25)
-            const double* P = el_p + 3 * off[q];
-            double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
-            int bi = 0;
-            ctr.proj += (unsigned long long)cnt[q];
-            for (long long e = 1; e < cnt[q]; ++e) {
-              double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-              if (d2v < bd) {
-                bd = d2v;
-                bi = (int)e;
-              }
-            }
-            cand = bi;
-            WProb trial = prob;
-            long long e = off[q] + bi;
-            wprob_set(trial, q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
-            val = wsolve(trial, cfg.o, anchor >= 0 ? &sol : nullptr, &an, ws, ctr);
-          }
-          // lowest (value, m) among value < best_obj
-          double bv = (val < best_obj) ? val : kInf;
-          int bm = (val < best_obj) ? m : 0x7fffffff;
-          for (int o = 16; o > 0; o >>= 1) {
-            double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            int om = __shfl_xor_sync(0xffffffffu, bm, o);
-            if (ov < bv || (ov == bv && om < bm)) {
-              bv = ov;
-              bm = om;
-            }
-          }
-          if (bm != 0x7fffffff) {
-            int src = bm - mb;
-            best_obj = bv;
-            best_m = bm;
-            best_id = __shfl_sync(0xffffffffu, cand, src);
-            best_anchor = __shfl_sync(0xffffffffu, an, src);
-            for (int c = 0; c < kMaxC; ++c) {
-              best_sol.a[c] = __shfl_sync(0xffffffffu, ws.a[c], src);
-              best_sol.bx[c] = __shfl_sync(0xffffffffu, ws.bx[c], src);
-              best_sol.by[c] = __shfl_sync(0xffffffffu, ws.by[c], src);
-            }
-          }
-        }
-        (void)best_m;
-        if (best_id >= 0) {
-          ids[q] = best_id;
-          long long e = off[q] + best_id;
-          wprob_set(prob, q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
-          sol = best_sol;
-          obj = best_obj;
-          anchor = best_anchor;
-        }
-      }
-    }
-    if (lane == 0) {
-      double* R = s_res + warp * stride;
-      R[0] = obj;
-      R[1] = (double)anchor;
-      for (int q = 0; q < k; ++q) R[2 + q] = (double)ids[q];
-      for (int c = 0; c < kMaxC; ++c) {
-        R[2 + k + c] = sol.a[c];
-        R[2 + k + kMaxC + c] = sol.bx[c];
-        R[2 + k + 2 * kMaxC + c] = sol.by[c];
-      }
-    }
-    }  // r < restarts
-    // fold this round's restarts into the per-block result in restart order
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double* best = s_res + nw * stride;
-      for (int w = 0; w < nw && rbase + w < cfg.restarts; ++w) {
-        double* R = s_res + w * stride;
-        bool first = (rbase + w) == 0;
-        if (first || R[0] < best[0])
-          for (int t = 0; t < stride; ++t) best[t] = R[t];
-        if (first && !(R[0] < kInf)) best[0] = kInf;
-      }
-    }
-    __syncthreads();
-  }
-  ctr_flush(ctr);
-  if (threadIdx.x == 0) {
-    double* best = s_res + nw * stride;
-    out_obj[a] = best[0];
-    int an = (int)best[1];
-    // result.solution stays default (anchor -1) unless a restart beat +inf
-    if (!(best[0] < kInf)) an = -1;
-    out_anchor[a] = an;
-    for (int q = 0; q < k; ++q) out_ids[a * kMaxK + q] = (int)best[2 + q];
-    for (int c = 0; c < 3 * kMaxC; ++c) out_sol[a * 3 * kMaxC + c] = best[2 + k + c];
-    balanced[a] = (an >= 0 && best[0] < eps_stable) ? 1 : 0;
-  }
-}
-
-// ------------------------------------------------ lookup-attempt targets
-// reverse_lookup (contact_field.cpp:450-484) for every slot of the active
-// candidates: the element's hit list is recomputed from (sample, group,
-// pose) in patch order, one hit is drawn from stream 'revs', and the
-// best-aligned code of that box gives the representative.
-__global__ void k_targets(int nAct, const int* act, const int* alive_idx, int k, int attempt,
-                          int c_lo, int B, int pass, uint64_t seed, DField f,
-                          const int* group_of_patch, const double* patch_pts,
-                          const double* patch_nrm, const int* patch_link, const int* chosen,
-                          const int* opt_ids, const long long* el_off, const double* el_p,
-                          const double* el_n, double theta, double* tgt, int* tgt_link,
-                          int* err) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nAct * k) return;
-  int ai = t / k, slot = t % k;
-  int a = act[ai];
-  int i = alive_idx[a];
-  int g = chosen[i * kMaxK + slot];
-  long long e = el_off[a * k + slot] + opt_ids[a * kMaxK + slot];
-  V3 p = v3_load(el_p + 3 * e), n = v3_load(el_n + 3 * e);
-  int nh = 0;
-  sample_hits(f, f.codebook, p, n, theta, [&](int patch, int, double) {
-    if (group_of_patch[patch] == g) ++nh;
-  });
-  if (nh == 0) {
-    atomicExch(err, 1);
-    return;
-  }
-  uint64_t gid = (uint64_t)pass * B + (uint64_t)(c_lo + i);
-  DRng rng;
-  rng.seed(mix_seed(seed, kTagReverse, (gid << 6) + ((uint64_t)attempt << 3) + (uint64_t)slot));
-  int pick = (int)rng.index((uint64_t)nh);
-  int box = -1, cnt = 0;
-  sample_hits(f, f.codebook, p, n, theta, [&](int patch, int b, double) {
-    if (group_of_patch[patch] == g) {
-      if (cnt == pick) box = b;
-      ++cnt;
-    }
-  });
-  int best = -1;
-  double best_dot = -2.0;
-  long long q0 = f.box_code_off[box], q1 = f.box_code_off[box + 1];
-  for (long long q = q0; q < q1; ++q) {
-    int code = f.codes[q];
-    double d = -dot(v3(f.codebook[3 * code], f.codebook[3 * code + 1], f.codebook[3 * code + 2]), n);
-    if (d > best_dot) {
-      best_dot = d;
-      best = (int)(q - q0);
-    }
-  }
-  const double* rp = f.rep_pn + 6 * (q0 + best);
-  double* T = tgt + (size_t)(ai * k + slot) * 12;
-  v3_store(T, p);
-  v3_store(T + 3, neg(n));
-  v3_store(T + 6, v3_load(rp));
-  v3_store(T + 9, v3_load(rp + 3));
-  tgt_link[ai * k + slot] = patch_link[f.box_patch[box]];
-}
-
-__device__ __forceinline__ void load_targets(const double* tgt, const int* tl, int k, Target* T) {
-  for (int q = 0; q < k; ++q) {
-    const double* s = tgt + 12 * q;
-    T[q].op = v3_load(s);
-    T[q].on = v3_load(s + 3);
-    T[q].hp = v3_load(s + 6);
-    T[q].hn = v3_load(s + 9);
-    T[q].link = tl[q];
-  }
-}
-
-// realize_grasp from mid_config, one thread per active candidate.
-__global__ void k_realize(int nAct, int k, IkCfg P, int rounds, int fine_iters,
-                          const double* tgt, const int* tgt_link, double* q_out, double* max_res,
-                          int* finite, unsigned long long* used) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nAct) return;
-  Target T[kMaxK];
-  load_targets(tgt + (size_t)t * k * 12, tgt_link + t * k, k, T);
-  double q[kMaxDof];
-  for (int j = 0; j < c_hand.dof; ++j) q[j] = c_hand.mid[j];
-  double mr;
-  unsigned long long u;
-  Ctr ctr = {0, 0, 0, 0, 0};
-  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u, ctr);
-  ctr_flush(ctr);
-  for (int j = 0; j < c_hand.dof; ++j) q_out[(size_t)t * kMaxDof + j] = q[j];
-  max_res[t] = mr;
-  finite[t] = fin ? 1 : 0;
-  used[t] = u;
-}
-
 // ------------------------------------------------ validate_grasp_collisions
 // collision.cpp:230-288, block per call.  Only clean() and the deepest
 // penetration feed decisions; both are order independent (any / max).
@@ -760,169 +520,6 @@ struct CollCfg {
   DSamples raw;
   const int* part_link;
 };
-
-__global__ void k_collision(int n_calls, CollCfg C, const int* call_cand, const int* call_on,
-                            const double* q_all, const double* pose, const double* obj_aabb,
-                            uint8_t* clean_out, double* maxpen_out) {
-  __shared__ double s_fr[kMaxLinks * 12];
-  __shared__ double s_box[64 * 6];
-  __shared__ int s_pairs[2 * 2112];
-  __shared__ int s_np;
-  __shared__ int s_viol;
-  __shared__ double scratch[32];
-  int call = blockIdx.x;
-  if (call >= n_calls) return;
-  if (call_on && !call_on[call]) return;
-  int i = call_cand[call];
-  const int np = c_hand.n_parts;
-  if (threadIdx.x == 0) {
-    Xf f[kMaxLinks];
-    fk(q_all + (size_t)call * kMaxDof, f);
-    for (int l = 0; l < c_hand.n_links; ++l) store_xf(s_fr + 12 * l, f[l]);
-    s_np = 0;
-    s_viol = 0;
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < np; p += blockDim.x) {
-    V3 mn, mx;
-    world_bounds(p, load_xf(s_fr + 12 * C.part_link[p]), &mn, &mx);
-    s_box[6 * p + 0] = mn.x - C.margin;
-    s_box[6 * p + 1] = mn.y - C.margin;
-    s_box[6 * p + 2] = mn.z - C.margin;
-    s_box[6 * p + 3] = mx.x + C.margin;
-    s_box[6 * p + 4] = mx.y + C.margin;
-    s_box[6 * p + 5] = mx.z + C.margin;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // broad_phase (collision.cpp:22-45), pair order kept
-    const double* ob = obj_aabb + 6 * i;
-    double oi[6] = {ob[0] - C.margin, ob[1] - C.margin, ob[2] - C.margin,
-                    ob[3] + C.margin, ob[4] + C.margin, ob[5] + C.margin};
-    bool have_obj = C.raw.n > 0;
-    int cnt = 0;
-    auto ovl = [](const double* a, const double* b) {
-      return a[0] <= b[3] && a[1] <= b[4] && a[2] <= b[5] && a[3] >= b[0] && a[4] >= b[1] &&
-             a[5] >= b[2];
-    };
-    for (int p = 0; p < np; ++p) {
-      for (int q = p + 1; q < np; ++q)
-        if (ovl(s_box + 6 * p, s_box + 6 * q) && cnt < 2112) {
-          s_pairs[2 * cnt] = p;
-          s_pairs[2 * cnt + 1] = q;
-          ++cnt;
-        }
-      if (have_obj && ovl(s_box + 6 * p, oi) && cnt < 2112) {
-        s_pairs[2 * cnt] = p;
-        s_pairs[2 * cnt + 1] = -1;
-        ++cnt;
-      }
-    }
-    s_np = cnt;
-  }
-  __syncthreads();
-  const int npairs = s_np;
-  // narrow phase 1: GJK on link-link candidates, one pair per thread
-  for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
-    int pa = s_pairs[2 * e], pb = s_pairs[2 * e + 1];
-    if (pb < 0) continue;
-    int la = C.part_link[pa], lb = C.part_link[pb];
-    if (la == lb || c_hand.parent[la] == lb || c_hand.parent[lb] == la) continue;
-    if (gjk_distance(pa, load_xf(s_fr + 12 * la), pb, load_xf(s_fr + 12 * lb)) == 0.0)
-      atomicOr(&s_viol, 1);
-  }
-  // narrow phase 2: half-plane depth of the object samples per part
-  Xf x = load_xf(pose + 12 * i);
-  double maxpen = 0.0;
-  for (int e = 0; e < npairs; ++e) {
-    int pa = s_pairs[2 * e], pb = s_pairs[2 * e + 1];
-    if (pb >= 0) continue;
-    Xf inv = xf_inverse(load_xf(s_fr + 12 * C.part_link[pa]));
-    const double* b = c_hand.bounds + 6 * pa;
-    double mx = 0.0;
-    bool off = false;
-    for (int j = threadIdx.x; j < C.raw.n; j += blockDim.x) {
-      V3 local = xf_apply(inv, xf_apply(x, C.raw.p(j)));
-      if (!(local.x >= b[0] - 1e-9 && local.y >= b[1] - 1e-9 && local.z >= b[2] - 1e-9 &&
-            local.x <= b[3] + 1e-9 && local.y <= b[4] + 1e-9 && local.z <= b[5] + 1e-9))
-        continue;
-      double depth = part_interior_depth(pa, local);
-      if (depth > C.margin) {
-        off = true;
-        mx = dmax(mx, depth);
-      }
-    }
-    if (off) atomicOr(&s_viol, 1);
-    mx = block_max(mx, scratch);
-    maxpen = dmax(maxpen, mx);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    clean_out[call] = s_viol ? 0 : 1;
-    if (maxpen_out) maxpen_out[call] = maxpen;
-  }
-}
-
-// ------------------------------------------------------ attempt bookkeeping
-// pipeline.cpp:496-520: keep the best attempt (clear first, then lower
-// residual); stop searching once a clear attempt is kept.
-__global__ void k_attempt_update(int nAct, const int* act, int k, int attempt,
-                                 const double* q_try, const double* res, const int* finite,
-                                 const unsigned long long* used, const uint8_t* clean,
-                                 const int* conv, const double* tgt, const int* tgt_link,
-                                 double contact_tol, int* have, int* best_clear,
-                                 double* best_res, double* best_q, unsigned long long* best_used,
-                                 double* best_tgt, int* best_link, int* best_attempt,
-                                 int* searching) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nAct) return;
-  int a = act[t];
-  if (!finite[t]) return;
-  bool cv = res[t] <= contact_tol;
-  bool clear = cv ? (clean[t] != 0) : false;
-  (void)conv;
-  bool better;
-  if (!have[a]) better = true;
-  else if (clear != (best_clear[a] != 0)) better = clear;
-  else better = res[t] < best_res[a];
-  if (better) {
-    have[a] = 1;
-    best_clear[a] = clear ? 1 : 0;
-    best_res[a] = res[t];
-    for (int j = 0; j < kMaxDof; ++j) best_q[(size_t)a * kMaxDof + j] = q_try[(size_t)t * kMaxDof + j];
-    best_used[a] = used[t];
-    for (int c = 0; c < 12 * k; ++c) best_tgt[(size_t)a * kMaxK * 12 + c] = tgt[(size_t)t * k * 12 + c];
-    for (int q = 0; q < k; ++q) best_link[a * kMaxK + q] = tgt_link[t * k + q];
-    best_attempt[a] = attempt;
-  }
-  if (best_clear[a]) searching[a] = 0;
-}
-
-// ------------------------------------------------------- unused joints
-// pipeline.cpp:535-551: every attempt redraws each unused joint in ascending
-// order from stream 'unus'; attempt j therefore starts at draw j * #unused.
-__global__ void k_unused_q(int nAct, const int* act, const int* alive_idx, int attempt, int c_lo,
-                           int B, int pass, uint64_t seed, const double* best_q,
-                           const unsigned long long* best_used, double* q_out) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nAct) return;
-  int a = act[t];
-  int i = alive_idx[a];
-  uint64_t gid = (uint64_t)pass * B + (uint64_t)(c_lo + i);
-  Mt64 g;
-  mt_seed(g, mix_seed(seed, kTagUnused, gid));
-  unsigned long long used = best_used[a];
-  const int dof = c_hand.dof;
-  int nu = 0;
-  for (int j = 0; j < dof; ++j)
-    if (!((used >> j) & 1ull)) ++nu;
-  for (long long d = 0; d < (long long)attempt * nu; ++d) mt_next(g);
-  double* q = q_out + (size_t)t * kMaxDof;
-  for (int j = 0; j < dof; ++j) {
-    q[j] = best_q[(size_t)a * kMaxDof + j];
-    if ((used >> j) & 1ull) continue;
-    q[j] = c_hand.jlo[j] + (c_hand.jhi[j] - c_hand.jlo[j]) * u01(mt_next(g));
-  }
-}
 
 // ------------------------------------------------------------ postprocess
 // pipeline.cpp:553-603: contacts re-projected at the final q, force
@@ -933,82 +530,5 @@ struct FinalCfg {
   double contact_tol, lambda, mu, eps;
   WOpts o;
 };
-
-__global__ void k_finalize(int nT, const int* act, const int* alive_idx, FinalCfg C, DSamples fs,
-                           const double* pose, const int* n_static, const int* st_link,
-                           const double* st_p, const double* st_n, const double* q_final,
-                           const uint8_t* clean, const double* best_tgt, const int* best_link,
-                           lg_grasp* out, int* valid, int* dropped) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nT) return;
-  int a = act[t];
-  int i = alive_idx[a];
-  const int k = C.k;
-  lg_grasp& g = out[a];
-  valid[a] = 0;
-  dropped[a] = 0;
-  g.n_contacts = 0;
-  g.penetration_free = 0;
-  g.stable = 0;
-  g.ik_converged = 0;
-  g.objective = 0.0;
-  const double* q = q_final + (size_t)a * kMaxDof;
-  Xf fr[kMaxLinks];
-  fk(q, fr);
-  Xf x = load_xf(pose + 12 * i);
-  double worst = 0.0;
-  for (int s = 0; s < k; ++s) {
-    const double* T = best_tgt + (size_t)a * kMaxK * 12 + 12 * s;
-    int link = best_link[a * kMaxK + s];
-    Xf inv = xf_inverse(fr[link]);
-    V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
-    double d = closest_on_parts(link, xf_apply(inv, v3_load(T)), &sp, &sn);
-    if (!is_finite(d)) {
-      dropped[a] = 1;
-      return;
-    }
-    worst = dmax(worst, d);
-    V3 pw = xf_apply(fr[link], sp);
-    int nearest = 0;
-    double best_d2 = kInf;
-    for (int j = 0; j < fs.n; ++j) {
-      double d2 = sqnorm(sub(xf_apply(x, fs.p(j)), pw));
-      if (d2 < best_d2) {
-        best_d2 = d2;
-        nearest = j;
-      }
-    }
-    int ci = g.n_contacts++;
-    v3_store(g.contact_p[ci], pw);
-    v3_store(g.contact_n[ci], neg(xf_rotate(x, fs.nrm(nearest))));
-    g.contact_link[ci] = link;
-  }
-  if (n_static[i]) {
-    int ci = g.n_contacts++;
-    v3_store(g.contact_p[ci], v3_load(st_p + 3 * i));
-    v3_store(g.contact_n[ci], v3_load(st_n + 3 * i));
-    g.contact_link[ci] = st_link[i];
-  }
-  g.ik_converged = worst <= C.contact_tol;
-  g.penetration_free = clean[a] ? 1 : 0;
-  WProb w;
-  w.n = g.n_contacts;
-  w.lambda = C.lambda;
-  w.mu = C.mu;
-  for (int c = 0; c < g.n_contacts; ++c) wprob_set(w, c, v3_load(g.contact_p[c]), v3_load(g.contact_n[c]));
-  WState ws;
-  int an;
-  Ctr ctr = {0, 0, 0, 0, 0};
-  double obj = wsolve(w, C.o, nullptr, &an, ws, ctr);
-  ctr_flush(ctr);
-  g.objective = obj;
-  g.stable = obj < C.eps ? 1 : 0;
-  g.g = 0;
-  m3_store(g.pose_R, x.R);
-  v3_store(g.pose_t, x.t);
-  g.dof = c_hand.dof;
-  for (int j = 0; j < c_hand.dof; ++j) g.q[j] = q[j];
-  valid[a] = (g.penetration_free && g.stable && g.ik_converged) ? 1 : 0;
-}
 
 }  // namespace lgd

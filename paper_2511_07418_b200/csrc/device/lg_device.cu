@@ -304,21 +304,23 @@ void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
   dupload(ctx->h_part_link, d.part_link, (size_t)d.n_parts, s);
   ctx->n_parts = d.n_parts;
   CK(cudaMemcpyToSymbolAsync(c_hand, &h, sizeof(DHand), 0, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyToSymbolAsync(g_hand, &h, sizeof(DHand), 0, cudaMemcpyHostToDevice, s));
 }
 
 // realize_grasp, one warp per problem, 4 warps per CTA.
 void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCfg& P, int rounds,
                          int fine_iters, const double* tgt, int tgt_stride, const int* tl,
                          int tl_stride, const double* q_init, double* q_out, double* max_res,
-                         int* finite, unsigned long long* used, int dof) {
+                         int* finite, unsigned long long* used, int dof, int n_links) {
   const int wpb = 4;
-  size_t smem = realize_warp_smem(dof, wpb);
+  const int kmax = kk ? kMaxK : k;
+  size_t smem = realize_warp_smem(dof, kmax, n_links, wpb);
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(k_realize_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  k_realize_warp<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, P, rounds, fine_iters, tgt,
+  k_realize_warp<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt,
                                                              tgt_stride, tl, tl_stride, q_init, q_out,
                                                              max_res, finite, used);
 }
@@ -641,7 +643,10 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       check_launch();
       int cb_smem = 3 * F.C <= 6144 ? 1 : 0;
       size_t qsm = cb_smem ? 3 * (size_t)F.C * sizeof(double) : 0;
-      if (F.grid_ok)
+      if (ensure_dirlists(field, cfg.theta_hit))
+        k_query3<<<Bl, 256, qsm, s>>>(Bl, field->f, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
+                                      d_mask, d_cnt);
+      else if (F.grid_ok)
         k_query2<<<Bl, 256, qsm, s>>>(Bl, F, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem, d_mask,
                                       d_cnt);
       else
@@ -754,17 +759,22 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     co.o = wo;
     co.per_restart = per_restart;
     co.per_cand = per_cand;
-    int nw = std::min(R, 8);
-    size_t co_smem = copt2_smem(k, nw);
+    int nw = std::min(R, 4);
     static bool co_attr = false;
     if (!co_attr) {
-      CK(cudaFuncSetAttribute(k_contact_opt2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CK(cudaFuncSetAttribute(k_contact_opt2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       co_attr = true;
     }
     tk.start();
-    k_contact_opt2<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp,
-                                                d_eln, d_draws, d_oid, d_oobj, d_oan, d_osol,
-                                                cfg.eps_stable, d_bal);
+    if (k + 1 <= 3)  // k contacts + at most one static
+      k_contact_opt2<3><<<nA, 32 * nw, copt2_smem<3>(k, nw), s>>>(
+          nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan,
+          d_osol, cfg.eps_stable, d_bal);
+    else
+      k_contact_opt2<kMaxC><<<nA, 32 * nw, copt2_smem<kMaxC>(k, nw), s>>>(
+          nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan,
+          d_osol, cfg.eps_stable, d_bal);
     LAUNCH(ctx);
     check_launch();
     copt_s += tk.stop();
@@ -841,7 +851,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       auto* d_used = dalloc<unsigned long long>(b_used, (size_t)nP);
       tk.start();
       launch_realize_warp(s, (int)nP, k, nullptr, ikc, cfg.finetune_rounds, cfg.finetune_iterations,
-                          d_tgt, k * 12, d_tl, k, nullptr, d_qt, d_res, d_fin, d_used, hd.dof);
+                          d_tgt, k * 12, d_tl, k, nullptr, d_qt, d_res, d_fin, d_used, hd.dof,
+                          hd.n_links);
       LAUNCH(ctx);
       check_launch();
       realize_s += tk.stop();
@@ -1056,26 +1067,6 @@ __global__ void k_wrench_batch(int m, const int* n, const double* pts, const dou
   }
 }
 
-__global__ void k_realize_var(int m, const int* kk, IkCfg P, int rounds, int fine_iters,
-                              const double* tgt, const int* tl, double* q_out, double* max_res,
-                              int* finite, unsigned long long* used) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m) return;
-  int k = kk[t];
-  Target T[kMaxK];
-  load_targets(tgt + (size_t)t * kMaxK * 12, tl + t * kMaxK, k, T);
-  double q[kMaxDof];
-  for (int j = 0; j < c_hand.dof; ++j) q[j] = q_out[(size_t)t * kMaxDof + j];
-  double mr;
-  unsigned long long u;
-  Ctr ctr = {0, 0, 0, 0, 0};
-  bool fin = realize_grasp(q, T, k, P, rounds, fine_iters, &mr, &u, ctr);
-  for (int j = 0; j < c_hand.dof; ++j) q_out[(size_t)t * kMaxDof + j] = q[j];
-  max_res[t] = mr;
-  finite[t] = fin ? 1 : 0;
-  used[t] = u;
-}
-
 }  // namespace
 
 extern "C" {
@@ -1217,7 +1208,7 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
     P.iterations = iterations;
     P.max_backtracks = 10;
     launch_realize_warp(s, m, 0, d_k, P, finetune_rounds, finetune_iterations, d_t, kMaxK * 12, d_l,
-                        kMaxK, d_q, d_q, d_r, d_f, d_u, hand->dof);
+                        kMaxK, d_q, d_q, d_r, d_f, d_u, hand->dof, hand->n_links);
     check_launch();
     auto hq = ddownload(d_q, q0.size(), s);
     for (int i = 0; i < m; ++i)
@@ -1379,7 +1370,10 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
     size_t qsm = cb_smem ? 3 * (size_t)f->f.C * sizeof(double) : 0;
     DField fq = f->f;  // the dense path bakes the field's own groups into rec
     if (!std::equal(f->h_gop.begin(), f->h_gop.end(), group_of_patch)) fq.grid_ok = 0;
-    k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
+    if (fq.grid_ok && ensure_dirlists(f, theta))
+      k_query3<<<m, 256, qsm, s>>>(m, f->f, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
+    else
+      k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
     check_launch();
     CK(cudaMemcpyAsync(masks, d_mask, sizeof(uint32_t) * m * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -17,7 +17,8 @@ for r in data:
     name = name if len(name) < 60 else name[:57] + "..."
     tot[name] += v
     cnt[name] += 1
-steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+# steps = launches of a once-per-pass kernel unless given
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, cnt.get("lgd::k_place_pose", 1))
 T = sum(tot.values())
 print(f"{'kernel':60s} {'launches':>8s} {'ms/step':>9s} {'share':>6s}")
 for n, v in sorted(tot.items(), key=lambda x: -x[1]):
