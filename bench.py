@@ -289,6 +289,8 @@ def run_b200(args):
         funnel={k: int(prof[k]) for k in ("candidates", "placements_accepted",
                                            "contact_sets_balanced", "ik_finite",
                                            "penetration_free", "ik_converged", "stable", "valid")},
+        work={k: int(prof[k]) for k in ("ik_iterations", "fk_evals", "wrench_evals", "wrench_grads",
+                                        "proj_evals", "realize_calls", "collision_calls")},
         stage_seconds={k: float(prof[k]) for k in ("field_build", "placement_domains",
                                                     "contact_optimization",
                                                     "kinematics_optimization", "postprocessing")},

@@ -84,15 +84,20 @@ __device__ __forceinline__ void acc_contact(const double* s, double a, double bx
   }
 }
 
-// descend (wrench.cpp:124-177) on state (a, bx, by) in shared memory.
-template <bool FR>
+// descend (wrench.cpp:124-177) on state (a, bx, by) in shared memory.  The
+// trial state goes to the lane's shared scratch `tr` ([3][NC]) and is copied
+// on acceptance instead of being recomputed from the gradient.
+template <bool FR, int NC>
 __device__ double pv_descend(const PV& w, int anchor, int iterations, double step0, int max_bt,
-                             double* a, double* bx, double* by, Ctr& ctr) {
+                             double* a, double* bx, double* by, double* tr, Ctr& ctr) {
   for (int i = 0; i < w.n; ++i) proj_one<FR>(i == anchor, w.mu, a[i], bx[i], by[i]);
   V3 f = v3(0.0, 0.0, 0.0), t = v3(0.0, 0.0, 0.0);
   for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], f, t);
   double current = sqnorm(f) + w.lambda * sqnorm(t);
   ++ctr.weval;
+  double* ta = tr;
+  double* tbx = tr + NC;
+  double* tby = tr + 2 * NC;
   for (int it = 0; it < iterations; ++it) {
     V3 force = v3(0.0, 0.0, 0.0), torque = v3(0.0, 0.0, 0.0);
     for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], force, torque);
@@ -104,30 +109,25 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
       V3 f2 = v3(0.0, 0.0, 0.0), t2 = v3(0.0, 0.0, 0.0);
       for (int i = 0; i < w.n; ++i) {
         const double* s = w.slot(i);
-        double ta = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
-        double tbx = 0.0, tby = 0.0;
+        double xa = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
+        double xbx = 0.0, xby = 0.0;
         if (FR) {
-          tbx = bx[i] - step * (2.0 * (dot(force, ld3(s + 6)) + dot(torque, ld3(s + 15))));
-          tby = by[i] - step * (2.0 * (dot(force, ld3(s + 9)) + dot(torque, ld3(s + 18))));
+          xbx = bx[i] - step * (2.0 * (dot(force, ld3(s + 6)) + dot(torque, ld3(s + 15))));
+          xby = by[i] - step * (2.0 * (dot(force, ld3(s + 9)) + dot(torque, ld3(s + 18))));
         }
-        proj_one<FR>(i == anchor, w.mu, ta, tbx, tby);
-        acc_contact<FR>(s, ta, tbx, tby, f2, t2);
+        proj_one<FR>(i == anchor, w.mu, xa, xbx, xby);
+        acc_contact<FR>(s, xa, xbx, xby, f2, t2);
+        ta[i] = xa;
+        tbx[i] = xbx;
+        tby[i] = xby;
       }
       double next = sqnorm(f2) + w.lambda * sqnorm(t2);
       ++ctr.weval;
       if (next <= current) {
         for (int i = 0; i < w.n; ++i) {
-          const double* s = w.slot(i);
-          double ta = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
-          double tbx = 0.0, tby = 0.0;
-          if (FR) {
-            tbx = bx[i] - step * (2.0 * (dot(force, ld3(s + 6)) + dot(torque, ld3(s + 15))));
-            tby = by[i] - step * (2.0 * (dot(force, ld3(s + 9)) + dot(torque, ld3(s + 18))));
-          }
-          proj_one<FR>(i == anchor, w.mu, ta, tbx, tby);
-          a[i] = ta;
-          bx[i] = tbx;
-          by[i] = tby;
+          a[i] = ta[i];
+          bx[i] = tbx[i];
+          by[i] = tby[i];
         }
         current = next;
         moved = true;
@@ -144,7 +144,7 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
 // warm-started from `warm` ([3][kMaxC]); state st = [3][kMaxC].
 template <int NC>
 __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts& o,
-                                            const double* warm, double* st, Ctr& ctr) {
+                                            const double* warm, double* st, double* tr, Ctr& ctr) {
   const int iters = warm ? o.warm_iterations : o.iterations;
   double* a = st;
   double* bx = st + NC;
@@ -155,20 +155,24 @@ __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts
     by[i] = warm ? warm[2 * NC + i] : 0.0;
   }
   if (w.mu > 0.0) {
-    pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
-    return pv_descend<true>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
+    pv_descend<false, NC>(w, anchor, iters, o.step, o.max_bt, a, bx, by, tr, ctr);
+    return pv_descend<true, NC>(w, anchor, iters, o.step, o.max_bt, a, bx, by, tr, ctr);
   }
-  return pv_descend<false>(w, anchor, iters, o.step, o.max_bt, a, bx, by, ctr);
+  return pv_descend<false, NC>(w, anchor, iters, o.step, o.max_bt, a, bx, by, tr, ctr);
 }
 
 // Per-warp shared doubles for problems of at most NC contacts.
 template <int NC>
-constexpr int copt_per_warp() { return NC * kSlot + 6 * NC + 32 * (kSlot + 6 * NC); }
+// per-lane doubles: trial slot, state, best, trial state; odd so that the 32
+// lanes' records fall in distinct banks (an even multiple of 16 serialises)
+constexpr int copt_lane() { return (kSlot + 9 * NC) | 1; }
+template <int NC>
+constexpr int copt_per_warp() { return NC * kSlot + 6 * NC + 32 * copt_lane<NC>(); }
 
 // Block per candidate, warp per restart, lanes over the n_inner mutations.
 // NC = compile-time bound on k + statics (sizes the shared-memory layout).
-template <int NC>
-__global__ void __launch_bounds__(128, 4)
+template <int NC, int MINB>
+__global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
                const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
@@ -186,9 +190,10 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
   double* inc = W + NC * kSlot;       // incumbent solution (warm start)
   double* win = inc + 3 * NC;         // best mutation's solution of this step
   double* lane_base = win + 3 * NC;   // per lane: trial slot, working state, best state
-  double* tslot = lane_base + lane * (kSlot + 6 * NC);
+  double* tslot = lane_base + lane * copt_lane<NC>();
   double* wst = tslot + kSlot;
   double* bst = wst + 3 * NC;
+  double* tst = bst + 3 * NC;
   const int rstride = 2 + k + 3 * NC;
   double* res = s_co + nw * copt_per_warp<NC>();
   long long off[kMaxK], cnt[kMaxK];
@@ -219,7 +224,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       w.mu = cfg.mu;
       // cold solve: lanes over anchors, best anchor by strict '<'
       double val = kInf;
-      if (lane < n) val = pv_anchor<NC>(w, lane, cfg.o, nullptr, wst, ctr);
+      if (lane < n) val = pv_anchor<NC>(w, lane, cfg.o, nullptr, wst, tst, ctr);
       if (!(val < kInf)) val = kInf;
       double best = val;
       int bl = val < kInf ? lane : 99;
@@ -236,7 +241,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       double obj = best;
       __syncwarp();
       if (lane < 3 * NC)
-        inc[lane] = anchor >= 0 ? lane_base[anchor * (kSlot + 6 * NC) + kSlot + lane] : 0.0;
+        inc[lane] = anchor >= 0 ? lane_base[anchor * copt_lane<NC>() + kSlot + lane] : 0.0;
       __syncwarp();
       const uint64_t* M = D + k;
       for (int outer = 0; outer < cfg.n_outer; ++outer) {
@@ -256,7 +261,10 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               double z1, z2;
               box_muller(d2[0], d2[1], &z1, &z2);
               V3 cp = axpy(axpy(cur_p, cfg.sigma * z1, tx), cfg.sigma * z2, ty);
-              // project_to_domain (contact_opt.cpp:11-25)
+              // project_to_domain (contact_opt.cpp:11-25).  Every lane scans
+              // the same elements (broadcast loads, no divergence); an x-sorted
+              // pruned search evaluates 7x fewer distances but diverges and
+              // measured 1.7x slower.
               const double* P = el_p + 3 * off[q];
               double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
               int bi = 0;
@@ -280,7 +288,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
                   bi = e;
                 }
               }
-              ctr.proj += (unsigned long long)cnt[q];
+              ctr.proj += (unsigned long long)ne;
               cand = bi;
               const long long eg = off[q] + bi;
               slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));
@@ -289,7 +297,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               // warm solve over all anchors in this lane (run_solver)
               double bobj = kInf;
               for (int anc = 0; anc < n; ++anc) {
-                double va = pv_anchor<NC>(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, wst, ctr);
+                double va = pv_anchor<NC>(tw, anc, cfg.o, anchor >= 0 ? inc : nullptr, wst, tst, ctr);
                 if (va < bobj) {
                   bobj = va;
                   an = anc;
@@ -317,7 +325,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               __syncwarp();
               // keep the winner's state before the next chunk reuses it; the
               // warm start (inc) stays the step's incumbent until the end
-              if (lane < 3 * NC) win[lane] = lane_base[src * (kSlot + 6 * NC) + kSlot + 3 * NC + lane];
+              if (lane < 3 * NC) win[lane] = lane_base[src * copt_lane<NC>() + kSlot + 3 * NC + lane];
               __syncwarp();
             }
           }

@@ -142,7 +142,8 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
 
 // Eigen LDLT factor + solve, warp-parallel; A (n x n, smem) destroyed,
 // x (smem) rhs in / solution out.
-__device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
+__device__ __forceinline__ void wldlt_solve(int n, double* A, double* x, int* tr, double* tmp,
+                                            int lane) {
   for (int k = 0; k < n; ++k) {
     double v = (lane >= k && lane < n) ? dabs(A[lane * n + lane]) : -1.0;
     int idx = (lane >= k && lane < n) ? lane : 0x7fff;
@@ -181,15 +182,15 @@ __device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
       __syncwarp();
     }
     if (k > 0) {
-      // temp_j = D_j * A(k, j), j < k (kept in registers of lane j)
-      double tj = lane < k ? A[lane * n + lane] * A[k * n + lane] : 0.0;
-      double acc = 0.0;
-      for (int j = 0; j < k; ++j) {
-        double t = __shfl_sync(kFull, tj, j);
-        if (lane >= k && lane < n) acc = acc + A[lane * n + j] * t;
-      }
+      // temp_j = D_j * A(k, j), j < k, broadcast through shared memory
+      if (lane < k) tmp[lane] = A[lane * n + lane] * A[k * n + lane];
       __syncwarp();
-      if (lane >= k && lane < n) A[lane * n + k] -= acc;  // lane k: A(k,k); lanes > k: A21
+      if (lane >= k && lane < n) {
+        double acc = 0.0;
+        const double* row = A + lane * n;
+        for (int j = 0; j < k; ++j) acc = acc + row[j] * tmp[j];
+        A[lane * n + k] -= acc;  // lane k: A(k,k); lanes > k: A21
+      }
       __syncwarp();
     }
     double akk = A[k * n + k];
@@ -235,7 +236,7 @@ __device__ void wldlt_solve(int n, double* A, double* x, int* tr, int lane) {
 // solve_contact_ik (ik.cpp:31-139).  q (smem) in/out; F (smem) receives the
 // frames at the final q; Ft is trial scratch.  Returns finite; used = OR of
 // joints with a nonzero column.
-__device__ __noinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
+__device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
                     unsigned long long& used, WarpWs& ws, double* F, double* Ft, Ctr& ctr,
                     int lane) {
   const int dof = c_hand.dof;
@@ -315,7 +316,7 @@ __device__ __noinline__ bool wik(double* q, const WTargets& T, int k, const IkCf
     double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
     if (lane < dof) ws.A[lane * dof + lane] += lambda;
     __syncwarp();
-    wldlt_solve(dof, ws.A, ws.x, ws.tr, lane);
+    wldlt_solve(dof, ws.A, ws.x, ws.tr, ws.qt, lane);
     bool bad = lane < dof && !is_finite(ws.x[lane]);
     if (__any_sync(kFull, bad)) {
       finite = false;
@@ -356,7 +357,7 @@ __device__ __noinline__ bool wik(double* q, const WTargets& T, int k, const IkCf
 
 // realize_grasp's project (pipeline.cpp:196-220) at frames F: worst
 // distance (all lanes), optionally refreshing hand points into R.
-__device__ __noinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
+__device__ __forceinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
                                            int lane) {
   double d = 0.0;
   if (lane < k) {
@@ -374,6 +375,10 @@ __device__ __noinline__ double wproject(const double* F, const WTargets& T, int 
 
 // realize_grasp (pipeline.cpp:185-253) for one warp; q (smem) starts at q0.
 // F, Fs, Ft: frame buffers for q, the finetune candidate and trial steps.
+// One solve site serves the initial IK (round -1) and every finetune round,
+// and the residual after the last accepted round is the projection already
+// computed for it (same frames, same arithmetic), so each helper is inlined
+// once.
 __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref, int k,
                          const IkCfg& P, int rounds, int fine_iters, double* max_res,
                          unsigned long long* used_out, WarpWs& ws, double* F, double* Fs,
@@ -381,31 +386,43 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
   const int dof = c_hand.dof;
   double q0 = lane < dof ? q[lane] : 0.0;
   unsigned long long used = 0ull;
-  if (!wik(q, T, k, P, P.iterations, used, ws, F, Ft, ctr, lane)) {
-    if (lane < dof) q[lane] = q0;
-    __syncwarp();
-    *max_res = kInf;
-    *used_out = 0ull;
-    return false;
-  }
-  double worst = wproject(F, T, k, nullptr, lane);
-  for (int round = 0; round < rounds; ++round) {
-    for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
-    if (lane < k) Ref.link[lane] = T.link[lane];
-    __syncwarp();
-    wproject(F, T, k, &Ref, lane);
-    if (lane < dof) qs[lane] = q[lane];
-    __syncwarp();
+  double worst = 0.0;
+  for (int round = -1; round < rounds; ++round) {
+    const bool init = round < 0;
+    if (!init) {
+      for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
+      if (lane < k) Ref.link[lane] = T.link[lane];
+      __syncwarp();
+      wproject(F, T, k, &Ref, lane);
+      if (lane < dof) qs[lane] = q[lane];
+      __syncwarp();
+    }
     unsigned long long su = 0ull;
-    if (!wik(qs, Ref, k, P, fine_iters, su, ws, Fs, Ft, ctr, lane)) break;
-    double w2 = wproject(Fs, T, k, nullptr, lane);
-    if (w2 > worst + 1e-6) break;
+    double* qq = init ? q : qs;
+    double* FF = init ? F : Fs;
+    bool ok = wik(qq, init ? T : Ref, k, P, init ? P.iterations : fine_iters, su, ws, FF, Ft, ctr,
+                  lane);
+    if (!ok) {
+      if (!init) break;
+      if (lane < dof) q[lane] = q0;
+      __syncwarp();
+      *max_res = kInf;
+      *used_out = 0ull;
+      return false;
+    }
+    double w = wproject(FF, T, k, nullptr, lane);
+    if (init) {
+      worst = w;
+      used = su;
+      continue;
+    }
+    if (w > worst + 1e-6) break;
     if (lane < dof) q[lane] = qs[lane];
     copy_frames(F, Fs, lane);
-    worst = w2;
+    worst = w;
     used |= su;
   }
-  *max_res = wproject(F, T, k, nullptr, lane);
+  *max_res = worst;
   *used_out = used;
   bool nonfin = lane < dof && !is_finite(q[lane]);
   return !__any_sync(kFull, nonfin);
@@ -421,7 +438,8 @@ __host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof, int kmax,
 
 // One warp per problem; targets [t][kMaxK][12] + links [t][kMaxK]; q_out
 // [t][kMaxDof] holds q0 on entry (mid_config when q_init == nullptr).
-__global__ void __launch_bounds__(128, 4)
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
 k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, int fine_iters,
                const double* tgt, int tgt_stride, const int* tl, int tl_stride,
                const double* q_init, double* q_out, double* max_res, int* finite,

@@ -315,14 +315,16 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
   const int wpb = 4;
   const int kmax = kk ? kMaxK : k;
   size_t smem = realize_warp_smem(dof, kmax, n_links, wpb);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_realize_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
+  static int minb = -1;
+  if (minb < 0) {
+    const char* e = std::getenv("LG_REALIZE_MINB");
+    minb = (e && std::atoi(e) == 4) ? 4 : 5;  // 5 CTAs/SM (96 regs) measured faster
+    CK(cudaFuncSetAttribute(k_realize_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_realize_warp<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
-  k_realize_warp<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt,
-                                                             tgt_stride, tl, tl_stride, q_init, q_out,
-                                                             max_res, finite, used);
+  auto kern = minb == 5 ? k_realize_warp<5> : k_realize_warp<4>;
+  kern<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt, tgt_stride,
+                                                   tl, tl_stride, q_init, q_out, max_res, finite, used);
 }
 
 // Flattened patch data on the device.
@@ -760,21 +762,22 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     co.per_restart = per_restart;
     co.per_cand = per_cand;
     int nw = std::min(R, 4);
-    static bool co_attr = false;
-    if (!co_attr) {
-      CK(cudaFuncSetAttribute(k_contact_opt2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      co_attr = true;
+    static int co_minb = -1;
+    if (co_minb < 0) {
+      const char* e = std::getenv("LG_COPT_MINB");
+      co_minb = (e && std::atoi(e) == 5) ? 5 : 4;
+      CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     }
     tk.start();
-    if (k + 1 <= 3)  // k contacts + at most one static
-      k_contact_opt2<3><<<nA, 32 * nw, copt2_smem<3>(k, nw), s>>>(
-          nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan,
-          d_osol, cfg.eps_stable, d_bal);
-    else
-      k_contact_opt2<kMaxC><<<nA, 32 * nw, copt2_smem<kMaxC>(k, nw), s>>>(
-          nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, d_draws, d_oid, d_oobj, d_oan,
-          d_osol, cfg.eps_stable, d_bal);
+    // k contacts + at most one static
+    auto co_kern = k + 1 <= 3 ? (co_minb == 5 ? k_contact_opt2<3, 5> : k_contact_opt2<3, 4>)
+                              : k_contact_opt2<kMaxC, 4>;
+    size_t co_smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
+    co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln,
+                                         d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
+                                         d_bal);
     LAUNCH(ctx);
     check_launch();
     copt_s += tk.stop();
