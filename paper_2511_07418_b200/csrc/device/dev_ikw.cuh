@@ -20,6 +20,9 @@
 namespace lgd {
 
 constexpr unsigned kFull = 0xffffffffu;
+// Shared-memory stride of one link frame (R row-major, t): 13 doubles, odd,
+// so lanes reading different links' frames hit distinct banks.
+constexpr int kFS = 13;
 
 __device__ __forceinline__ Xf ld_xf(const double* p) {
   Xf x;
@@ -60,13 +63,13 @@ __device__ __forceinline__ void wfk_s(const double* q, double* F, int lane) {
     p = g_hand.parent[lane];
   }
   for (int d = 0; d < c_hand.n_levels; ++d) {
-    if (lvl == d) st_xf(F + 12 * lane, p < 0 ? loc : xf_compose(ld_xf(F + 12 * p), loc));
+    if (lvl == d) st_xf(F + kFS * lane, p < 0 ? loc : xf_compose(ld_xf(F + kFS * p), loc));
     __syncwarp();
   }
 }
 
 __device__ __forceinline__ void copy_frames(double* dst, const double* src, int lane) {
-  for (int a = lane; a < 12 * c_hand.n_links; a += 32) dst[a] = src[a];
+  for (int a = lane; a < kFS * c_hand.n_links; a += 32) dst[a] = src[a];
   __syncwarp();
 }
 
@@ -87,7 +90,7 @@ __device__ __forceinline__ double warp_max_d(double v) {
 __device__ __forceinline__ double wresidual(const double* F, const WTargets& T, int k, double beta,
                                             double* r, int lane) {
   if (lane < k) {
-    Xf Fl = ld_xf(F + 12 * T.link[lane]);
+    Xf Fl = ld_xf(F + kFS * T.link[lane]);
     const double* t = T.t + 12 * lane;
     V3 op = v3_load(t), on = v3_load(t + 3);
     V3 hp = xf_apply(Fl, v3_load(t + 6));
@@ -115,7 +118,7 @@ struct WarpWs {
 };
 
 __host__ __device__ __forceinline__ size_t warp_ws_bytes(int k, int dof) {
-  size_t d = (size_t)6 * k * dof + (size_t)dof * dof + 12 * k + 2 * dof + 6 * k;
+  size_t d = (size_t)6 * k * dof + (size_t)dof * (dof | 1) + 12 * k + 2 * dof + 6 * k;
   return (d * sizeof(double) + (size_t)dof * sizeof(int) + 15) & ~(size_t)15;
 }
 
@@ -125,7 +128,7 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
   w.J = p;
   p += 6 * k * dof;
   w.A = p;
-  p += dof * dof;
+  p += dof * (dof | 1);
   w.r = p;
   p += 6 * k;
   w.rt = p;
@@ -142,10 +145,10 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
 
 // Eigen LDLT factor + solve, warp-parallel; A (n x n, smem) destroyed,
 // x (smem) rhs in / solution out.
-__device__ __forceinline__ void wldlt_solve(int n, double* A, double* x, int* tr, double* tmp,
-                                            int lane) {
+__device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, int* tr,
+                                            double* tmp, int lane) {
   for (int k = 0; k < n; ++k) {
-    double v = (lane >= k && lane < n) ? dabs(A[lane * n + lane]) : -1.0;
+    double v = (lane >= k && lane < n) ? dabs(A[lane * ld + lane]) : -1.0;
     int idx = (lane >= k && lane < n) ? lane : 0x7fff;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -160,41 +163,41 @@ __device__ __forceinline__ void wldlt_solve(int n, double* A, double* x, int* tr
     if (lane == 0) tr[k] = big;
     if (k != big) {
       if (lane < k) {
-        double t = A[k * n + lane];
-        A[k * n + lane] = A[big * n + lane];
-        A[big * n + lane] = t;
+        double t = A[k * ld + lane];
+        A[k * ld + lane] = A[big * ld + lane];
+        A[big * ld + lane] = t;
       }
       if (lane > big && lane < n) {
-        double t = A[lane * n + k];
-        A[lane * n + k] = A[lane * n + big];
-        A[lane * n + big] = t;
+        double t = A[lane * ld + k];
+        A[lane * ld + k] = A[lane * ld + big];
+        A[lane * ld + big] = t;
       }
       if (lane == 0) {
-        double t = A[k * n + k];
-        A[k * n + k] = A[big * n + big];
-        A[big * n + big] = t;
+        double t = A[k * ld + k];
+        A[k * ld + k] = A[big * ld + big];
+        A[big * ld + big] = t;
       }
       if (lane > k && lane < big) {
-        double u = A[lane * n + k];
-        A[lane * n + k] = A[big * n + lane];
-        A[big * n + lane] = u;
+        double u = A[lane * ld + k];
+        A[lane * ld + k] = A[big * ld + lane];
+        A[big * ld + lane] = u;
       }
       __syncwarp();
     }
     if (k > 0) {
       // temp_j = D_j * A(k, j), j < k, broadcast through shared memory
-      if (lane < k) tmp[lane] = A[lane * n + lane] * A[k * n + lane];
+      if (lane < k) tmp[lane] = A[lane * ld + lane] * A[k * ld + lane];
       __syncwarp();
       if (lane >= k && lane < n) {
         double acc = 0.0;
-        const double* row = A + lane * n;
+        const double* row = A + lane * ld;
         for (int j = 0; j < k; ++j) acc = acc + row[j] * tmp[j];
-        A[lane * n + k] -= acc;  // lane k: A(k,k); lanes > k: A21
+        A[lane * ld + k] -= acc;  // lane k: A(k,k); lanes > k: A21
       }
       __syncwarp();
     }
-    double akk = A[k * n + k];
-    if (dabs(akk) > 0.0 && lane > k && lane < n) A[lane * n + k] /= akk;
+    double akk = A[k * ld + k];
+    if (dabs(akk) > 0.0 && lane > k && lane < n) A[lane * ld + k] /= akk;
     __syncwarp();
   }
   if (lane == 0)
@@ -209,10 +212,10 @@ __device__ __forceinline__ void wldlt_solve(int n, double* A, double* x, int* tr
   for (int j = 0; j < n; ++j) {  // forward: L unit lower
     double xj = __shfl_sync(kFull, xi - s, j);
     if (lane == j) xi = xj;
-    if (lane > j && lane < n) s = s + A[lane * n + j] * xj;
+    if (lane > j && lane < n) s = s + A[lane * ld + j] * xj;
   }
   if (lane < n) {
-    double d = A[lane * n + lane];
+    double d = A[lane * ld + lane];
     if (dabs(d) > 2.2250738585072014e-308) xi /= d;
     else xi = 0.0;
   }
@@ -220,7 +223,7 @@ __device__ __forceinline__ void wldlt_solve(int n, double* A, double* x, int* tr
   for (int j = n - 1; j >= 0; --j) {  // backward: L^T
     double xj = __shfl_sync(kFull, xi - s, j);
     if (lane == j) xi = xj;
-    if (lane < j) s = s + A[j * n + lane] * xj;
+    if (lane < j) s = s + A[j * ld + lane] * xj;
   }
   if (lane < n) x[lane] = xi;
   __syncwarp();
@@ -240,6 +243,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
                     unsigned long long& used, WarpWs& ws, double* F, double* Ft, Ctr& ctr,
                     int lane) {
   const int dof = c_hand.dof;
+  const int ld = dof | 1;  // odd row stride: column accesses hit distinct banks
   const int rows = 6 * k;
   if (lane < dof) q[lane] = dclamp(q[lane], g_hand.jlo[lane], g_hand.jhi[lane]);
   __syncwarp();
@@ -256,7 +260,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     // Jacobian points: lane p < 2k -> target p/2, half p%2
     if (lane < 2 * k) {
       int i = lane >> 1;
-      Xf Fl = ld_xf(F + 12 * T.link[i]);
+      Xf Fl = ld_xf(F + kFS * T.link[i]);
       const double* t = T.t + 12 * i;
       V3 lp = (lane & 1) ? axpy(v3_load(t + 6), P.beta, v3_load(t + 9)) : v3_load(t + 6);
       v3_store(ws.pts + 3 * lane, xf_apply(Fl, lp));
@@ -265,7 +269,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     // joint columns
     if (lane < dof) {
       int lj = g_hand.jlink[lane];
-      Xf Fj = ld_xf(F + 12 * lj);
+      Xf Fj = ld_xf(F + kFS * lj);
       V3 axis = mul(Fj.R, v3_load(g_hand.axis[lj]));
       bool rev = g_hand.jtype[lj] == 1;
       double cm = 0.0;
@@ -300,8 +304,8 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       int b = a + rem;
       double s = 0.0;
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
-      ws.A[a * dof + b] = s;
-      ws.A[b * dof + a] = s;
+      ws.A[a * ld + b] = s;
+      ws.A[b * ld + a] = s;
     }
     if (lane < dof) {
       double s = 0.0;
@@ -311,12 +315,12 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     __syncwarp();
     double tr = 0.0;
     if (lane == 0)
-      for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * dof + a];
+      for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * ld + a];
     tr = __shfl_sync(kFull, tr, 0);
     double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
-    if (lane < dof) ws.A[lane * dof + lane] += lambda;
+    if (lane < dof) ws.A[lane * ld + lane] += lambda;
     __syncwarp();
-    wldlt_solve(dof, ws.A, ws.x, ws.tr, ws.qt, lane);
+    wldlt_solve(dof, ld, ws.A, ws.x, ws.tr, ws.qt, lane);
     bool bad = lane < dof && !is_finite(ws.x[lane]);
     if (__any_sync(kFull, bad)) {
       finite = false;
@@ -361,7 +365,7 @@ __device__ __forceinline__ double wproject(const double* F, const WTargets& T, i
                                            int lane) {
   double d = 0.0;
   if (lane < k) {
-    Xf inv = xf_inverse(ld_xf(F + 12 * T.link[lane]));
+    Xf inv = xf_inverse(ld_xf(F + kFS * T.link[lane]));
     V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
     d = closest_on_parts(T.link[lane], xf_apply(inv, v3_load(T.t + 12 * lane)), &sp, &sn);
     if (R) {
@@ -431,7 +435,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
 // Per-warp shared bytes: workspace + targets, refreshed targets, q, qs,
 // three frame buffers, links (16-byte aligned).
 __host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof, int kmax, int nl) {
-  size_t b = warp_ws_bytes(kmax, dof) + (size_t)(24 * kmax + 2 * dof + 3 * 12 * nl) * sizeof(double) +
+  size_t b = warp_ws_bytes(kmax, dof) + (size_t)(24 * kmax + 2 * dof + 3 * kFS * nl) * sizeof(double) +
              2 * kmax * sizeof(int);
   return (b + 15) & ~(size_t)15;
 }
@@ -460,9 +464,9 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   double* q = extra + 24 * kmax;
   double* qs = q + dof;
   double* F = qs + dof;
-  double* Fs = F + 12 * nl;
-  double* Ft = Fs + 12 * nl;
-  T.link = (int*)(Ft + 12 * nl);
+  double* Fs = F + kFS * nl;
+  double* Ft = Fs + kFS * nl;
+  T.link = (int*)(Ft + kFS * nl);
   Ref.link = T.link + kmax;
   const double* src = tgt + (size_t)t * tgt_stride;
   for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];

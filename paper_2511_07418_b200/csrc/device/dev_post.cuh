@@ -23,7 +23,7 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
                              const double* q_all, const double* pose, const double* obj_aabb,
                              int clean_only, uint8_t* clean_out, double* maxpen_out) {
   __shared__ double s_q[kMaxDof];
-  __shared__ double s_fr[kMaxLinks * 12];
+  __shared__ double s_fr[kMaxLinks * kFS];
   __shared__ double s_box[64 * 6];
   __shared__ int s_obj[64];
   __shared__ int s_nobj;
@@ -45,7 +45,7 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
   __syncthreads();
   for (int p = tid; p < np; p += blockDim.x) {
     V3 mn, mx;
-    world_bounds(p, ld_xf(s_fr + 12 * C.part_link[p]), &mn, &mx);
+    world_bounds(p, ld_xf(s_fr + kFS * C.part_link[p]), &mn, &mx);
     s_box[6 * p + 0] = mn.x - C.margin;
     s_box[6 * p + 1] = mn.y - C.margin;
     s_box[6 * p + 2] = mn.z - C.margin;
@@ -72,7 +72,7 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
     int la = C.part_link[pa], lb = C.part_link[pb];
     if (la == lb || g_hand.parent[la] == lb || g_hand.parent[lb] == la) continue;
     if (clean_only && *(volatile int*)&s_viol) continue;
-    if (gjk_distance(pa, ld_xf(s_fr + 12 * la), pb, ld_xf(s_fr + 12 * lb)) == 0.0)
+    if (gjk_distance(pa, ld_xf(s_fr + kFS * la), pb, ld_xf(s_fr + kFS * lb)) == 0.0)
       atomicOr(&s_viol, 1);
   }
   __syncthreads();
@@ -83,7 +83,7 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
     const int nobj = s_nobj;
     for (int o = 0; o < nobj; ++o) {
       int pa = s_obj[o];
-      Xf inv = xf_inverse(ld_xf(s_fr + 12 * C.part_link[pa]));
+      Xf inv = xf_inverse(ld_xf(s_fr + kFS * C.part_link[pa]));
       const double* b = c_hand.bounds + 6 * pa;
       double mx = 0.0;
       bool off = false;
@@ -274,7 +274,7 @@ __global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, Fi
                                 const double* best_tgt, const int* best_link, lg_grasp* out,
                                 int* valid, int* dropped) {
   __shared__ double s_q[4][kMaxDof];
-  __shared__ double s_F[4][12 * kMaxLinks];
+  __shared__ double s_F[4][kFS * kMaxLinks];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t = blockIdx.x * (blockDim.x >> 5) + w;
   if (t >= nT) return;
@@ -290,7 +290,7 @@ __global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, Fi
   double d = 0.0;
   V3 pw = v3(0, 0, 0);
   if (lane < k) {
-    Xf F = ld_xf(s_F[w] + 12 * link);
+    Xf F = ld_xf(s_F[w] + kFS * link);
     const double* T = best_tgt + (size_t)a * kMaxK * 12 + 12 * lane;
     Xf inv = xf_inverse(F);
     V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
