@@ -35,21 +35,25 @@ __device__ __forceinline__ void st_xf(double* p, const Xf& x) {
   v3_store(p + 9, x.t);
 }
 
-// Pre-motion origin composed with the joint motion at q (hand.cpp:281-290).
-__device__ __forceinline__ Xf link_local(int l, const double* q) {
+// Pre-motion origin composed with the joint motion qv (hand.cpp:281-290).
+__device__ __forceinline__ Xf link_local_v(int l, double qv) {
   Xf local;
   local.R = m3_load(g_hand.R[l]);
   local.t = v3_load(g_hand.t[l]);
   int jt = g_hand.jtype[l];
   if (jt == 1) {
     Xf m;
-    m.R = angle_axis(q[g_hand.jidx[l]], v3_load(g_hand.axis[l]));
+    m.R = angle_axis(qv, v3_load(g_hand.axis[l]));
     m.t = v3(0.0, 0.0, 0.0);
     local = xf_compose(local, m);
   } else if (jt == 2) {
-    local.t = add(local.t, mul(local.R, scale(q[g_hand.jidx[l]], v3_load(g_hand.axis[l]))));
+    local.t = add(local.t, mul(local.R, scale(qv, v3_load(g_hand.axis[l]))));
   }
   return local;
+}
+__device__ __forceinline__ Xf link_local(int l, const double* q) {
+  int j = g_hand.jidx[l];
+  return link_local_v(l, j >= 0 ? q[j] : 0.0);
 }
 
 // forward_kinematics into shared memory F[n_links][12], q in shared memory.
@@ -68,16 +72,99 @@ __device__ __forceinline__ void wfk_s(const double* q, double* F, int lane) {
   }
 }
 
-__device__ __forceinline__ void copy_frames(double* dst, const double* src, int lane) {
-  for (int a = lane; a < kFS * c_hand.n_links; a += 32) dst[a] = src[a];
-  __syncwarp();
-}
-
 // Target layout in shared memory: [k][12] = op(3) on(3) hp(3) hn(3); links [k].
 struct WTargets {
   double* t;
   int* link;
 };
+
+// The links the contact IK can see: the union of the root -> target-link
+// chains.  The residual reads target-link frames and every nonzero Jacobian
+// column belongs to a joint on a target chain, so solve_contact_ik never
+// needs any other frame; FK is evaluated on these m links only, in G = 32/m
+// lane groups (up to 4), one backtracking trial per group.
+struct WChain {
+  int m, G, maxlvl;
+  int *link, *pslot, *lvl, *sol, *tslot, *hdr;
+};
+constexpr int kChainInts = 4 * kMaxLinks + kMaxK + 2;
+
+__device__ __forceinline__ void wchain_build(WChain& C, const int* tlink, int k, int lane) {
+  if (lane == 0) {
+    const int nl = c_hand.n_links;
+    int m = 0, maxl = 0;
+    for (int l = 0; l < nl; ++l) {
+      bool need = false;
+      for (int i = 0; i < k; ++i) {
+        int t = tlink[i];
+        for (int d = 0; d < g_hand.chain_len[t]; ++d) need |= g_hand.chain[t][d] == l;
+      }
+      C.sol[l] = need ? m : -1;
+      if (need) {
+        C.link[m] = l;
+        C.lvl[m] = g_hand.level[l];
+        maxl = C.lvl[m] > maxl ? C.lvl[m] : maxl;
+        ++m;
+      }
+    }
+    for (int j = 0; j < m; ++j) {
+      int p = g_hand.parent[C.link[j]];
+      C.pslot[j] = p >= 0 ? C.sol[p] : -1;
+    }
+    for (int i = 0; i < k; ++i) C.tslot[i] = C.sol[tlink[i]];
+    C.hdr[0] = m;
+    C.hdr[1] = maxl;
+  }
+  __syncwarp();
+  C.m = C.hdr[0];
+  C.maxlvl = C.hdr[1];
+  int g = C.m > 0 ? 32 / C.m : 1;
+  C.G = g > 4 ? 4 : g;
+}
+
+// Joint value of backtracking trial b: q + clamp(dq / 2^b) clamped to the
+// limits, dq halved b times as the sequential line search does.
+__device__ __forceinline__ double trial_joint(const double* q, const double* dq, int j, int b,
+                                              double step_clamp) {
+  double d = dq[j];
+  for (int h = 0; h < b; ++h) d *= 0.5;
+  return dclamp(q[j] + dmin(dmax(d, -step_clamp), step_clamp), g_hand.jlo[j], g_hand.jhi[j]);
+}
+
+// FK of the chain links for ng groups into FG[g][m][kFS]; group g uses trial
+// b0 + g, or q itself when b0 < 0 (one group).
+__device__ __forceinline__ void wchain_fk(const WChain& C, double* FG, int ng, const double* q,
+                                         const double* dq, int b0, double step_clamp, int lane) {
+  const bool on = lane < ng * C.m;
+  const int g = on ? lane / C.m : 0, j = on ? lane - g * C.m : 0;
+  Xf loc = xf_identity();
+  int lv = -1, ps = -1;
+  if (on) {
+    int l = C.link[j];
+    int jl = g_hand.jidx[l];
+    double qv = 0.0;
+    if (jl >= 0) qv = b0 < 0 ? q[jl] : trial_joint(q, dq, jl, b0 + g, step_clamp);
+    loc = link_local_v(l, qv);
+    lv = C.lvl[j];
+    ps = C.pslot[j];
+  }
+  double* Fg = FG + (size_t)g * C.m * kFS;
+  for (int d = 0; d <= C.maxlvl; ++d) {
+    if (lv == d) st_xf(Fg + kFS * j, ps < 0 ? loc : xf_compose(ld_xf(Fg + kFS * ps), loc));
+    __syncwarp();
+  }
+}
+
+// Chain frames of group g -> link-indexed frames F.
+__device__ __forceinline__ void wchain_commit(const WChain& C, const double* FG, int g, double* F,
+                                             int lane) {
+  if (lane < C.m) {
+    const double* src = FG + ((size_t)g * C.m + lane) * kFS;
+    double* dst = F + kFS * C.link[lane];
+    for (int a = 0; a < 12; ++a) dst[a] = src[a];
+  }
+  __syncwarp();
+}
 
 __device__ __forceinline__ double warp_max_d(double v) {
 #pragma unroll
@@ -148,18 +235,32 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
 __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, int* tr,
                                             double* tmp, int lane) {
   for (int k = 0; k < n; ++k) {
-    double v = (lane >= k && lane < n) ? dabs(A[lane * ld + lane]) : -1.0;
-    int idx = (lane >= k && lane < n) ? lane : 0x7fff;
+    // pivot = first index of max |A(i,i)|, i >= k.  Non-negative doubles
+    // order like their bit patterns, so the max is two 32-bit warp
+    // reductions (high word, then low word among the ties) and the first
+    // lane holding it; a NaN diagonal takes the comparison-based reduction.
+    const bool act = lane >= k && lane < n;
+    double v = act ? dabs(A[lane * ld + lane]) : -1.0;
+    int big;
+    if (!__any_sync(kFull, act && v != v)) {
+      unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+      unsigned hi = __reduce_max_sync(kFull, act ? (unsigned)(bits >> 32) : 0u);
+      bool tie = act && (unsigned)(bits >> 32) == hi;
+      unsigned lo = __reduce_max_sync(kFull, tie ? (unsigned)bits : 0u);
+      big = __ffs(__ballot_sync(kFull, tie && (unsigned)bits == lo)) - 1;
+    } else {
+      int idx = act ? lane : 0x7fff;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_xor_sync(kFull, v, o);
-      int oi = __shfl_xor_sync(kFull, idx, o);
-      if (ov > v || (ov == v && oi < idx)) {
-        v = ov;
-        idx = oi;
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(kFull, v, o);
+        int oi = __shfl_xor_sync(kFull, idx, o);
+        if (ov > v || (ov == v && oi < idx)) {
+          v = ov;
+          idx = oi;
+        }
       }
+      big = idx;
     }
-    const int big = idx;
     if (lane == 0) tr[k] = big;
     if (k != big) {
       if (lane < k) {
@@ -240,20 +341,20 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
 // frames at the final q; Ft is trial scratch.  Returns finite; used = OR of
 // joints with a nonzero column.
 __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
-                    unsigned long long& used, WarpWs& ws, double* F, double* Ft, Ctr& ctr,
-                    int lane) {
+                    unsigned long long& used, WarpWs& ws, double* F, const WChain& C, double* FG,
+                    double* rtG, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   const int ld = dof | 1;  // odd row stride: column accesses hit distinct banks
   const int rows = 6 * k;
   if (lane < dof) q[lane] = dclamp(q[lane], g_hand.jlo[lane], g_hand.jhi[lane]);
   __syncwarp();
   used = 0ull;
-  wfk_s(q, F, lane);
+  wchain_fk(C, FG, 1, q, nullptr, -1, 0.0, lane);
+  wchain_commit(C, FG, 0, F, lane);
   ++ctr.fk;
   if (k == 0) return true;
   bool finite = true;
   double* r = ws.r;
-  double* rt = ws.rt;
   double objective = wresidual(F, T, k, P.beta, r, lane);
   for (int it = 0; it < iterations; ++it) {
     ++ctr.ik_it;
@@ -326,27 +427,44 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       finite = false;
       break;
     }
+    // backtracking line search, G trials at a time; the first trial (in
+    // order) with obj <= objective is the one the sequential search keeps
     bool moved = false;
-    double dq = lane < dof ? ws.x[lane] : 0.0;
-    for (int bt = 0; bt <= P.max_backtracks; ++bt) {
-      if (lane < dof)
-        ws.qt[lane] = dclamp(q[lane] + dmin(dmax(dq, -P.step_clamp), P.step_clamp), g_hand.jlo[lane],
-                             g_hand.jhi[lane]);
-      __syncwarp();
-      wfk_s(ws.qt, Ft, lane);
-      ++ctr.fk;
-      double obj_try = wresidual(Ft, T, k, P.beta, rt, lane);
-      if (obj_try <= objective) {
-        if (lane < dof) q[lane] = ws.qt[lane];
-        copy_frames(F, Ft, lane);
-        double* sw = r;
-        r = rt;
-        rt = sw;
-        objective = obj_try;
-        moved = true;
-        break;
+    const int rk = 6 * k;
+    for (int b0 = 0; b0 <= P.max_backtracks && !moved; b0 += C.G) {
+      const int ng = (P.max_backtracks + 1 - b0) < C.G ? (P.max_backtracks + 1 - b0) : C.G;
+      wchain_fk(C, FG, ng, q, ws.x, b0, P.step_clamp, lane);
+      ctr.fk += ng;
+      if (lane < ng * k) {  // stacked_residual (ik.cpp:13-27) per group
+        int g = lane / k, i = lane - g * k;
+        Xf Fl = ld_xf(FG + ((size_t)g * C.m + C.tslot[i]) * kFS);
+        const double* tt = T.t + 12 * i;
+        V3 op = v3_load(tt), on = v3_load(tt + 3);
+        V3 hp = xf_apply(Fl, v3_load(tt + 6));
+        V3 hn = xf_rotate(Fl, v3_load(tt + 9));
+        V3 a = sub(op, hp);
+        V3 bb = sub(axpy(op, P.beta, on), axpy(hp, P.beta, hn));
+        double* o = rtG + g * rk + 6 * i;
+        o[0] = a.x;
+        o[1] = a.y;
+        o[2] = a.z;
+        o[3] = bb.x;
+        o[4] = bb.y;
+        o[5] = bb.z;
       }
-      dq *= 0.5;
+      __syncwarp();
+      double obj_try = 0.0;
+      if (lane < ng)
+        for (int i = 0; i < rk; ++i) obj_try = obj_try + rtG[lane * rk + i] * rtG[lane * rk + i];
+      unsigned accm = __ballot_sync(kFull, lane < ng && obj_try <= objective);
+      if (accm) {
+        const int g = __ffs(accm) - 1;
+        objective = __shfl_sync(kFull, obj_try, g);
+        if (lane < dof) q[lane] = trial_joint(q, ws.x, lane, b0 + g, P.step_clamp);
+        if (lane < rk) r[lane] = rtG[g * rk + lane];
+        wchain_commit(C, FG, g, F, lane);
+        moved = true;
+      }
     }
     if (!moved) break;
     double mp = 0.0;
@@ -361,7 +479,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
 
 // realize_grasp's project (pipeline.cpp:196-220) at frames F: worst
 // distance (all lanes), optionally refreshing hand points into R.
-__device__ __forceinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
+__device__ __noinline__ double wproject(const double* F, const WTargets& T, int k, WTargets* R,
                                            int lane) {
   double d = 0.0;
   if (lane < k) {
@@ -378,15 +496,16 @@ __device__ __forceinline__ double wproject(const double* F, const WTargets& T, i
 }
 
 // realize_grasp (pipeline.cpp:185-253) for one warp; q (smem) starts at q0.
-// F, Fs, Ft: frame buffers for q, the finetune candidate and trial steps.
 // One solve site serves the initial IK (round -1) and every finetune round,
 // and the residual after the last accepted round is the projection already
-// computed for it (same frames, same arithmetic), so each helper is inlined
-// once.
+// computed for it (same frames, same arithmetic).  One link-indexed frame
+// buffer suffices: a finetune solve starts from frames(q) (held in Fa since
+// the last accepted solve) and leaves frames(qs) there; a rejected round ends
+// the loop.  Only the target chains' frames are ever valid (see WChain).
 __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref, int k,
                          const IkCfg& P, int rounds, int fine_iters, double* max_res,
-                         unsigned long long* used_out, WarpWs& ws, double* F, double* Fs,
-                         double* Ft, Ctr& ctr, int lane) {
+                         unsigned long long* used_out, WarpWs& ws, double* Fa, const WChain& C,
+                         double* FG, double* rtG, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   double q0 = lane < dof ? q[lane] : 0.0;
   unsigned long long used = 0ull;
@@ -397,15 +516,14 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
       for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
       if (lane < k) Ref.link[lane] = T.link[lane];
       __syncwarp();
-      wproject(F, T, k, &Ref, lane);
+      wproject(Fa, T, k, &Ref, lane);
       if (lane < dof) qs[lane] = q[lane];
       __syncwarp();
     }
     unsigned long long su = 0ull;
     double* qq = init ? q : qs;
-    double* FF = init ? F : Fs;
-    bool ok = wik(qq, init ? T : Ref, k, P, init ? P.iterations : fine_iters, su, ws, FF, Ft, ctr,
-                  lane);
+    bool ok = wik(qq, init ? T : Ref, k, P, init ? P.iterations : fine_iters, su, ws, Fa, C, FG, rtG,
+                  ctr, lane);
     if (!ok) {
       if (!init) break;
       if (lane < dof) q[lane] = q0;
@@ -414,7 +532,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
       *used_out = 0ull;
       return false;
     }
-    double w = wproject(FF, T, k, nullptr, lane);
+    double w = wproject(Fa, T, k, nullptr, lane);
     if (init) {
       worst = w;
       used = su;
@@ -422,7 +540,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
     }
     if (w > worst + 1e-6) break;
     if (lane < dof) q[lane] = qs[lane];
-    copy_frames(F, Fs, lane);
+    __syncwarp();
     worst = w;
     used |= su;
   }
@@ -433,10 +551,12 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
 }
 
 // Per-warp shared bytes: workspace + targets, refreshed targets, q, qs,
-// three frame buffers, links (16-byte aligned).
+// link frames, chain trial frames [32][kFS], trial residuals [4][6k], links,
+// chain tables (16-byte aligned).
 __host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof, int kmax, int nl) {
-  size_t b = warp_ws_bytes(kmax, dof) + (size_t)(24 * kmax + 2 * dof + 3 * kFS * nl) * sizeof(double) +
-             2 * kmax * sizeof(int);
+  size_t b = warp_ws_bytes(kmax, dof) +
+             (size_t)(24 * kmax + 2 * dof + kFS * nl + 32 * kFS + 24 * kmax) * sizeof(double) +
+             (2 * kmax + kChainInts) * sizeof(int);
   return (b + 15) & ~(size_t)15;
 }
 
@@ -464,19 +584,27 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   double* q = extra + 24 * kmax;
   double* qs = q + dof;
   double* F = qs + dof;
-  double* Fs = F + kFS * nl;
-  double* Ft = Fs + kFS * nl;
-  T.link = (int*)(Ft + kFS * nl);
+  double* FG = F + kFS * nl;
+  double* rtG = FG + 32 * kFS;
+  T.link = (int*)(rtG + 24 * kmax);
   Ref.link = T.link + kmax;
+  WChain C;
+  C.link = Ref.link + kmax;
+  C.pslot = C.link + kMaxLinks;
+  C.lvl = C.pslot + kMaxLinks;
+  C.sol = C.lvl + kMaxLinks;
+  C.tslot = C.sol + kMaxLinks;
+  C.hdr = C.tslot + kMaxK;
   const double* src = tgt + (size_t)t * tgt_stride;
   for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
   if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
   if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
   __syncwarp();
+  wchain_build(C, T.link, kt, lane);
   Ctr ctr = {0, 0, 0, 0, 0};
   double mr;
   unsigned long long u;
-  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, Fs, Ft, ctr, lane);
+  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, ctr, lane);
   if (lane == 0) ctr_flush(ctr);
   if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
   if (lane == 0) {

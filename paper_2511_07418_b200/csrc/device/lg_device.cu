@@ -318,11 +318,13 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
   static int minb = -1;
   if (minb < 0) {
     const char* e = std::getenv("LG_REALIZE_MINB");
-    minb = (e && std::atoi(e) == 4) ? 4 : 5;  // 5 CTAs/SM (96 regs) measured faster
+    minb = e ? std::atoi(e) : 5;  // 5 CTAs/SM (96 regs) measured fastest
+    if (minb != 4 && minb != 6) minb = 5;
     CK(cudaFuncSetAttribute(k_realize_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_realize_warp<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_realize_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
-  auto kern = minb == 5 ? k_realize_warp<5> : k_realize_warp<4>;
+  auto kern = minb == 6 ? k_realize_warp<6> : (minb == 5 ? k_realize_warp<5> : k_realize_warp<4>);
   kern<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt, tgt_stride,
                                                    tl, tl_stride, q_init, q_out, max_res, finite, used);
 }

@@ -1,7 +1,9 @@
-# parity + A/B of the realize launch bound + launch list
+# parity + A/B of a launch-bound env knob ($AB_VAR over $AB_VALS) + launch list
+AB_VAR=${AB_VAR:-LG_REALIZE_MINB}; AB_VALS=${AB_VALS:-"5 6"}
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
-for mb in 4 5; do export LG_COPT_MINB=$mb
-  python bench.py --no-cpu --steps 5 --warmup 3 > gpurun_out/bench_mb$mb.log 2>&1; echo "mb=$mb rc=$?"
-  tail -1 gpurun_out/bench_mb$mb.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["stage_seconds"], d["work"])'
+for v in $AB_VALS; do export $AB_VAR=$v
+  python bench.py --no-cpu --steps 5 --warmup 3 > gpurun_out/bench_ab$v.log 2>&1; echo "$AB_VAR=$v rc=$?"
+  tail -1 gpurun_out/bench_ab$v.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["stage_seconds"])'
 done
+unset $AB_VAR
 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/launches.csv python bench.py --no-cpu --no-clocks --steps 1 --warmup 3 > gpurun_out/ncu_l.log 2>&1; python tools/launch_summary.py gpurun_out/launches.csv > gpurun_out/launch_summary.txt; head -6 gpurun_out/launch_summary.txt
