@@ -31,6 +31,14 @@ WORKLOADS = {
                         cfg="configs/allegro.cfg"),
     "allegro_cylinder": dict(hand="hands/allegro_like.urdf", obj="objects/cylinder_r025_l100.obj",
                              cfg="configs/allegro.cfg"),
+    # configs[2]: LEAP-class hand on tool-like primitive unions (100k seeds, 8 GPUs)
+    "leap_mug": dict(hand="hands/leap_like.urdf", obj="objects/mug.obj", cfg="configs/leap.cfg"),
+    "leap_hammer": dict(hand="hands/leap_like.urdf", obj="objects/hammer.obj",
+                        cfg="configs/leap.cfg"),
+    "leap_drill": dict(hand="hands/leap_like.urdf", obj="objects/drill.obj", cfg="configs/leap.cfg"),
+    # configs[3]: Shadow-class 22-DoF hand, high-poly object (~113k samples)
+    "shadow_icosphere": dict(hand="hands/shadow_like.urdf", obj="objects/icosphere_r030_s6.obj",
+                             cfg="configs/shadow.cfg"),
     # configs[0]: the reference's bundled CPU-runnable case
     "four_finger_sphere": dict(hand="hands/four_finger.urdf", obj="objects/sphere_r030.obj",
                                cfg="configs/four_finger.cfg"),

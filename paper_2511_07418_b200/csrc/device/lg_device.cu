@@ -771,6 +771,14 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      // shared-memory carve-out (percent): less shared memory leaves more L1
+      // for the domain scans, at the cost of resident CTAs
+      const char* cv = std::getenv("LG_COPT_CARVE");
+      if (cv) {
+        int pct = std::atoi(cv);
+        CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      }
     }
     tk.start();
     // k contacts + at most one static
