@@ -175,7 +175,7 @@ template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
-               const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
+               const double* el_xs, const int* el_ix, int sorted_min, const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
                double* out_sol, double eps_stable, int* balanced) {
   extern __shared__ __align__(16) double s_co[];
   const int a = blockIdx.x;
@@ -261,34 +261,78 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               double z1, z2;
               box_muller(d2[0], d2[1], &z1, &z2);
               V3 cp = axpy(axpy(cur_p, cfg.sigma * z1, tx), cfg.sigma * z2, ty);
-              // project_to_domain (contact_opt.cpp:11-25).  Every lane scans
-              // the same elements (broadcast loads, no divergence); an x-sorted
-              // pruned search evaluates 7x fewer distances but diverges and
-              // measured 1.7x slower.
+              // project_to_domain (contact_opt.cpp:11-25): nearest element,
+              // first index among equal distances.
               const double* P = el_p + 3 * off[q];
-              double bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
-              int bi = 0;
               const int ne = (int)cnt[q];
-              int e = 1;
-              // four independent distances in flight, compared in index order
-              for (; e + 4 <= ne; e += 4) {
-                double d0 = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                double d1 = sqnorm(sub(v3(P[3 * e + 3], P[3 * e + 4], P[3 * e + 5]), cp));
-                double d2 = sqnorm(sub(v3(P[3 * e + 6], P[3 * e + 7], P[3 * e + 8]), cp));
-                double d3 = sqnorm(sub(v3(P[3 * e + 9], P[3 * e + 10], P[3 * e + 11]), cp));
-                if (d0 < bd) { bd = d0; bi = e; }
-                if (d1 < bd) { bd = d1; bi = e + 1; }
-                if (d2 < bd) { bd = d2; bi = e + 2; }
-                if (d3 < bd) { bd = d3; bi = e + 3; }
-              }
-              for (; e < ne; ++e) {
-                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                if (d2v < bd) {
-                  bd = d2v;
-                  bi = e;
+              double bd;
+              int bi;
+              unsigned long long visited;
+              if (el_xs && ne >= sorted_min) {
+                // Large domain (warp-uniform branch): visit elements in order
+                // of |x - cp.x| from the domain's x-sorted index.  An element
+                // whose exact first distance term (P.x - cp.x)^2 exceeds the
+                // best distance cannot reach it ((a + b) + c >= a for b, c >=
+                // 0), so the scan stops there with the serial scan's
+                // (distance, index) minimum.
+                const double* xs = el_xs + off[q];
+                const int* ix = el_ix + off[q];
+                int lo = 0, hi = ne;  // first xs >= cp.x
+                while (lo < hi) {
+                  int mid = (lo + hi) >> 1;
+                  if (xs[mid] < cp.x) lo = mid + 1;
+                  else hi = mid;
                 }
+                int r = lo, l = lo - 1;
+                bd = kInf;
+                bi = 0x7fffffff;
+                visited = 0;
+                while (r < ne || l >= 0) {
+                  double ar = r < ne ? xs[r] - cp.x : kInf;
+                  double al = l >= 0 ? xs[l] - cp.x : kInf;
+                  double tr = ar * ar, tl = al * al;
+                  bool right = l < 0 || (r < ne && tr <= tl);
+                  if ((right ? tr : tl) > bd) break;
+                  int e = right ? ix[r++] : ix[l--];
+                  double dv = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  ++visited;
+                  if (dv < bd || (dv == bd && e < bi)) {
+                    bd = dv;
+                    bi = e;
+                  }
+                }
+                if (bi == 0x7fffffff) bi = -1;  // non-finite query: serial scan below
+              } else {
+                bi = -1;
               }
-              ctr.proj += (unsigned long long)ne;
+              if (bi < 0) {
+                // Every lane scans the same elements (broadcast loads, no
+                // divergence): faster than the pruned search for domains of
+                // a few thousand elements.
+                bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
+                bi = 0;
+                int e = 1;
+                // four independent distances in flight, compared in index order
+                for (; e + 4 <= ne; e += 4) {
+                  double d0 = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  double d1 = sqnorm(sub(v3(P[3 * e + 3], P[3 * e + 4], P[3 * e + 5]), cp));
+                  double d2 = sqnorm(sub(v3(P[3 * e + 6], P[3 * e + 7], P[3 * e + 8]), cp));
+                  double d3 = sqnorm(sub(v3(P[3 * e + 9], P[3 * e + 10], P[3 * e + 11]), cp));
+                  if (d0 < bd) { bd = d0; bi = e; }
+                  if (d1 < bd) { bd = d1; bi = e + 1; }
+                  if (d2 < bd) { bd = d2; bi = e + 2; }
+                  if (d3 < bd) { bd = d3; bi = e + 3; }
+                }
+                for (; e < ne; ++e) {
+                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  if (d2v < bd) {
+                    bd = d2v;
+                    bi = e;
+                  }
+                }
+                visited = (unsigned long long)ne;
+              }
+              ctr.proj += visited;
               cand = bi;
               const long long eg = off[q] + bi;
               slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));

@@ -183,3 +183,45 @@ def test_sharded_full_size_against_oracle_shard():
     assert mismatched_fields(sub, ref.traces) == {}
     gsub = dev.grasps[(dev.grasps["g"] >= lo) & (dev.grasps["g"] < hi)]
     assert mismatched_fields(gsub, ref.grasps, GRASP_FIELDS) == {}
+
+
+def _cfg(hand, obj, cfg, batch, **over):
+    p = lg.parse_config(asset("configs", cfg), hand=asset("hands", hand),
+                        object=asset("objects", obj), batch=batch)
+    p.want_trace = 1
+    for k, v in over.items():
+        setattr(p, k, v)
+    return p
+
+
+@pytest.mark.parametrize("args", [
+    # BASELINE config 3: LEAP-class hand on a tool-like union (reduced field)
+    ("leap_like.urdf", "mug.obj", "leap.cfg", 48, dict(field_configs=128)),
+    ("leap_like.urdf", "drill.obj", "leap.cfg", 32, dict(field_configs=128)),
+    # config 4: Shadow-class 22 DoF, k = 3 of 5 groups (reduced sampling)
+    ("shadow_like.urdf", "icosphere_r030_s6.obj", "shadow.cfg", 32,
+     dict(field_configs=64, samples_per_cm2=20.0, patch_radius=0.012)),
+    # config 2 hand, cylinder object
+    ("allegro_like.urdf", "cylinder_r025_l100.obj", "allegro.cfg", 64, dict(field_configs=256)),
+])
+def test_run_batch_synthetic_hands_bit_exact(args):
+    p = _cfg(*args[:4], **args[4])
+    dev, ref = _run_both(p)
+    for k in FUNNEL:
+        assert dev.profile[k] == ref.profile[k], k
+    assert mismatched_fields(dev.traces, ref.traces) == {}
+    assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
+
+
+@pytest.mark.parametrize("case", [dict(batch=96), dict(batch=64, hand="two_finger")])
+def test_sorted_projection_path_bit_exact(case, monkeypatch):
+    """The optional x-sorted pruned nearest-element search (LG_PROJ_SORTED_MIN)
+    forced onto every domain: identical stage traces."""
+    monkeypatch.setenv("LG_PROJ_SORTED_MIN", "1")
+    case = dict(case)
+    p = cfg1(batch=case.pop("batch"), **case)
+    dev, ref = _run_both(p)
+    for k in FUNNEL:
+        assert dev.profile[k] == ref.profile[k], k
+    assert mismatched_fields(dev.traces, ref.traces) == {}
+    assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
