@@ -356,6 +356,44 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
                      int finetune_iterations, double* q, double* max_residual,
                      int* finite, unsigned long long* used_joints);
 
+/* validate_dataset (validate.cpp:56-175) per grasp: every measured quantity
+ * the reference's checks read, in its check order.  status: 0 fully checked,
+ * 1 joint vector size mismatch, 2 pose not rigid, 3 joint limits violated,
+ * 4 no contacts (the reference's `continue` cases).  contact_state: 0 checked,
+ * 1 invalid link id, 2 normal not unit length.  wrench_error: 0 solved,
+ * 1 zero normal, 2 normal not unit length (tangent_basis throws). */
+typedef struct lg_grasp_check {
+  int status;
+  double rigid_error;
+  int n_limit;
+  int limit_link[LG_MAX_DOF];
+  double limit_value[LG_MAX_DOF];
+  int n_contacts;
+  int contact_state[LG_MAX_CONTACTS];
+  double hand_dist[LG_MAX_CONTACTS];
+  double object_dist[LG_MAX_CONTACTS];
+  double worst_depth;
+  int wrench_error;
+  double wrench_objective;
+} lg_grasp_check;
+
+/* validate_dataset on the GPU: n grasps against the hand, the object mesh
+ * (verts [nv][3], tris [nt][3]) and its surface samples ([ns][6], the
+ * sample_surface stream 'objs' the reference re-draws); p supplies
+ * contact_tol, penetration_margin, lambda_torque, mu, eps_stable and the PGD
+ * settings. */
+int lg_validate_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_grasp* grasps,
+                      long long n, const double* obj_verts, int nv, const int* obj_tris,
+                      int nt, const double* samples, int ns, const lg_run_params* p,
+                      lg_grasp_check* out);
+/* The reference's ValidationReport issues for these checks, one
+ * "<grasp>\t<message>\n" line each, message text as validate.cpp words it.
+ * Writes at most cap bytes (NUL-terminated) and the required size to
+ * *needed; *n_issues receives the issue count. */
+int lg_validation_issues(const lg_hand* hand, const lg_grasp_check* checks, long long n,
+                         const lg_run_params* p, char* buf, size_t cap, size_t* needed,
+                         long long* n_issues);
+
 /* run_batch (pipeline.cpp:308-625): the whole forward pass on the device,
  * field build included.  raw_samples = sample_surface of the object. */
 int lg_run_batch(lg_ctx* ctx, const lg_hand_desc* hand,

@@ -274,6 +274,140 @@ long long orc_field_nodes(void* fp) {
 }
 void orc_field_destroy(void* f) { delete (OrcField*)f; }
 
+// validate_dataset (validate.cpp:56-175) restated per grasp, recording every
+// quantity the reference's checks read (the issue texts are formatted from
+// these by the library's lg_validation_issues).
+int orc_validate(const lg_hand_desc* hd, const lg_grasp* grasps, long long n,
+                 const double* verts, int nv, const int* tris, int nt, const double* samples,
+                 int ns, const lg_run_params* p, lg_grasp_check* out) {
+  return guard([&] {
+    Hand h = Hand::from_desc(*hd);
+    const int nl = (int)h.links.size();
+    (void)nv;
+    for (long long gi = 0; gi < n; ++gi) {
+      const lg_grasp& g = grasps[gi];
+      lg_grasp_check r;
+      std::memset(&r, 0, sizeof(r));
+      r.n_contacts = g.n_contacts;
+      out[gi] = r;
+      lg_grasp_check& c = out[gi];
+      if (g.dof != h.dof) {
+        c.status = 1;
+        continue;
+      }
+      lgm::M3 R;
+      for (int a = 0; a < 9; ++a) R.m[a] = g.pose_R[a];
+      c.rigid_error = lgm::orthonormal_error(R);
+      if (c.rigid_error > 1e-6) {
+        c.status = 2;
+        continue;
+      }
+      for (int l = 0; l < nl; ++l) {
+        const Link& L = h.links[l];
+        if (L.jidx < 0) continue;
+        double v = g.q[L.jidx];
+        if (v < L.lo - 1e-9 || v > L.hi + 1e-9) {
+          c.limit_link[c.n_limit] = l;
+          c.limit_value[c.n_limit] = v;
+          ++c.n_limit;
+        }
+      }
+      if (c.n_limit) {
+        c.status = 3;
+        continue;
+      }
+      if (g.n_contacts <= 0) {
+        c.status = 4;
+        continue;
+      }
+      auto frames = forward_kinematics(h, g.q);
+      Xf pose;
+      for (int a = 0; a < 9; ++a) pose.R.m[a] = g.pose_R[a];
+      pose.t = lgm::v3(g.pose_t[0], g.pose_t[1], g.pose_t[2]);
+      Xf obj_inv = lgm::xf_inverse(pose);
+      for (int ci = 0; ci < g.n_contacts; ++ci) {
+        int link = g.contact_link[ci];
+        V3 pos = lgm::v3(g.contact_p[ci][0], g.contact_p[ci][1], g.contact_p[ci][2]);
+        V3 nrm = lgm::v3(g.contact_n[ci][0], g.contact_n[ci][1], g.contact_n[ci][2]);
+        if (link < 0 || link >= nl) {
+          c.contact_state[ci] = 1;
+          continue;
+        }
+        if (std::abs(lgm::norm(nrm) - 1.0) > 1e-6) {
+          c.contact_state[ci] = 2;
+          continue;
+        }
+        V3 local = lgm::xf_apply(lgm::xf_inverse(frames[link]), pos);
+        double dh = kInf;  // distance_to_link_surface (:30-42)
+        for (int pi : h.links[link].parts) {
+          const Part& P = h.parts[pi];
+          for (const auto& t : P.tris) {
+            V3 cp = closest_point_on_triangle(local, P.verts[t[0]], P.verts[t[1]], P.verts[t[2]]);
+            dh = std::min(dh, lgm::norm(lgm::sub(local, cp)));
+          }
+        }
+        c.hand_dist[ci] = dh;
+        V3 op = lgm::xf_apply(obj_inv, pos);
+        double dobj = kInf;  // distance_to_mesh (:19-28)
+        for (int t = 0; t < nt; ++t) {
+          const int* tr = tris + 3 * t;
+          V3 cp = closest_point_on_triangle(op, lgm::v3_load(verts + 3 * tr[0]),
+                                            lgm::v3_load(verts + 3 * tr[1]),
+                                            lgm::v3_load(verts + 3 * tr[2]));
+          dobj = std::min(dobj, lgm::norm(lgm::sub(op, cp)));
+        }
+        c.object_dist[ci] = dobj;
+      }
+      double worst = 0.0;  // object samples vs every link part (:125-143)
+      std::vector<Xf> inv(nl);
+      for (int l = 0; l < nl; ++l) inv[l] = lgm::xf_inverse(frames[l]);
+      for (int j = 0; j < ns; ++j) {
+        V3 world = lgm::xf_apply(pose, lgm::v3_load(samples + 6 * j));
+        for (int l = 0; l < nl; ++l) {
+          if (h.links[l].parts.empty()) continue;
+          V3 local = lgm::xf_apply(inv[l], world);
+          for (int pi : h.links[l].parts) {
+            const Part& P = h.parts[pi];
+            const Aabb& b = P.bounds;
+            if (!(local.x >= b.min.x - 1e-9 && local.y >= b.min.y - 1e-9 && local.z >= b.min.z - 1e-9 &&
+                  local.x <= b.max.x + 1e-9 && local.y <= b.max.y + 1e-9 && local.z <= b.max.z + 1e-9))
+              continue;
+            double depth = kInf;  // plane_depth (:44-52)
+            bool outside = false;
+            for (size_t k = 0; k < P.plane_n.size(); ++k) {
+              double slack = P.plane_d[k] - lgm::dot(P.plane_n[k], local);
+              if (slack < 0.0) {
+                outside = true;
+                break;
+              }
+              depth = std::min(depth, slack);
+            }
+            double d = (outside || P.plane_n.empty()) ? 0.0 : depth;
+            worst = std::max(worst, d);
+          }
+        }
+      }
+      c.worst_depth = worst;
+      std::vector<V3> pts, nrms;
+      for (int ci = 0; ci < g.n_contacts; ++ci) {
+        pts.push_back(lgm::v3(g.contact_p[ci][0], g.contact_p[ci][1], g.contact_p[ci][2]));
+        nrms.push_back(lgm::v3(g.contact_n[ci][0], g.contact_n[ci][1], g.contact_n[ci][2]));
+      }
+      try {
+        WrenchProblem wp = make_wrench_problem(pts, nrms, p->lambda_torque, p->mu);
+        WrenchOpts o;
+        o.iterations = p->pgd_iterations;
+        o.warm_iterations = p->pgd_warm_iterations;
+        o.step = p->pgd_step;
+        c.wrench_objective = solve_gswo(wp, o, nullptr).objective;
+      } catch (const std::invalid_argument& e) {
+        c.wrench_error = std::string(e.what()).find("zero") != std::string::npos ? 1 : 2;
+      }
+    }
+  });
+}
+
+
 // ContactFieldIndex::save (contact_field.cpp:570-600): the GGCF v1 stream,
 // field by field, from the oracle's map-built index and its BVHs.
 extern "C++" {

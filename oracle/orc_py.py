@@ -54,6 +54,8 @@ def lib():
             "orc_field_export": (C.c_int, [vp, P(A.FieldCsr)]),
             "orc_field_nodes": (C.c_longlong, [vp]),
             "orc_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
+            "orc_validate": (C.c_int, [HD, vp, C.c_longlong, dp, C.c_int, ip, C.c_int, dp, C.c_int,
+                                       P(A.RunParams), vp]),
             "orc_field_destroy": (None, [vp]),
             "orc_query": (C.c_int, [vp, HD, dp, C.c_int, dp, C.c_double, P(C.c_uint32), dp, ip]),
             "orc_reverse_lookup": (C.c_int, [vp, HD, dp, C.c_int, dp, C.c_double, C.c_int,
@@ -428,3 +430,16 @@ def run_batch_field(field, hand_desc, patches_desc, raw_samples, params, workers
     check(lib().orc_run_batch_field(field._h, C.byref(hand_desc), C.byref(patches_desc), _p(raw),
                                     len(raw), C.byref(params), int(workers), C.byref(h)))
     return OrcResult(h)
+
+
+def validate(hand_desc, grasps, mesh_verts, mesh_tris, samples, params):
+    """validate_dataset restated (validate.cpp:56-175): lg_grasp_check records."""
+    g = np.ascontiguousarray(grasps)
+    v = np.ascontiguousarray(mesh_verts, dtype=np.float64)
+    t = np.ascontiguousarray(mesh_tris, dtype=np.int32)
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    out = np.zeros(len(g), dtype=A.check_dtype())
+    check(lib().orc_validate(C.byref(hand_desc), g.ctypes.data_as(C.c_void_p), len(g), _p(v), len(v),
+                             t.ctypes.data_as(C.POINTER(C.c_int)), len(t), _p(s), len(s),
+                             C.byref(params), out.ctypes.data_as(C.c_void_p)))
+    return out

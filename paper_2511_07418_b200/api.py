@@ -80,6 +80,10 @@ def lib():
         "lg_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
         "lg_field_load": (C.c_int, [vp, P(A.HandDesc), C.c_char_p, C.c_uint64, P(vp)]),
         "lg_field_destroy": (None, [vp]),
+        "lg_validate_batch": (C.c_int, [vp, P(A.HandDesc), vp, C.c_longlong, A.dp, C.c_int, A.ip,
+                                        C.c_int, A.dp, C.c_int, P(A.RunParams), vp]),
+        "lg_validation_issues": (C.c_int, [vp, vp, C.c_longlong, P(A.RunParams), C.c_char_p,
+                                           C.c_size_t, P(C.c_size_t), P(C.c_longlong)]),
         "lg_query_domains_batch": (C.c_int, [vp, vp, A.ip, A.dp, C.c_int, A.dp, C.c_int,
                                              C.c_double, P(C.c_uint32), A.dp]),
         "lg_preprocess": (C.c_int, [vp, A.dp, C.c_int, C.c_double, C.c_double,
@@ -471,6 +475,39 @@ def run_batch(ctx, hand, patches, raw_samples, params, field=None):
                                        field._h, _dp(raw), len(raw), C.byref(params),
                                        C.byref(h)))
     return RunResult(h)
+
+
+def validate_batch(ctx, hand, grasps, mesh, samples, params):
+    """validate_dataset (validate.cpp:56-175) on the GPU: per-grasp checks
+    (structured array of lg_grasp_check)."""
+    g = np.ascontiguousarray(grasps)
+    assert g.dtype == A.grasp_dtype()
+    v, t = mesh.arrays()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.int32)
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    out = np.zeros(len(g), dtype=A.check_dtype())
+    check(lib().lg_validate_batch(ctx._h, C.byref(hand.desc), g.ctypes.data_as(C.c_void_p), len(g),
+                                  _dp(v), len(v), _ip(t), len(t), _dp(s), len(s), C.byref(params),
+                                  out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def validation_issues(hand, checks, params):
+    """ValidationReport.issues as [(grasp, message)], texts as validate.cpp
+    words them."""
+    c = np.ascontiguousarray(checks)
+    need, cnt = C.c_size_t(0), C.c_longlong(0)
+    check(lib().lg_validation_issues(hand._h, c.ctypes.data_as(C.c_void_p), len(c),
+                                     C.byref(params), None, 0, C.byref(need), C.byref(cnt)))
+    buf = C.create_string_buffer(need.value)
+    check(lib().lg_validation_issues(hand._h, c.ctypes.data_as(C.c_void_p), len(c),
+                                     C.byref(params), buf, need.value, C.byref(need), C.byref(cnt)))
+    out = []
+    for line in buf.value.decode().splitlines():
+        gi, what = line.split("\t", 1)
+        out.append((int(gi), what))
+    return out
 
 
 def write_dataset(path, grasps):

@@ -22,6 +22,7 @@
 #include "../capi_common.hpp"
 #include "dev_copt.cuh"
 #include "dev_post.cuh"
+#include "dev_validate.cuh"
 
 using namespace lgd;
 
@@ -1144,6 +1145,58 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
         beta_x[6 * i + c] = h_s[18 * i + 6 + c];
         beta_y[6 * i + c] = h_s[18 * i + 12 + c];
       }
+  });
+}
+
+int lg_validate_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_grasp* grasps, long long n,
+                      const double* obj_verts, int nv, const int* obj_tris, int nt,
+                      const double* samples, int ns, const lg_run_params* p,
+                      lg_grasp_check* out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !p || (n && (!grasps || !out)))
+      throw std::invalid_argument("lg_validate_batch: null argument");
+    if (nv < 0 || nt < 0 || ns < 0 || (nt && (!obj_verts || !obj_tris)) || (ns && !samples))
+      throw std::invalid_argument("lg_validate_batch: bad object arrays");
+    if (n == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    for (int t = 0; t < 3 * nt; ++t)
+      if (obj_tris[t] < 0 || obj_tris[t] >= nv) throw std::invalid_argument("lg_validate_batch: triangle index out of range");
+    for (long long i = 0; i < n; ++i)
+      if (grasps[i].n_contacts < 0 || grasps[i].n_contacts > LG_MAX_CONTACTS || grasps[i].dof < 0 ||
+          grasps[i].dof > LG_MAX_DOF)
+        throw std::invalid_argument("lg_validate_batch: grasp record out of range");
+    Buf bg, bo, bv, bt, sc[6];
+    const lg_grasp* d_g = dupload(bg, grasps, (size_t)n, s);
+    lg_grasp_check* d_o = dalloc<lg_grasp_check>(bo, (size_t)n);
+    ValCfg C;
+    C.dof = hand->dof;
+    C.contact_tol = p->contact_tol;
+    C.penetration_margin = p->penetration_margin;
+    C.lambda = p->lambda_torque;
+    C.mu = p->mu;
+    C.eps_stable = p->eps_stable;
+    C.o.iterations = p->pgd_iterations;
+    C.o.warm_iterations = p->pgd_warm_iterations;
+    C.o.step = p->pgd_step;
+    C.o.max_bt = 20;  // WrenchSolveOptions default (wrench.hpp)
+    C.obj_v = nt ? dupload(bv, obj_verts, 3 * (size_t)nv, s) : nullptr;
+    C.obj_t = nt ? dupload(bt, obj_tris, 3 * (size_t)nt, s) : nullptr;
+    C.nt = nt;
+    std::vector<double> col(ns);
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < ns; ++i) col[i] = samples[6 * i + a];
+      if (ns) dupload(sc[a], col.data(), (size_t)ns, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    DSamples S = make_samples(sc, ns);
+    k_validate<<<(unsigned)n, 256, 0, s>>>(n, d_g, C, S, d_o);
+    check_launch();
+    k_validate_wrench<<<grid_for(n, 64), 64, 0, s>>>(n, d_g, C, d_o);
+    check_launch();
+    CK(cudaMemcpyAsync(out, d_o, sizeof(lg_grasp_check) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   });
 }
 

@@ -4,6 +4,8 @@
 #include <string>
 
 #include "../capi_common.hpp"
+#include <cstdio>
+#include <algorithm>
 #include "host.hpp"
 
 struct lg_hand {
@@ -256,6 +258,85 @@ int lg_write_dataset(const char* path, const lg_grasp* g, long long n) {
 }
 int lg_write_profile(const char* path, const lg_profile* p) {
   return guard([&] { lgh::write_profile(path, *p); });
+}
+
+// ValidationReport issue texts (validate.cpp:56-175); numbers as an ostream
+// with default formatting prints them (%g, 6 significant digits).
+int lg_validation_issues(const lg_hand* hand, const lg_grasp_check* checks, long long n,
+                         const lg_run_params* p, char* buf, size_t cap, size_t* needed,
+                         long long* n_issues) {
+  return guard([&] {
+    if (!hand || (!checks && n) || !p) throw std::invalid_argument("lg_validation_issues: null argument");
+    std::string out;
+    long long count = 0;
+    auto num = [](double v) {
+      char t[64];
+      std::snprintf(t, sizeof(t), "%g", v);
+      return std::string(t);
+    };
+    auto add = [&](long long gi, const std::string& what) {
+      out += std::to_string(gi) + "\t" + what + "\n";
+      ++count;
+    };
+    const auto& links = hand->h.links;
+    for (long long gi = 0; gi < n; ++gi) {
+      const lg_grasp_check& c = checks[gi];
+      if (c.status == 1) {
+        add(gi, "joint vector size mismatch");
+        continue;
+      }
+      if (c.status == 2) {
+        add(gi, "pose not rigid: transform rotation is not orthonormal");
+        continue;
+      }
+      if (c.status == 3) {
+        for (int k = 0; k < c.n_limit; ++k) {
+          int l = c.limit_link[k];
+          std::string name = (l >= 0 && l < (int)links.size()) ? links[l].joint_name : std::string("?");
+          add(gi, "joint " + name + " out of limits: " + num(c.limit_value[k]));
+        }
+        continue;
+      }
+      if (c.status == 4) {
+        add(gi, "no contacts");
+        continue;
+      }
+      for (int ci = 0; ci < c.n_contacts; ++ci) {
+        if (c.contact_state[ci] == 1) {
+          add(gi, "contact with invalid link id");
+          continue;
+        }
+        if (c.contact_state[ci] == 2) {
+          add(gi, "contact normal not unit length");
+          continue;
+        }
+        if (c.hand_dist[ci] > p->contact_tol)
+          add(gi, "contact " + std::to_string(ci) + " is " + num(c.hand_dist[ci]) +
+                      " m off the hand surface (limit " + num(p->contact_tol) + ")");
+        if (c.object_dist[ci] > p->contact_tol)
+          add(gi, "contact " + std::to_string(ci) + " is " + num(c.object_dist[ci]) +
+                      " m off the object surface (limit " + num(p->contact_tol) + ")");
+      }
+      if (c.worst_depth > p->penetration_margin)
+        add(gi, "object penetrates the hand by " + num(c.worst_depth) + " m (limit " +
+                    num(p->penetration_margin) + ")");
+      if (c.wrench_error == 1) {
+        add(gi, "wrench recheck failed: tangent_basis: zero normal");
+      } else if (c.wrench_error == 2) {
+        add(gi, "wrench recheck failed: tangent_basis: normal is not unit length");
+      } else if (!(c.wrench_objective < p->eps_stable)) {
+        add(gi, "wrench objective " + num(c.wrench_objective) + " not under stability threshold " +
+                    num(p->eps_stable));
+      }
+    }
+    if (needed) *needed = out.size() + 1;
+    if (n_issues) *n_issues = count;
+    if (buf && cap) {
+      size_t m = std::min(cap - 1, out.size());
+      std::memcpy(buf, out.data(), m);
+      buf[m] = '\0';
+    }
+  });
 }
 
 }  // extern "C"

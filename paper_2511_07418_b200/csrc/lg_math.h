@@ -442,6 +442,28 @@ LG_HD M3 transpose(const M3& a) {
   return r;
 }
 
+// Eigen's 3x3 determinant (cofactor expansion down the first column).
+LG_HD double det3(const M3& a) {
+  const double* m = a.m;
+  double t0 = m[0] * (m[4] * m[8] - m[5] * m[7]);
+  double t1 = m[3] * (m[1] * m[8] - m[2] * m[7]);
+  double t2 = m[6] * (m[1] * m[5] - m[2] * m[4]);
+  return (t0 - t1) + t2;
+}
+
+// RigidTransform::orthonormal_error (geometry.hpp:53-59):
+// max(max |R R^T - I|, |det R - 1|).
+LG_HD double orthonormal_error(const M3& r) {
+  M3 p = mul(r, transpose(r));
+  double e = 0.0;
+  for (int i = 0; i < 9; ++i) {
+    double v = dabs(p.m[i] - ((i % 4 == 0) ? 1.0 : 0.0));
+    e = (i == 0 || v > e) ? v : e;
+  }
+  double d = dabs(det3(r) - 1.0);
+  return dmax(e, d);
+}
+
 // Eigen AngleAxis<double>::toRotationMatrix (axis used as given).
 LG_HD M3 angle_axis(double angle, V3 axis) {
   double s = lgm::xsin(angle);

@@ -108,6 +108,17 @@ class Profile(C.Structure):
         ("index_from_cache", C.c_longlong)]
 
 
+class GraspCheck(C.Structure):
+    """lg_grasp_check: validate_dataset's measured quantities per grasp."""
+    _fields_ = [
+        ("status", C.c_int), ("rigid_error", C.c_double), ("n_limit", C.c_int),
+        ("limit_link", C.c_int * LG_MAX_DOF), ("limit_value", C.c_double * LG_MAX_DOF),
+        ("n_contacts", C.c_int), ("contact_state", C.c_int * LG_MAX_CONTACTS),
+        ("hand_dist", C.c_double * LG_MAX_CONTACTS), ("object_dist", C.c_double * LG_MAX_CONTACTS),
+        ("worst_depth", C.c_double), ("wrench_error", C.c_int), ("wrench_objective", C.c_double),
+    ]
+
+
 class Trace(C.Structure):
     _fields_ = [
         ("g", C.c_longlong), ("pass_", C.c_int), ("c", C.c_int),
@@ -153,6 +164,10 @@ def _np_dtype(struct):
 
 def grasp_dtype():
     return _np_dtype(Grasp)
+
+
+def check_dtype():
+    return _np_dtype(GraspCheck)
 
 
 def trace_dtype():
