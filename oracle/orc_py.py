@@ -434,7 +434,7 @@ def run_batch_field(field, hand_desc, patches_desc, raw_samples, params, workers
 
 def validate(hand_desc, grasps, mesh_verts, mesh_tris, samples, params):
     """validate_dataset restated (validate.cpp:56-175): lg_grasp_check records."""
-    g = np.ascontiguousarray(grasps)
+    g = np.ascontiguousarray(np.asarray(grasps).astype(A.grasp_dtype()))
     v = np.ascontiguousarray(mesh_verts, dtype=np.float64)
     t = np.ascontiguousarray(mesh_tris, dtype=np.int32)
     s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)

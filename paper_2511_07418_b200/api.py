@@ -480,8 +480,7 @@ def run_batch(ctx, hand, patches, raw_samples, params, field=None):
 def validate_batch(ctx, hand, grasps, mesh, samples, params):
     """validate_dataset (validate.cpp:56-175) on the GPU: per-grasp checks
     (structured array of lg_grasp_check)."""
-    g = np.ascontiguousarray(grasps)
-    assert g.dtype == A.grasp_dtype()
+    g = np.ascontiguousarray(np.asarray(grasps).astype(A.grasp_dtype()))
     v, t = mesh.arrays()
     v = np.ascontiguousarray(v, dtype=np.float64)
     t = np.ascontiguousarray(t, dtype=np.int32)

@@ -57,6 +57,10 @@ k_validate(long long n, const lg_grasp* grasps, ValCfg C, DSamples samples, lg_g
     r.worst_depth = 0.0;
     r.wrench_error = 0;
     r.wrench_objective = 0.0;
+    for (int j = 0; j < LG_MAX_DOF; ++j) {
+      r.limit_link[j] = 0;
+      r.limit_value[j] = 0.0;
+    }
     for (int c = 0; c < LG_MAX_CONTACTS; ++c) {
       r.contact_state[c] = 0;
       r.hand_dist[c] = 0.0;
