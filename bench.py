@@ -112,6 +112,23 @@ def flop_model(prof, k, n_static_frac, mu, dof, links, depth):
     return dict(contact_opt=wrench + proj, realize=ik)
 
 
+def kernel_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    summary of the default bench workload (tools/ncu_summary.py)."""
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            rows = json.load(f)
+    except (OSError, ValueError):
+        return None, None
+    names = {"k_contact_opt": "k_contact_opt2", "k_realize": "k_realize_warp"}
+    want = names.get(kernel, kernel)
+    for r in rows:
+        if r["kernel"].startswith(want) and "dram_bytes" in r:
+            return r["dram_bytes"], os.path.relpath(path, ROOT)
+    return None, None
+
+
 def fp64_peak():
     path = os.path.join(ROOT, "profiles", "fp64_peak.json")
     try:
@@ -290,8 +307,10 @@ def run_b200(args):
     flops, secs = kern[dom]
     peak, peak_src = fp64_peak()
     achieved = flops / secs / 1e12 if secs > 0 else 0.0
+    traffic, traffic_src = kernel_traffic(dom) if args.workload == "allegro_box" else (None, None)
     roof = dict(bound="fp64", kernel=dom, achieved=achieved, peak=peak, unit="TFLOP/s",
-                frac=achieved / peak, traffic=None, peak_source=peak_src,
+                frac=achieved / peak, traffic=traffic, traffic_source=traffic_src,
+                peak_source=peak_src,
                 kernel_share_of_step=secs / prof["device_seconds"],
                 note="SIMT FP64 kernel (no HBM- or tensor-bound stage); algorithmic FLOPs from "
                      "device work counters x SURVEY 8(d) per-unit model")

@@ -241,6 +241,7 @@ void lg_result_destroy(lg_result* r);
 typedef struct lg_hand lg_hand;
 typedef struct lg_mesh lg_mesh;
 typedef struct lg_patches lg_patches;
+typedef struct lg_ctx lg_ctx;
 
 typedef struct lg_load_report {
   long long triangles_read, triangles_kept, degenerate_dropped;
@@ -280,6 +281,11 @@ uint64_t lg_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
 int lg_hand_patches(const lg_hand* h, double samples_per_cm2,
                     double patch_radius, uint64_t seed, int field_cap,
                     lg_patches** out);
+/* The same patches with decompose_patches' greedy cover and field-point
+ * subsets on the GPU (hand sampling stays on the host); identical output. */
+int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double samples_per_cm2,
+                           double patch_radius, uint64_t seed, int field_cap,
+                           lg_patches** out);
 int lg_patches_export(const lg_patches* p, lg_patches_desc* out);
 void lg_patches_destroy(lg_patches* p);
 
@@ -289,7 +295,6 @@ int lg_write_profile(const char* path, const lg_profile* p);
 
 /* ---- device side (sm_100a) ---------------------------------------------- */
 
-typedef struct lg_ctx lg_ctx;
 typedef struct lg_field lg_field;
 
 int lg_device_count(int* n);

@@ -7,7 +7,7 @@ Python mirror of the reference's C++ API over that boundary.
 """
 from .api import (  # noqa: F401
     ContactFieldIndex, Context, CudaError, HandModel, Mesh, Patches, RunResult,
-    default_config, device_count, hand_patches, index_cache_key, lib, load_hand, load_mesh,
+    default_config, device_count, hand_patches, hand_patches_device, index_cache_key, lib, load_hand, load_mesh,
     mix_seed, parse_config, prepare_inputs, preprocess_object, query_domains_batch, run_batch,
     sample_surface, validate_batch, validation_issues, write_dataset, write_profile,
 )

@@ -80,6 +80,8 @@ def lib():
         "lg_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
         "lg_field_load": (C.c_int, [vp, P(A.HandDesc), C.c_char_p, C.c_uint64, P(vp)]),
         "lg_field_destroy": (None, [vp]),
+        "lg_hand_patches_device": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_uint64, C.c_int,
+                                             P(vp)]),
         "lg_validate_batch": (C.c_int, [vp, P(A.HandDesc), vp, C.c_longlong, A.dp, C.c_int, A.ip,
                                         C.c_int, A.dp, C.c_int, P(A.RunParams), vp]),
         "lg_validation_issues": (C.c_int, [vp, vp, C.c_longlong, P(A.RunParams), C.c_char_p,
@@ -302,6 +304,16 @@ class Patches:
 
     def link_of_patch(self):
         return np.ctypeslib.as_array(self.desc.link, shape=(self.n_patches,)).copy()
+
+
+def hand_patches_device(ctx, hand, samples_per_cm2, patch_radius, seed, field_cap=8):
+    """hand_patches with decompose_patches' greedy cover and field-point
+    subsets on the GPU (identical patches)."""
+    h = C.c_void_p()
+    check(lib().lg_hand_patches_device(ctx._h, hand._h, float(samples_per_cm2),
+                                       float(patch_radius), C.c_uint64(seed), int(field_cap),
+                                       C.byref(h)))
+    return Patches(h)
 
 
 def hand_patches(hand, samples_per_cm2, patch_radius, seed, field_cap=8):

@@ -166,7 +166,16 @@ __device__ __forceinline__ void wchain_commit(const WChain& C, const double* FG,
   __syncwarp();
 }
 
+// Warp max of v.  Non-negative finite doubles order like their bit
+// patterns, so the common case is two 32-bit warp reductions; anything else
+// takes the comparison butterfly.
 __device__ __forceinline__ double warp_max_d(double v) {
+  if (__all_sync(kFull, v >= 0.0 && v <= 1.7976931348623157e308)) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    unsigned hi = __reduce_max_sync(kFull, (unsigned)(b >> 32));
+    unsigned lo = __reduce_max_sync(kFull, (unsigned)(b >> 32) == hi ? (unsigned)b : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(kFull, v, o));
   return v;
@@ -388,12 +397,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       }
       if (cm > 1e-12) used |= 1ull << lane;
     }
-    {
-      unsigned long long u = used;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) u |= __shfl_xor_sync(kFull, u, o);
-      used = u;
-    }
+    used = __reduce_or_sync(kFull, (unsigned)used);  // dof <= 32: one word
     __syncwarp();
     // J^T J (upper triangle, mirrored) and J^T r
     const int ne = dof * (dof + 1) / 2;

@@ -23,6 +23,8 @@
 #include "dev_copt.cuh"
 #include "dev_post.cuh"
 #include "dev_validate.cuh"
+#include "dev_patches.cuh"
+#include "../host/capi_types.hpp"
 
 using namespace lgd;
 
@@ -1145,6 +1147,87 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
         beta_x[6 * i + c] = h_s[18 * i + 6 + c];
         beta_y[6 * i + c] = h_s[18 * i + 12 + c];
       }
+  });
+}
+
+int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double spc, double radius,
+                           uint64_t seed, int cap, lg_patches** out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !out) throw std::invalid_argument("lg_hand_patches_device: null argument");
+    const auto& H = hand->h;
+    // per-link hand samples, stream 'hnds' (pipeline.cpp:277-285), host side
+    std::vector<int> seg_link;
+    std::vector<long long> off{0};
+    std::vector<double> pos, nrm;
+    for (size_t l = 0; l < H.links.size(); ++l) {
+      if (H.links[l].visual.verts.empty()) continue;
+      auto S = lgh::sample_surface(H.links[l].visual, spc, lgm::mix_seed(seed, 0x686e6473ull, l));
+      if (S.empty()) continue;
+      seg_link.push_back((int)l);
+      for (const auto& x : S) {
+        pos.insert(pos.end(), {x.p.x, x.p.y, x.p.z});
+        nrm.insert(nrm.end(), {x.n.x, x.n.y, x.n.z});
+      }
+      off.push_back((long long)(pos.size() / 3));
+    }
+    if (radius <= 0.0 || cap < 1) throw std::invalid_argument("decompose_patches: bad radius or cap");
+    if (cap > 16) throw std::invalid_argument("lg_hand_patches_device: field cap above 16");
+    const long long total = off.back();
+    if (total == 0) throw std::invalid_argument("decompose_patches: no surface samples");
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    const int nseg = (int)seg_link.size();
+    Buf bl, bo, bp, ba, bb, bm, bs, bn;
+    const int* d_l = dupload(bl, seg_link.data(), seg_link.size(), s);
+    const long long* d_o = dupload(bo, off.data(), off.size(), s);
+    const double* d_p = dupload(bp, pos.data(), pos.size(), s);
+    int* d_a = dalloc<int>(ba, (size_t)total);
+    int* d_b = dalloc<int>(bb, (size_t)total);
+    int* d_m = dalloc<int>(bm, (size_t)total);
+    int* d_s = dalloc<int>(bs, (size_t)total);
+    int* d_n = dalloc<int>(bn, (size_t)nseg);
+    k_patch_cover<<<nseg, kCoverThreads, 0, s>>>(nseg, d_l, d_o, d_p, 0.5 * radius, seed, d_a, d_b,
+                                                 d_m, d_s, d_n);
+    check_launch();
+    auto members = ddownload(d_m, (size_t)total, s);
+    auto pstart = ddownload(d_s, (size_t)total, s);
+    auto npatch = ddownload(d_n, (size_t)nseg, s);
+    // global patch order = link order, then cover order (patch.id)
+    std::vector<int> msize, fp_off{0};
+    auto* P = new lg_patches;
+    std::unique_ptr<lg_patches> own(P);
+    lgh::Patches& R = P->p;
+    R.point_off.push_back(0);
+    R.fp_off.push_back(0);
+    for (int b = 0; b < nseg; ++b) {
+      const long long base = off[b];
+      const int N = (int)(off[b + 1] - base);
+      for (int k = 0; k < npatch[b]; ++k) {
+        int st = pstart[base + k], en = k + 1 < npatch[b] ? pstart[base + k + 1] : N;
+        R.link.push_back(seg_link[b]);
+        for (int i = st; i < en; ++i) {
+          long long g = base + members[base + i];
+          R.pts.insert(R.pts.end(), {pos[3 * g], pos[3 * g + 1], pos[3 * g + 2]});
+          R.nrm.insert(R.nrm.end(), {nrm[3 * g], nrm[3 * g + 1], nrm[3 * g + 2]});
+        }
+        R.point_off.push_back((int)(R.pts.size() / 3));
+        msize.push_back(en - st);
+        fp_off.push_back(fp_off.back() + std::min(en - st, cap));
+      }
+    }
+    const int np = (int)msize.size();
+    std::vector<int> gid(np);
+    for (int t = 0; t < np; ++t) gid[t] = t;
+    Buf bg, bz, bf, bq;
+    const int* d_g = dupload(bg, gid.data(), gid.size(), s);
+    const int* d_z = dupload(bz, msize.data(), msize.size(), s);
+    const int* d_f = dupload(bf, fp_off.data(), fp_off.size(), s);
+    int* d_q = dalloc<int>(bq, (size_t)fp_off.back());
+    k_patch_fields<<<grid_for(np, 128), 128, 0, s>>>(np, d_g, d_z, d_f, cap, seed, d_q);
+    check_launch();
+    R.fps = ddownload(d_q, (size_t)fp_off.back(), s);
+    R.fp_off = fp_off;
+    *out = own.release();
   });
 }
 

@@ -6,19 +6,7 @@
 #include "../capi_common.hpp"
 #include <cstdio>
 #include <algorithm>
-#include "host.hpp"
-
-struct lg_hand {
-  lgh::Hand h;
-};
-struct lg_mesh {
-  lgh::Mesh m;
-  std::vector<double> fv;
-  std::vector<int> ft;
-};
-struct lg_patches {
-  lgh::Patches p;
-};
+#include "capi_types.hpp"
 
 namespace lgc {
 thread_local std::string g_error;

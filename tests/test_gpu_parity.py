@@ -225,3 +225,30 @@ def test_sorted_projection_path_bit_exact(case, monkeypatch):
         assert dev.profile[k] == ref.profile[k], k
     assert mismatched_fields(dev.traces, ref.traces) == {}
     assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
+
+
+def _patch_arrays(pt):
+    d = pt.desc
+    P = d.n_patches
+    arr = np.ctypeslib.as_array
+    po = arr(d.point_off, shape=(P + 1,)).copy()
+    fo = arr(d.fp_off, shape=(P + 1,)).copy()
+    return dict(link=arr(d.link, shape=(P,)).copy(), point_off=po, fp_off=fo,
+                points=arr(d.points, shape=(3 * po[-1],)).copy(),
+                normals=arr(d.normals, shape=(3 * po[-1],)).copy(),
+                field_points=arr(d.field_points, shape=(fo[-1],)).copy())
+
+
+@pytest.mark.parametrize("hand_name,spc,radius,cap", [
+    ("four_finger.urdf", 30.0, 0.014, 8),
+    ("allegro_like.urdf", 30.0, 0.012, 8),
+    ("shadow_like.urdf", 1000.0, 0.008, 8),   # config 4: ~810k hand samples
+    ("shadow_like.urdf", 200.0, 0.008, 3),
+])
+def test_patches_device_identical(ctx, hand_name, spc, radius, cap):
+    """decompose_patches on the GPU == the host cover."""
+    hand = lg.load_hand(asset("hands", hand_name))
+    a = _patch_arrays(lg.hand_patches(hand, spc, radius, 7, cap))
+    b = _patch_arrays(lg.hand_patches_device(ctx, hand, spc, radius, 7, cap))
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
