@@ -86,7 +86,8 @@ __device__ __forceinline__ void acc_contact(const double* s, double a, double bx
 
 // descend (wrench.cpp:124-177) on state (a, bx, by) in shared memory.  The
 // trial state goes to the lane's shared scratch `tr` ([3][NC]) and is copied
-// on acceptance instead of being recomputed from the gradient.
+// on acceptance instead of being recomputed from the gradient, and the
+// accepted trial's force / torque sums serve as the next gradient's.
 template <bool FR, int NC>
 __device__ double pv_descend(const PV& w, int anchor, int iterations, double step0, int max_bt,
                              double* a, double* bx, double* by, double* tr, Ctr& ctr) {
@@ -99,10 +100,12 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
   double* tbx = tr + NC;
   double* tby = tr + 2 * NC;
   for (int it = 0; it < iterations; ++it) {
-    V3 force = v3(0.0, 0.0, 0.0), torque = v3(0.0, 0.0, 0.0);
-    for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], force, torque);
+    // the gradient's force / torque sums at the current state are exactly the
+    // sums of its evaluation (same state, same operations, same order): the
+    // initial one, then the accepted trial's
+    V3 force = f;
     ++ctr.wgrad;
-    torque = v3(torque.x * w.lambda, torque.y * w.lambda, torque.z * w.lambda);
+    V3 torque = v3(t.x * w.lambda, t.y * w.lambda, t.z * w.lambda);
     double step = step0;
     bool moved = false;
     for (int bt = 0; bt <= max_bt; ++bt) {
@@ -129,6 +132,8 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
           bx[i] = tbx[i];
           by[i] = tby[i];
         }
+        f = f2;
+        t = t2;
         current = next;
         moved = true;
         break;
@@ -312,12 +317,24 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
                 bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
                 bi = 0;
                 int e = 1;
-                // four independent distances in flight, compared in index order
+                // peel to an even global element (16-byte aligned pairs)
+                if (e < ne && ((off[q] + e) & 1)) {
+                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  if (d2v < bd) {
+                    bd = d2v;
+                    bi = e;
+                  }
+                  ++e;
+                }
+                // four independent distances in flight (six 16-byte loads),
+                // compared in index order
                 for (; e + 4 <= ne; e += 4) {
-                  double d0 = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                  double d1 = sqnorm(sub(v3(P[3 * e + 3], P[3 * e + 4], P[3 * e + 5]), cp));
-                  double d2 = sqnorm(sub(v3(P[3 * e + 6], P[3 * e + 7], P[3 * e + 8]), cp));
-                  double d3 = sqnorm(sub(v3(P[3 * e + 9], P[3 * e + 10], P[3 * e + 11]), cp));
+                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
                   if (d0 < bd) { bd = d0; bi = e; }
                   if (d1 < bd) { bd = d1; bi = e + 1; }
                   if (d2 < bd) { bd = d2; bi = e + 2; }
