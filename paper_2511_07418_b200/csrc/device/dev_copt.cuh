@@ -326,8 +326,29 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
                   }
                   ++e;
                 }
-                // four independent distances in flight (six 16-byte loads),
-                // compared in index order
+                // eight independent distances in flight (twelve 16-byte
+                // loads: the domain streams from L2), compared in index order
+                for (; e + 8 <= ne; e += 8) {
+                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                  double2 b0 = Q[6], b1 = Q[7], b2 = Q[8], b3 = Q[9], b4 = Q[10], b5 = Q[11];
+                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
+                  double d4 = sqnorm(sub(v3(b0.x, b0.y, b1.x), cp));
+                  double d5 = sqnorm(sub(v3(b1.y, b2.x, b2.y), cp));
+                  double d6 = sqnorm(sub(v3(b3.x, b3.y, b4.x), cp));
+                  double d7 = sqnorm(sub(v3(b4.y, b5.x, b5.y), cp));
+                  if (d0 < bd) { bd = d0; bi = e; }
+                  if (d1 < bd) { bd = d1; bi = e + 1; }
+                  if (d2 < bd) { bd = d2; bi = e + 2; }
+                  if (d3 < bd) { bd = d3; bi = e + 3; }
+                  if (d4 < bd) { bd = d4; bi = e + 4; }
+                  if (d5 < bd) { bd = d5; bi = e + 5; }
+                  if (d6 < bd) { bd = d6; bi = e + 6; }
+                  if (d7 < bd) { bd = d7; bi = e + 7; }
+                }
                 for (; e + 4 <= ne; e += 4) {
                   const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
                   double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];

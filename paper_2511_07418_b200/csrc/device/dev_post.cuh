@@ -132,6 +132,113 @@ __global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const
   }
 }
 
+// validate_grasp_collisions, one warp per configuration (4 per CTA, no
+// block barriers): the warp's FK, part boxes and object-overlap list, then
+// the link-link GJK pairs and the object-sample sweep, lanes striding over
+// each; every test is the reference's exact one (see k_collision2), the
+// verdict an OR and the depth a max.
+constexpr int kCollWarps = 4;
+struct CollWarpSmem {
+  double q[kMaxDof];
+  double fr[kMaxLinks * kFS];
+  double inv[kMaxLinks * kFS];
+  double box[64 * 6];
+  int obj[64];
+  int nobj, viol;
+};
+
+__global__ void __launch_bounds__(32 * kCollWarps)
+k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, const double* q_all,
+             const double* pose, const double* obj_aabb, int clean_only, uint8_t* clean_out,
+             double* maxpen_out) {
+  __shared__ CollWarpSmem S[kCollWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int call = blockIdx.x * kCollWarps + wid;
+  if (call >= n_calls) return;  // warp-uniform
+  if (call_on && !call_on[call]) return;
+  CollWarpSmem& W = S[wid];
+  const int i = call_cand[call];
+  const int np = c_hand.n_parts, nl = c_hand.n_links;
+  if (lane < c_hand.dof) W.q[lane] = q_all[(size_t)call * kMaxDof + lane];
+  if (lane == 0) {
+    W.nobj = 0;
+    W.viol = 0;
+  }
+  __syncwarp();
+  wfk_s(W.q, W.fr, lane);
+  if (lane < nl) st_xf(W.inv + kFS * lane, xf_inverse(ld_xf(W.fr + kFS * lane)));
+  const double* ob = obj_aabb + 6 * i;
+  const double oi[6] = {ob[0] - C.margin, ob[1] - C.margin, ob[2] - C.margin,
+                        ob[3] + C.margin, ob[4] + C.margin, ob[5] + C.margin};
+  auto ovl = [](const double* a, const double* b) {
+    return a[0] <= b[3] && a[1] <= b[4] && a[2] <= b[5] && a[3] >= b[0] && a[4] >= b[1] &&
+           a[5] >= b[2];
+  };
+  for (int p = lane; p < np; p += 32) {
+    V3 mn, mx;
+    world_bounds(p, ld_xf(W.fr + kFS * C.part_link[p]), &mn, &mx);
+    double* bx = W.box + 6 * p;
+    bx[0] = mn.x - C.margin;
+    bx[1] = mn.y - C.margin;
+    bx[2] = mn.z - C.margin;
+    bx[3] = mx.x + C.margin;
+    bx[4] = mx.y + C.margin;
+    bx[5] = mx.z + C.margin;
+    if (C.raw.n > 0 && ovl(bx, oi)) W.obj[atomicAdd(&W.nobj, 1)] = p;
+  }
+  __syncwarp();
+  // broad phase (collision.cpp:22-45) + GJK narrow phase
+  for (int e = lane; e < np * np; e += 32) {
+    int pa = e / np, pb = e % np;
+    if (pb <= pa || !ovl(W.box + 6 * pa, W.box + 6 * pb)) continue;
+    int la = C.part_link[pa], lb = C.part_link[pb];
+    if (la == lb || g_hand.parent[la] == lb || g_hand.parent[lb] == la) continue;
+    if (clean_only && *(volatile int*)&W.viol) break;
+    if (gjk_distance(pa, ld_xf(W.fr + kFS * la), pb, ld_xf(W.fr + kFS * lb)) == 0.0)
+      atomicOr(&W.viol, 1);
+  }
+  // object samples (collision.cpp:260-284): world point once, world-box
+  // prefilter (widened 1e-6), then the exact local test and depth
+  double mx = 0.0;
+  const int nobj = W.nobj;
+  if (nobj > 0) {
+    const Xf x = load_xf(pose + 12 * i);
+    for (int j = lane; j < C.raw.n; j += 32) {
+      if (clean_only && *(volatile int*)&W.viol) break;
+      V3 w = xf_apply(x, C.raw.p(j));
+      bool hit = false;
+      for (int o = 0; o < nobj; ++o) {
+        const int pa = W.obj[o];
+        const double* bx = W.box + 6 * pa;
+        if (!(w.x >= bx[0] - 1e-6 && w.y >= bx[1] - 1e-6 && w.z >= bx[2] - 1e-6 &&
+              w.x <= bx[3] + 1e-6 && w.y <= bx[4] + 1e-6 && w.z <= bx[5] + 1e-6))
+          continue;
+        V3 local = xf_apply(ld_xf(W.inv + kFS * C.part_link[pa]), w);
+        const double* b = c_hand.bounds + 6 * pa;
+        if (!(local.x >= b[0] - 1e-9 && local.y >= b[1] - 1e-9 && local.z >= b[2] - 1e-9 &&
+              local.x <= b[3] + 1e-9 && local.y <= b[4] + 1e-9 && local.z <= b[5] + 1e-9))
+          continue;
+        double depth = part_interior_depth(pa, local);
+        if (depth > C.margin) {
+          hit = true;
+          mx = dmax(mx, depth);
+          if (clean_only) break;
+        }
+      }
+      if (hit) atomicOr(&W.viol, 1);
+    }
+  }
+  __syncwarp();
+  if (maxpen_out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = dmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    clean_out[call] = W.viol ? 0 : 1;
+    if (maxpen_out) maxpen_out[call] = mx;
+  }
+}
+
 // Reverse lookup for (candidate b, attempt, slot) (contact_field.cpp:450-484).
 __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int k, int A, int c_lo,
                               int Bsz, int pass, uint64_t seed, DField f,

@@ -906,7 +906,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nP);
       CK(cudaMemsetAsync(d_clean, 0, nP, s));
-      k_collision2<<<(int)nP, 128, 0, s>>>((int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, 1,
+      k_collision3<<<((int)nP + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
+          (int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, 1,
                                             d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
@@ -981,7 +982,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nU);
       out.profile.collision_calls += nU;
-      k_collision2<<<(int)nU, 128, 0, s>>>((int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, 1,
+      k_collision3<<<((int)nU + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
+          (int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, 1,
                                             d_clean, nullptr);
       LAUNCH(ctx);
       check_launch();
@@ -1322,7 +1324,8 @@ int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const doubl
     cc.margin = margin;
     cc.raw = S;
     cc.part_link = ctx->h_part_link.as<int>();
-    k_collision2<<<m, 128, 0, s>>>(m, cc, d_i, nullptr, d_q, d_p, d_b, 0, d_c, d_m);
+    k_collision3<<<(m + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(m, cc, d_i, nullptr, d_q,
+                                                                             d_p, d_b, 0, d_c, d_m);
     check_launch();
     CK(cudaMemcpyAsync(clean, d_c, (size_t)m, cudaMemcpyDeviceToHost, s));
     if (max_penetration)

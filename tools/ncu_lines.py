@@ -1,6 +1,6 @@
 """Per-source-line stall samples from an ncu report (needs -lineinfo).
 
-usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [TOP]
+usage: python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [TOP] [stall|inst]
 Runs `ncu -i REPORT --page source --csv --print-source cuda,sass -k KERNEL`
 and prints the TOP source lines by warp-stall samples with their dominant
 stall reasons.
@@ -15,6 +15,7 @@ import sys
 def main():
     rep, kern = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+    by = sys.argv[4] if len(sys.argv) > 4 else "stall"
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
                           "cuda,sass", "-k", kern], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -46,11 +47,13 @@ def main():
             return 0.0
 
     tot = sum(f(r[si]) for _, r in lines) or 1.0
-    ranked = sorted(lines, key=lambda x: -f(x[1][si]))[:top]
+    itot = sum(f(r[ie]) for _, r in lines) or 1.0
+    col = ie if by == "inst" else si
+    ranked = sorted(lines, key=lambda x: -f(x[1][col]))[:top]
     for fn, r in ranked:
         reasons = sorted(((f(r[i]), h[6:]) for i, h in stall), reverse=True)[:3]
         rs = " ".join(f"{h}:{100 * v / max(f(r[si]), 1):.0f}%" for v, h in reasons if v > 0)
-        print(f"{100 * f(r[si]) / tot:5.1f}% {fn}:{r[0]:>4s} inst={int(f(r[ie])):>11d} "
+        print(f"{100 * f(r[si]) / tot:5.1f}% {fn}:{r[0]:>4s} inst={100 * f(r[ie]) / itot:5.1f}% "
               f"{r[1].strip()[:70]:70s} {rs}")
 
 
