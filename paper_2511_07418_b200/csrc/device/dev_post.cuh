@@ -13,130 +13,16 @@
 
 namespace lgd {
 
-// validate_grasp_collisions (collision.cpp:230-288), block per configuration:
-// warp 0 runs the level-synchronous FK; threads build the part boxes and the
-// object-overlapping part list, then share the link-link GJK pairs and the
-// object-sample sweep with no barrier in between (sample chunks are handed
-// out dynamically, so threads that ran a GJK simply take fewer chunks).
-// Each sample is moved to world once; a part is tested only when the world
-// point lies in the part's world box (the transformed local box, so it
-// contains every point of the local AABB test, widened by 1e-6), and then
-// with the reference's exact local transform and depth.  clean() is an OR of
-// violations and max_penetration a max, both order independent.  With
-// clean_only (the pipeline consumes only clean()), work stops at the first
-// violation.
-__global__ void k_collision2(int n_calls, CollCfg C, const int* call_cand, const int* call_on,
-                             const double* q_all, const double* pose, const double* obj_aabb,
-                             int clean_only, uint8_t* clean_out, double* maxpen_out) {
-  __shared__ double s_q[kMaxDof];
-  __shared__ double s_fr[kMaxLinks * kFS];
-  __shared__ double s_box[64 * 6];
-  __shared__ double s_inv[64 * kFS];
-  __shared__ int s_obj[64];
-  __shared__ int s_nobj;
-  __shared__ int s_viol;
-  __shared__ int s_next;
-  __shared__ double scratch[32];
-  const int call = blockIdx.x;
-  if (call >= n_calls) return;
-  if (call_on && !call_on[call]) return;
-  const int i = call_cand[call];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int np = c_hand.n_parts;
-  if (tid < c_hand.dof) s_q[tid] = q_all[(size_t)call * kMaxDof + tid];
-  if (tid == 0) {
-    s_nobj = 0;
-    s_viol = 0;
-    s_next = 0;
-  }
-  __syncthreads();
-  if (tid < 32) wfk_s(s_q, s_fr, lane);
-  __syncthreads();
-  const double* ob = obj_aabb + 6 * i;
-  const double oi[6] = {ob[0] - C.margin, ob[1] - C.margin, ob[2] - C.margin,
-                        ob[3] + C.margin, ob[4] + C.margin, ob[5] + C.margin};
-  auto ovl = [](const double* a, const double* b) {
-    return a[0] <= b[3] && a[1] <= b[4] && a[2] <= b[5] && a[3] >= b[0] && a[4] >= b[1] &&
-           a[5] >= b[2];
-  };
-  for (int p = tid; p < np; p += blockDim.x) {
-    V3 mn, mx;
-    Xf fl = ld_xf(s_fr + kFS * C.part_link[p]);
-    world_bounds(p, fl, &mn, &mx);
-    double* bx = s_box + 6 * p;
-    bx[0] = mn.x - C.margin;
-    bx[1] = mn.y - C.margin;
-    bx[2] = mn.z - C.margin;
-    bx[3] = mx.x + C.margin;
-    bx[4] = mx.y + C.margin;
-    bx[5] = mx.z + C.margin;
-    if (C.raw.n > 0 && ovl(bx, oi)) {
-      int o = atomicAdd(&s_nobj, 1);
-      s_obj[o] = p;
-      st_xf(s_inv + kFS * o, xf_inverse(fl));
-    }
-  }
-  __syncthreads();
-  // broad phase (collision.cpp:22-45) + GJK narrow phase, pairs in parallel
-  for (int e = tid; e < np * np; e += blockDim.x) {
-    int pa = e / np, pb = e % np;
-    if (pb <= pa || !ovl(s_box + 6 * pa, s_box + 6 * pb)) continue;
-    int la = C.part_link[pa], lb = C.part_link[pb];
-    if (la == lb || g_hand.parent[la] == lb || g_hand.parent[lb] == la) continue;
-    if (clean_only && *(volatile int*)&s_viol) break;
-    if (gjk_distance(pa, ld_xf(s_fr + kFS * la), pb, ld_xf(s_fr + kFS * lb)) == 0.0)
-      atomicOr(&s_viol, 1);
-  }
-  // object samples (collision.cpp:260-284)
-  double mx = 0.0;
-  const int nobj = s_nobj;
-  if (nobj > 0) {
-    const Xf x = load_xf(pose + 12 * i);
-    // warps take 32-sample chunks (coalesced sample columns), lane per sample
-    for (;;) {
-      int j0 = 0;
-      if (lane == 0) j0 = (clean_only && *(volatile int*)&s_viol) ? C.raw.n : atomicAdd(&s_next, 32);
-      j0 = __shfl_sync(0xffffffffu, j0, 0);  // warp-uniform chunk / stop
-      if (j0 >= C.raw.n) break;
-      const int j = j0 + lane;
-      bool hit = false;
-      if (j < C.raw.n) {
-        V3 w = xf_apply(x, C.raw.p(j));
-        for (int o = 0; o < nobj; ++o) {
-          const double* bx = s_box + 6 * s_obj[o];
-          if (!(w.x >= bx[0] - 1e-6 && w.y >= bx[1] - 1e-6 && w.z >= bx[2] - 1e-6 &&
-                w.x <= bx[3] + 1e-6 && w.y <= bx[4] + 1e-6 && w.z <= bx[5] + 1e-6))
-            continue;
-          const int pa = s_obj[o];
-          V3 local = xf_apply(ld_xf(s_inv + kFS * o), w);
-          const double* b = c_hand.bounds + 6 * pa;
-          if (!(local.x >= b[0] - 1e-9 && local.y >= b[1] - 1e-9 && local.z >= b[2] - 1e-9 &&
-                local.x <= b[3] + 1e-9 && local.y <= b[4] + 1e-9 && local.z <= b[5] + 1e-9))
-            continue;
-          double depth = part_interior_depth(pa, local);
-          if (depth > C.margin) {
-            hit = true;
-            mx = dmax(mx, depth);
-            if (clean_only) break;
-          }
-        }
-      }
-      if (__any_sync(0xffffffffu, hit) && lane == 0) atomicOr(&s_viol, 1);
-    }
-  }
-  if (maxpen_out) mx = block_max(mx, scratch);  // synchronises the block
-  __syncthreads();
-  if (tid == 0) {
-    clean_out[call] = s_viol ? 0 : 1;
-    if (maxpen_out) maxpen_out[call] = mx;
-  }
-}
-
-// validate_grasp_collisions, one warp per configuration (4 per CTA, no
-// block barriers): the warp's FK, part boxes and object-overlap list, then
-// the link-link GJK pairs and the object-sample sweep, lanes striding over
-// each; every test is the reference's exact one (see k_collision2), the
-// verdict an OR and the depth a max.
+// validate_grasp_collisions (collision.cpp:230-288), one warp per
+// configuration (4 per CTA, no block barriers): the warp's FK, part boxes
+// and object-overlap list, then the link-link GJK pairs and the object-sample
+// sweep, lanes striding over each.  Each sample is moved to world once; a
+// part is tested only when the world point lies in the part's world box (the
+// transformed local box, so it contains every point the local AABB test
+// accepts, widened by 1e-6), and then with the reference's exact local
+// transform and depth.  clean() is an OR of violations and max_penetration a
+// max, both order independent.  With clean_only (the pipeline consumes only
+// clean()), work stops at the first violation.
 constexpr int kCollWarps = 4;
 struct CollWarpSmem {
   double q[kMaxDof];
