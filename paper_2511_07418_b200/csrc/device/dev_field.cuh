@@ -85,6 +85,49 @@ __device__ __forceinline__ int find_run(const DField& f, const long long* c) {
   }
 }
 
+// Cube map over directions: face f in 0..5 = +x,-x,+y,-y,+z,-z, (u, v) in
+// [-1, 1]^2 on the face, R x R cells.  Returns -1 for a zero / non-finite m.
+__host__ __device__ __forceinline__ V3 cube_dir(int face, double u, double v) {
+  switch (face) {
+    case 0: return v3(1.0, u, v);
+    case 1: return v3(-1.0, u, v);
+    case 2: return v3(u, 1.0, v);
+    case 3: return v3(u, -1.0, v);
+    case 4: return v3(u, v, 1.0);
+    default: return v3(u, v, -1.0);
+  }
+}
+__device__ __forceinline__ int cube_cell(V3 m, int R) {
+  double ax = fabs(m.x), ay = fabs(m.y), az = fabs(m.z);
+  int face;
+  double u, v, d;
+  if (ax >= ay && ax >= az) {
+    face = m.x > 0.0 ? 0 : 1;
+    d = ax;
+    u = m.y;
+    v = m.z;
+  } else if (ay >= az) {
+    face = m.y > 0.0 ? 2 : 3;
+    d = ay;
+    u = m.x;
+    v = m.z;
+  } else {
+    face = m.z > 0.0 ? 4 : 5;
+    d = az;
+    u = m.x;
+    v = m.y;
+  }
+  if (!(d > 0.0) || !(d <= 1.7976931348623157e308)) return -1;
+  u /= d;
+  v /= d;
+  double fi = (u + 1.0) * 0.5 * R, fj = (v + 1.0) * 0.5 * R;
+  if (!(fi >= -1.0 && fi <= R + 1.0 && fj >= -1.0 && fj <= R + 1.0)) return -1;
+  int i = (int)fi, j = (int)fj;
+  i = i < 0 ? 0 : (i >= R ? R - 1 : i);
+  j = j < 0 ? 0 : (j >= R ? R - 1 : j);
+  return (face * R + i) * R + j;
+}
+
 // ------------------------------------------------------------ field build
 // field_config (contact_field.cpp:101-114) + FK: one thread per config.
 __global__ void k_field_frames(int N, uint64_t seed, double* frames) {
@@ -108,7 +151,8 @@ __global__ void k_field_frames(int N, uint64_t seed, double* frames) {
 // so the lowest code wins ties.
 __global__ void k_field_vectors(int N, int F, const int* fp_link, const int* fp_point,
                                 const double* pts, const double* nrm, const double* frames,
-                                const double* codebook, int C, double w, long long* cells,
+                                const double* codebook, int C, double w, int qR,
+                                const int2* qrng, const uint16_t* qcodes, long long* cells,
                                 uint16_t* codes, long long* cmin, long long* cmax) {
   extern __shared__ double s_cb[];
   for (int i = threadIdx.x; i < 3 * C; i += blockDim.x) s_cb[i] = codebook[i];
@@ -130,11 +174,28 @@ __global__ void k_field_vectors(int N, int F, const int* fp_link, const int* fp_
     V3 n = xf_rotate(x, v3_load(nrm + 3 * pi));
     int best = 0;
     double best_dot = -2.0;
-    for (int i = 0; i < C; ++i) {
-      double d = dot(v3(s_cb[3 * i], s_cb[3 * i + 1], s_cb[3 * i + 2]), n);
-      if (d > best_dot) {
-        best_dot = d;
-        best = i;
+    // the codes of n's cube-map cell (ascending; they include every code
+    // that can be the argmax anywhere in the cell) or, off the fast path,
+    // the whole codebook: the same first-max code either way
+    double n2 = dot(n, n);
+    int cell = (qR > 0 && n2 >= 1.0 - 1e-9 && n2 <= 1.0 + 1e-9) ? cube_cell(n, qR) : -1;
+    int2 rg = cell >= 0 ? qrng[cell] : make_int2(0, -1);
+    if (rg.y >= 0) {
+      for (int t = 0; t < rg.y; ++t) {
+        int i = qcodes[rg.x + t];
+        double d = dot(v3(s_cb[3 * i], s_cb[3 * i + 1], s_cb[3 * i + 2]), n);
+        if (d > best_dot) {
+          best_dot = d;
+          best = i;
+        }
+      }
+    } else {
+      for (int i = 0; i < C; ++i) {
+        double d = dot(v3(s_cb[3 * i], s_cb[3 * i + 1], s_cb[3 * i + 2]), n);
+        if (d > best_dot) {
+          best_dot = d;
+          best = i;
+        }
       }
     }
     long long cl[3];
@@ -293,49 +354,6 @@ __global__ void k_cmask_fill(int n_runs, const int* run_start, const int* run_co
   }
 }
 
-// Cube map over directions: face f in 0..5 = +x,-x,+y,-y,+z,-z, (u, v) in
-// [-1, 1]^2 on the face, R x R cells.  Returns -1 for a zero / non-finite m.
-__host__ __device__ __forceinline__ V3 cube_dir(int face, double u, double v) {
-  switch (face) {
-    case 0: return v3(1.0, u, v);
-    case 1: return v3(-1.0, u, v);
-    case 2: return v3(u, 1.0, v);
-    case 3: return v3(u, -1.0, v);
-    case 4: return v3(u, v, 1.0);
-    default: return v3(u, v, -1.0);
-  }
-}
-__device__ __forceinline__ int cube_cell(V3 m, int R) {
-  double ax = fabs(m.x), ay = fabs(m.y), az = fabs(m.z);
-  int face;
-  double u, v, d;
-  if (ax >= ay && ax >= az) {
-    face = m.x > 0.0 ? 0 : 1;
-    d = ax;
-    u = m.y;
-    v = m.z;
-  } else if (ay >= az) {
-    face = m.y > 0.0 ? 2 : 3;
-    d = ay;
-    u = m.x;
-    v = m.z;
-  } else {
-    face = m.z > 0.0 ? 4 : 5;
-    d = az;
-    u = m.x;
-    v = m.y;
-  }
-  if (!(d > 0.0) || !(d <= 1.7976931348623157e308)) return -1;
-  u /= d;
-  v /= d;
-  double fi = (u + 1.0) * 0.5 * R, fj = (v + 1.0) * 0.5 * R;
-  if (!(fi >= -1.0 && fi <= R + 1.0 && fj >= -1.0 && fj <= R + 1.0)) return -1;
-  int i = (int)fi, j = (int)fj;
-  i = i < 0 ? 0 : (i >= R ? R - 1 : i);
-  j = j < 0 ? 0 : (j >= R ? R - 1 : j);
-  return (face * R + i) * R + j;
-}
-
 // One block per cube cell: the codes whose direction lies within
 // acos(theta) + (cell angular radius) + 1e-6 rad of the cell centre — a
 // superset of the codes that can pass -dot(code, n) >= theta for any unit n
@@ -428,6 +446,73 @@ __device__ __forceinline__ void sample_hits(const DField& f, const double* cb, V
     int b = f.cell_box[j];
     if (box_hit(f, cb, b, n, theta)) visit(f.box_patch[b], b, 0.0);
   }
+}
+
+// quantize_normal candidate lists (contact_field.cpp:160-172): for cube
+// cell X with centre u and angular radius r, let a = angle to the code
+// nearest u.  For any unit n in X the best code is within a + r of n
+// (that code is), hence within a + 2r of u: listing every code within
+// a + 2r + 1e-6 rad of u (ascending) keeps every possible argmax and every
+// tie.  One block per cell; lists longer than lmax fall back to the full
+// scan (count -1).
+__global__ void k_quantlist(int R, int lmax, const double* cb, int C, int2* rng, uint16_t* out) {
+  typedef cub::BlockScan<int, 128> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ double s_u[3], s_r, s_lim;
+  __shared__ double s_best[128];
+  __shared__ int s_cnt;
+  const int cell = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int face = cell / (R * R), i = (cell / R) % R, j = cell % R;
+    double u0 = -1.0 + 2.0 * i / R, u1 = -1.0 + 2.0 * (i + 1) / R;
+    double v0 = -1.0 + 2.0 * j / R, v1 = -1.0 + 2.0 * (j + 1) / R;
+    V3 c = normalized(cube_dir(face, 0.5 * (u0 + u1), 0.5 * (v0 + v1)));
+    double rho = 0.0;
+    double us[2] = {u0, u1}, vs[2] = {v0, v1};
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        double d = dot(c, normalized(cube_dir(face, us[a], vs[b])));
+        rho = fmax(rho, acos(fmin(1.0, fmax(-1.0, d))));
+      }
+    s_u[0] = c.x;
+    s_u[1] = c.y;
+    s_u[2] = c.z;
+    s_r = rho;
+    s_cnt = 0;
+  }
+  __syncthreads();
+  double mx = -2.0;  // nearest code to the centre: max dot
+  for (int k = threadIdx.x; k < C; k += blockDim.x) {
+    double nc = sqrt(cb[3 * k] * cb[3 * k] + cb[3 * k + 1] * cb[3 * k + 1] + cb[3 * k + 2] * cb[3 * k + 2]);
+    double d = (cb[3 * k] * s_u[0] + cb[3 * k + 1] * s_u[1] + cb[3 * k + 2] * s_u[2]) / nc;
+    mx = fmax(mx, d);
+  }
+  s_best[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = -2.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) m = fmax(m, s_best[t]);
+    double a = acos(fmin(1.0, fmax(-1.0, m)));
+    double lim = a + 2.0 * s_r + 1e-6;
+    s_lim = lim >= 3.141592653589793 ? -2.0 : cos(lim);
+  }
+  __syncthreads();
+  for (int base = 0; base < C; base += blockDim.x) {
+    int k = base + threadIdx.x;
+    int in = 0;
+    if (k < C) {
+      double nc = sqrt(cb[3 * k] * cb[3 * k] + cb[3 * k + 1] * cb[3 * k + 1] + cb[3 * k + 2] * cb[3 * k + 2]);
+      double d = (cb[3 * k] * s_u[0] + cb[3 * k + 1] * s_u[1] + cb[3 * k + 2] * s_u[2]) / nc;
+      in = d >= s_lim ? 1 : 0;
+    }
+    int pos, tot;
+    Scan(tmp).ExclusiveSum(in, pos, tot);
+    if (in && s_cnt + pos < lmax) out[(size_t)cell * lmax + s_cnt + pos] = (uint16_t)k;
+    __syncthreads();
+    if (threadIdx.x == 0) s_cnt += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rng[cell] = make_int2(cell * lmax, s_cnt <= lmax ? s_cnt : -1);
 }
 
 // Code-major reachability mask: bit g set iff some code c passes

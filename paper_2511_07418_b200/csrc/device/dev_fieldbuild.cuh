@@ -204,9 +204,17 @@ void build_field_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_de
   size_t cb_smem = 3 * (size_t)C * sizeof(double);
   if (cb_smem > 200 * 1024) throw std::invalid_argument("index build: codebook too large for the device build");
   CK(cudaFuncSetAttribute(k_field_vectors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb_smem));
+  // candidate-code lists for the quantizer's argmax (k_quantlist)
+  constexpr int QR = 16, QL = 64;
+  Buf qrng, qcodes;
+  int2* d_qrng = dalloc<int2>(qrng, 6 * QR * QR);
+  uint16_t* d_qcodes = dalloc<uint16_t>(qcodes, (size_t)6 * QR * QR * QL);
+  k_quantlist<<<6 * QR * QR, 128, 0, s>>>(QR, QL, d_cb, C, d_qrng, d_qcodes);
+  LAUNCH(ctx);
+  check_launch();
   k_field_vectors<<<grid_for(V, 256), 256, cb_smem, s>>>(
       N, P.F, P.fp_link.as<int>(), P.fp_point.as<int>(), P.pts.as<double>(), P.nrm.as<double>(),
-      d_frames, d_cb, C, w, d_cells, d_codes, d_cmm, d_cmm + 3);
+      d_frames, d_cb, C, w, QR, d_qrng, d_qcodes, d_cells, d_codes, d_cmm, d_cmm + 3);
   LAUNCH(ctx);
   check_launch();
   long long cmm_h[6];
