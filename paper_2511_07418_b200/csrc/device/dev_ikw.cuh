@@ -99,15 +99,18 @@ __device__ __forceinline__ void wchain_build(WChain& C, const int* tlink, int k,
         int t = tlink[i];
         for (int d = 0; d < g_hand.chain_len[t]; ++d) need |= g_hand.chain[t][d] == l;
       }
-      C.sol[l] = need ? m : -1;
-      if (need) {
+      // links with no joint on their chain (the palm) have constant frames:
+      // computed once (wchain_static), not per trial
+      const bool moving = need && g_hand.jmask[l] != 0u;
+      C.sol[l] = moving ? m : (need ? -2 - l : -1);
+      if (moving) {
         C.link[m] = l;
         C.lvl[m] = g_hand.level[l];
         maxl = C.lvl[m] > maxl ? C.lvl[m] : maxl;
         ++m;
       }
     }
-    for (int j = 0; j < m; ++j) {
+    for (int j = 0; j < m; ++j) {  // slot, -1 (no parent) or -2 - static parent link
       int p = g_hand.parent[C.link[j]];
       C.pslot[j] = p >= 0 ? C.sol[p] : -1;
     }
@@ -122,6 +125,28 @@ __device__ __forceinline__ void wchain_build(WChain& C, const int* tlink, int k,
   C.G = g > 4 ? 4 : g;
 }
 
+// Constant frames of the static chain links (no joint from the root) into
+// the link-indexed buffer F, in level order, by one lane.
+__device__ __forceinline__ void wchain_static(const int* tlink, int k, double* F, int lane) {
+  if (lane == 0) {
+    const int nl = c_hand.n_links;
+    for (int d = 0; d < c_hand.n_levels; ++d)
+      for (int l = 0; l < nl; ++l) {
+        if (g_hand.level[l] != d || g_hand.jmask[l] != 0u) continue;
+        bool need = false;
+        for (int i = 0; i < k; ++i) {
+          int t = tlink[i];
+          for (int e = 0; e < g_hand.chain_len[t]; ++e) need |= g_hand.chain[t][e] == l;
+        }
+        if (!need) continue;
+        Xf loc = link_local_v(l, 0.0);
+        int p = g_hand.parent[l];
+        st_xf(F + kFS * l, p < 0 ? loc : xf_compose(ld_xf(F + kFS * p), loc));
+      }
+  }
+  __syncwarp();
+}
+
 // Joint value of backtracking trial b: q + clamp(dq / 2^b) clamped to the
 // limits, dq halved b times as the sequential line search does.
 __device__ __forceinline__ double trial_joint(const double* q, const double* dq, int j, int b,
@@ -133,8 +158,9 @@ __device__ __forceinline__ double trial_joint(const double* q, const double* dq,
 
 // FK of the chain links for ng groups into FG[g][m][kFS]; group g uses trial
 // b0 + g, or q itself when b0 < 0 (one group).
-__device__ __forceinline__ void wchain_fk(const WChain& C, double* FG, int ng, const double* q,
-                                         const double* dq, int b0, double step_clamp, int lane) {
+__device__ __forceinline__ void wchain_fk(const WChain& C, double* FG, const double* F, int ng,
+                                         const double* q, const double* dq, int b0,
+                                         double step_clamp, int lane) {
   const bool on = lane < ng * C.m;
   const int g = on ? lane / C.m : 0, j = on ? lane - g * C.m : 0;
   Xf loc = xf_identity();
@@ -150,7 +176,9 @@ __device__ __forceinline__ void wchain_fk(const WChain& C, double* FG, int ng, c
   }
   double* Fg = FG + (size_t)g * C.m * kFS;
   for (int d = 0; d <= C.maxlvl; ++d) {
-    if (lv == d) st_xf(Fg + kFS * j, ps < 0 ? loc : xf_compose(ld_xf(Fg + kFS * ps), loc));
+    if (lv == d)
+      st_xf(Fg + kFS * j, ps == -1 ? loc
+                                   : xf_compose(ld_xf(ps >= 0 ? Fg + kFS * ps : F + kFS * (-2 - ps)), loc));
     __syncwarp();
   }
 }
@@ -358,7 +386,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
   if (lane < dof) q[lane] = dclamp(q[lane], g_hand.jlo[lane], g_hand.jhi[lane]);
   __syncwarp();
   used = 0ull;
-  wchain_fk(C, FG, 1, q, nullptr, -1, 0.0, lane);
+  wchain_fk(C, FG, F, 1, q, nullptr, -1, 0.0, lane);
   wchain_commit(C, FG, 0, F, lane);
   ++ctr.fk;
   if (k == 0) return true;
@@ -437,11 +465,12 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     const int rk = 6 * k;
     for (int b0 = 0; b0 <= P.max_backtracks && !moved; b0 += C.G) {
       const int ng = (P.max_backtracks + 1 - b0) < C.G ? (P.max_backtracks + 1 - b0) : C.G;
-      wchain_fk(C, FG, ng, q, ws.x, b0, P.step_clamp, lane);
+      wchain_fk(C, FG, F, ng, q, ws.x, b0, P.step_clamp, lane);
       ctr.fk += ng;
       if (lane < ng * k) {  // stacked_residual (ik.cpp:13-27) per group
         int g = lane / k, i = lane - g * k;
-        Xf Fl = ld_xf(FG + ((size_t)g * C.m + C.tslot[i]) * kFS);
+        const int ts = C.tslot[i];  // a static target link's frame is constant
+        Xf Fl = ld_xf(ts >= 0 ? FG + ((size_t)g * C.m + ts) * kFS : F + kFS * (-2 - ts));
         const double* tt = T.t + 12 * i;
         V3 op = v3_load(tt), on = v3_load(tt + 3);
         V3 hp = xf_apply(Fl, v3_load(tt + 6));
@@ -605,6 +634,7 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
   __syncwarp();
   wchain_build(C, T.link, kt, lane);
+  wchain_static(T.link, kt, F, lane);
   Ctr ctr = {0, 0, 0, 0, 0};
   double mr;
   unsigned long long u;
