@@ -310,6 +310,17 @@ void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
   CK(cudaMemcpyToSymbolAsync(g_hand, &h, sizeof(DHand), 0, cudaMemcpyHostToDevice, s));
 }
 
+// Kernel attributes are per device: set them the first time a (device,
+// kernel family) pair is launched in this process.
+bool first_on_device(int tag) {
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  return done.insert({dev, tag}).second;
+}
+
 // realize_grasp, one warp per problem, 4 warps per CTA.
 void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCfg& P, int rounds,
                          int fine_iters, const double* tgt, int tgt_stride, const int* tl,
@@ -318,11 +329,12 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
   const int wpb = 4;
   const int kmax = kk ? kMaxK : k;
   size_t smem = realize_warp_smem(dof, kmax, n_links, wpb);
-  static int minb = -1;
-  if (minb < 0) {
+  static const int minb = [] {
     const char* e = std::getenv("LG_REALIZE_MINB");
-    minb = e ? std::atoi(e) : 5;  // 5 CTAs/SM (96 regs) measured fastest
-    if (minb != 4 && minb != 6) minb = 5;
+    int v = e ? std::atoi(e) : 5;  // 5 CTAs/SM (96 regs) measured fastest
+    return (v == 4 || v == 6) ? v : 5;
+  }();
+  if (first_on_device(1)) {
     CK(cudaFuncSetAttribute(k_realize_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_realize_warp<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_realize_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -792,10 +804,11 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     co.per_restart = per_restart;
     co.per_cand = per_cand;
     int nw = std::min(R, 4);
-    static int co_minb = -1;
-    if (co_minb < 0) {
+    static const int co_minb = [] {
       const char* e = std::getenv("LG_COPT_MINB");
-      co_minb = (e && std::atoi(e) == 5) ? 5 : 4;
+      return (e && std::atoi(e) == 5) ? 5 : 4;
+    }();
+    if (first_on_device(2)) {
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
