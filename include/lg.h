@@ -17,8 +17,11 @@
  *   - input arrays are caller-owned and copied in; output arrays are either
  *     library-owned (valid until the owning handle is destroyed) or caller
  *     buffers with an explicit capacity;
- *   - one in-flight call per lg_ctx; there is no CPU fallback: on a machine
- *     without a CUDA device every device entry point returns LG_ERR_CUDA.
+ *   - one in-flight call per lg_ctx, and one in-flight device call per GPU:
+ *     the hand description is bound to the device's constant bank for the
+ *     call (one context per GPU, as the multi-GPU driver uses them);
+ *   - there is no CPU fallback: on a machine without a CUDA device every
+ *     device entry point returns LG_ERR_CUDA.
  *
  * Arrays of 3-vectors are row-major [n][3]; rotations are row-major 3x3;
  * object samples are [n][6] = (position xyz, unit outward normal xyz).
