@@ -180,7 +180,7 @@ template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
-               const double* el_xs, const int* el_ix, int sorted_min, const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
+               const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
                double* out_sol, double eps_stable, int* balanced) {
   extern __shared__ __align__(16) double s_co[];
   const int a = blockIdx.x;
@@ -267,109 +267,73 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               box_muller(d2[0], d2[1], &z1, &z2);
               V3 cp = axpy(axpy(cur_p, cfg.sigma * z1, tx), cfg.sigma * z2, ty);
               // project_to_domain (contact_opt.cpp:11-25): nearest element,
-              // first index among equal distances.
+              // first index among equal distances.  Every lane scans the same
+              // elements (broadcast loads, no divergence); pruned searches
+              // (x-sorted, object-frame grid) evaluate far fewer distances but
+              // diverge and measured slower.
               const double* P = el_p + 3 * off[q];
               const int ne = (int)cnt[q];
               double bd;
               int bi;
               unsigned long long visited;
-              if (el_xs && ne >= sorted_min) {
-                // Large domain (warp-uniform branch): visit elements in order
-                // of |x - cp.x| from the domain's x-sorted index.  An element
-                // whose exact first distance term (P.x - cp.x)^2 exceeds the
-                // best distance cannot reach it ((a + b) + c >= a for b, c >=
-                // 0), so the scan stops there with the serial scan's
-                // (distance, index) minimum.
-                const double* xs = el_xs + off[q];
-                const int* ix = el_ix + off[q];
-                int lo = 0, hi = ne;  // first xs >= cp.x
-                while (lo < hi) {
-                  int mid = (lo + hi) >> 1;
-                  if (xs[mid] < cp.x) lo = mid + 1;
-                  else hi = mid;
+              // Every lane scans the same elements (broadcast loads, no
+              // divergence): faster than the pruned search for domains of
+              // a few thousand elements.
+              bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
+              bi = 0;
+              int e = 1;
+              // peel to an even global element (16-byte aligned pairs)
+              if (e < ne && ((off[q] + e) & 1)) {
+                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                if (d2v < bd) {
+                  bd = d2v;
+                  bi = e;
                 }
-                int r = lo, l = lo - 1;
-                bd = kInf;
-                bi = 0x7fffffff;
-                visited = 0;
-                while (r < ne || l >= 0) {
-                  double ar = r < ne ? xs[r] - cp.x : kInf;
-                  double al = l >= 0 ? xs[l] - cp.x : kInf;
-                  double tr = ar * ar, tl = al * al;
-                  bool right = l < 0 || (r < ne && tr <= tl);
-                  if ((right ? tr : tl) > bd) break;
-                  int e = right ? ix[r++] : ix[l--];
-                  double dv = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                  ++visited;
-                  if (dv < bd || (dv == bd && e < bi)) {
-                    bd = dv;
-                    bi = e;
-                  }
-                }
-                if (bi == 0x7fffffff) bi = -1;  // non-finite query: serial scan below
-              } else {
-                bi = -1;
+                ++e;
               }
-              if (bi < 0) {
-                // Every lane scans the same elements (broadcast loads, no
-                // divergence): faster than the pruned search for domains of
-                // a few thousand elements.
-                bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
-                bi = 0;
-                int e = 1;
-                // peel to an even global element (16-byte aligned pairs)
-                if (e < ne && ((off[q] + e) & 1)) {
-                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                  if (d2v < bd) {
-                    bd = d2v;
-                    bi = e;
-                  }
-                  ++e;
-                }
-                // eight independent distances in flight (twelve 16-byte
-                // loads: the domain streams from L2), compared in index order
-                for (; e + 8 <= ne; e += 8) {
-                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
-                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
-                  double2 b0 = Q[6], b1 = Q[7], b2 = Q[8], b3 = Q[9], b4 = Q[10], b5 = Q[11];
-                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
-                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
-                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
-                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
-                  double d4 = sqnorm(sub(v3(b0.x, b0.y, b1.x), cp));
-                  double d5 = sqnorm(sub(v3(b1.y, b2.x, b2.y), cp));
-                  double d6 = sqnorm(sub(v3(b3.x, b3.y, b4.x), cp));
-                  double d7 = sqnorm(sub(v3(b4.y, b5.x, b5.y), cp));
-                  if (d0 < bd) { bd = d0; bi = e; }
-                  if (d1 < bd) { bd = d1; bi = e + 1; }
-                  if (d2 < bd) { bd = d2; bi = e + 2; }
-                  if (d3 < bd) { bd = d3; bi = e + 3; }
-                  if (d4 < bd) { bd = d4; bi = e + 4; }
-                  if (d5 < bd) { bd = d5; bi = e + 5; }
-                  if (d6 < bd) { bd = d6; bi = e + 6; }
-                  if (d7 < bd) { bd = d7; bi = e + 7; }
-                }
-                for (; e + 4 <= ne; e += 4) {
-                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
-                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
-                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
-                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
-                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
-                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
-                  if (d0 < bd) { bd = d0; bi = e; }
-                  if (d1 < bd) { bd = d1; bi = e + 1; }
-                  if (d2 < bd) { bd = d2; bi = e + 2; }
-                  if (d3 < bd) { bd = d3; bi = e + 3; }
-                }
-                for (; e < ne; ++e) {
-                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                  if (d2v < bd) {
-                    bd = d2v;
-                    bi = e;
-                  }
-                }
-                visited = (unsigned long long)ne;
+              // eight independent distances in flight (twelve 16-byte
+              // loads: the domain streams from L2), compared in index order
+              for (; e + 8 <= ne; e += 8) {
+                const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                double2 b0 = Q[6], b1 = Q[7], b2 = Q[8], b3 = Q[9], b4 = Q[10], b5 = Q[11];
+                double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
+                double d4 = sqnorm(sub(v3(b0.x, b0.y, b1.x), cp));
+                double d5 = sqnorm(sub(v3(b1.y, b2.x, b2.y), cp));
+                double d6 = sqnorm(sub(v3(b3.x, b3.y, b4.x), cp));
+                double d7 = sqnorm(sub(v3(b4.y, b5.x, b5.y), cp));
+                if (d0 < bd) { bd = d0; bi = e; }
+                if (d1 < bd) { bd = d1; bi = e + 1; }
+                if (d2 < bd) { bd = d2; bi = e + 2; }
+                if (d3 < bd) { bd = d3; bi = e + 3; }
+                if (d4 < bd) { bd = d4; bi = e + 4; }
+                if (d5 < bd) { bd = d5; bi = e + 5; }
+                if (d6 < bd) { bd = d6; bi = e + 6; }
+                if (d7 < bd) { bd = d7; bi = e + 7; }
               }
+              for (; e + 4 <= ne; e += 4) {
+                const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
+                if (d0 < bd) { bd = d0; bi = e; }
+                if (d1 < bd) { bd = d1; bi = e + 1; }
+                if (d2 < bd) { bd = d2; bi = e + 2; }
+                if (d3 < bd) { bd = d3; bi = e + 3; }
+              }
+              for (; e < ne; ++e) {
+                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                if (d2v < bd) {
+                  bd = d2v;
+                  bi = e;
+                }
+              }
+              visited = (unsigned long long)ne;
               ctr.proj += visited;
               cand = bi;
               const long long eg = off[q] + bi;

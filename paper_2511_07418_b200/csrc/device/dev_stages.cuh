@@ -451,8 +451,7 @@ __global__ void k_group_pick(int Bl, int c_lo, int B, int pass, uint64_t seed, i
 // scan over the mask row.  Writes sample id, position and normal (SoA).
 __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* chosen,
                               const uint32_t* mask, DSamples fs, const double* pose,
-                              const long long* el_off, int* el_s, double* el_p, double* el_n,
-                              double* el_x, int* el_i) {
+                              const long long* el_off, int* el_s, double* el_p, double* el_n) {
   typedef cub::BlockScan<int, 256> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
@@ -481,10 +480,6 @@ __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* ch
       el_n[3 * e] = n.x;
       el_n[3 * e + 1] = n.y;
       el_n[3 * e + 2] = n.z;
-      if (el_x) {  // sort key / value of the large-domain projection index
-        el_x[e] = p.x;
-        el_i[e] = s_base + pos;
-      }
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base += total;

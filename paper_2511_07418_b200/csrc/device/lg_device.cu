@@ -753,35 +753,10 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     int* d_els = dalloc<int>(b_els, (size_t)nel);
     double* d_elp = dalloc<double>(b_elp, 3 * (size_t)nel);
     double* d_eln = dalloc<double>(b_eln, 3 * (size_t)nel);
-    // Optional x-sorted projection index (stable segmented sort of (x, local
-    // index)) for domains of >= LG_PROJ_SORTED_MIN elements; the contact
-    // search then prunes its nearest-element scan on them.  Off by default:
-    // the divergent pruned scan measured slower than the broadcast brute
-    // force both on 870-element domains (Allegro, 111 vs 53 ms) and on
-    // 50k-element ones (Shadow/113k samples, 2.8 s vs 0.6 s per 2k seeds).
-    const char* sm_env = std::getenv("LG_PROJ_SORTED_MIN");
-    const int kSortedMin = sm_env ? std::max(1, std::atoi(sm_env)) : 0x7fffffff;
-    long long max_dom = 0;
-    for (size_t d = 0; d + 1 < eloff.size(); ++d) max_dom = std::max(max_dom, eloff[d + 1] - eloff[d]);
-    const bool sorted_idx = max_dom >= kSortedMin;
-    Buf b_elx, b_eli, b_elxs, b_elix;
-    double* d_elx = sorted_idx ? dalloc<double>(b_elx, (size_t)nel) : nullptr;
-    int* d_eli = sorted_idx ? dalloc<int>(b_eli, (size_t)nel) : nullptr;
-    double* d_elxs = sorted_idx ? dalloc<double>(b_elxs, (size_t)nel) : nullptr;
-    int* d_elix = sorted_idx ? dalloc<int>(b_elix, (size_t)nel) : nullptr;
     k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
-                                         d_elp, d_eln, d_elx, d_eli);
+                                         d_elp, d_eln);
     LAUNCH(ctx);
     check_launch();
-    if (sorted_idx) {
-      size_t bytes = 0;
-      CK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, d_elx, d_elxs, d_eli, d_elix,
-                                                   (int)nel, nA * k, d_eloff, d_eloff + 1, s));
-      void* tmp = ctx->tmp(bytes);
-      CK(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, d_elx, d_elxs, d_eli, d_elix,
-                                                   (int)nel, nA * k, d_eloff, d_eloff + 1, s));
-      LAUNCH(ctx);
-    }
     Buf b_draws, b_oid, b_oobj, b_oan, b_osol, b_bal;
     uint64_t* d_draws = dalloc<uint64_t>(b_draws, (size_t)nA * per_cand);
     k_copt_draws<<<grid_for(nA, 64), 64, 0, s>>>(nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, d_draws);
@@ -827,8 +802,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                               : k_contact_opt2<kMaxC, 4>;
     size_t co_smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
     co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln,
-                                         d_elxs, d_elix, kSortedMin, d_draws, d_oid, d_oobj, d_oan,
-                                         d_osol, cfg.eps_stable, d_bal);
+                                         d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
+                                         d_bal);
     LAUNCH(ctx);
     check_launch();
     copt_s += tk.stop();

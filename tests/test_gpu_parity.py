@@ -213,20 +213,6 @@ def test_run_batch_synthetic_hands_bit_exact(args):
     assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
 
 
-@pytest.mark.parametrize("case", [dict(batch=96), dict(batch=64, hand="two_finger")])
-def test_sorted_projection_path_bit_exact(case, monkeypatch):
-    """The optional x-sorted pruned nearest-element search (LG_PROJ_SORTED_MIN)
-    forced onto every domain: identical stage traces."""
-    monkeypatch.setenv("LG_PROJ_SORTED_MIN", "1")
-    case = dict(case)
-    p = cfg1(batch=case.pop("batch"), **case)
-    dev, ref = _run_both(p)
-    for k in FUNNEL:
-        assert dev.profile[k] == ref.profile[k], k
-    assert mismatched_fields(dev.traces, ref.traces) == {}
-    assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
-
-
 def _patch_arrays(pt):
     d = pt.desc
     P = d.n_patches
