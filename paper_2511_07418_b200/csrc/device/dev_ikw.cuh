@@ -152,6 +152,7 @@ __device__ __forceinline__ void wchain_static(const int* tlink, int k, double* F
 __device__ __forceinline__ double trial_joint(const double* q, const double* dq, int j, int b,
                                               double step_clamp) {
   double d = dq[j];
+  #pragma unroll 1
   for (int h = 0; h < b; ++h) d *= 0.5;
   return dclamp(q[j] + dmin(dmax(d, -step_clamp), step_clamp), g_hand.jlo[j], g_hand.jhi[j]);
 }
@@ -232,6 +233,7 @@ __device__ __forceinline__ double wresidual(const double* F, const WTargets& T, 
   __syncwarp();
   double s = 0.0;
   if (lane == 0)
+    #pragma unroll 1
     for (int i = 0; i < 6 * k; ++i) s = s + r[i] * r[i];
   return __shfl_sync(kFull, s, 0);
 }
@@ -339,6 +341,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     __syncwarp();
   }
   if (lane == 0)
+    #pragma unroll 1
     for (int k = 0; k < n; ++k) {
       double t = x[k];
       x[k] = x[tr[k]];
@@ -366,6 +369,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
   if (lane < n) x[lane] = xi;
   __syncwarp();
   if (lane == 0)
+    #pragma unroll 1
     for (int k = n - 1; k >= 0; --k) {
       double t = x[k];
       x[k] = x[tr[k]];
@@ -448,6 +452,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     __syncwarp();
     double tr = 0.0;
     if (lane == 0)
+      #pragma unroll 1
       for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * ld + a];
     tr = __shfl_sync(kFull, tr, 0);
     double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
@@ -488,6 +493,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       __syncwarp();
       double obj_try = 0.0;
       if (lane < ng)
+        #pragma unroll 1
         for (int i = 0; i < rk; ++i) obj_try = obj_try + rtG[lane * rk + i] * rtG[lane * rk + i];
       unsigned accm = __ballot_sync(kFull, lane < ng && obj_try <= objective);
       if (accm) {
