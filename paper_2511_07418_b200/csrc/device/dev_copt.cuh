@@ -91,8 +91,10 @@ __device__ __forceinline__ void acc_contact(const double* s, double a, double bx
 template <bool FR, int NC>
 __device__ double pv_descend(const PV& w, int anchor, int iterations, double step0, int max_bt,
                              double* a, double* bx, double* by, double* tr, Ctr& ctr) {
+  #pragma unroll 1
   for (int i = 0; i < w.n; ++i) proj_one<FR>(i == anchor, w.mu, a[i], bx[i], by[i]);
   V3 f = v3(0.0, 0.0, 0.0), t = v3(0.0, 0.0, 0.0);
+  #pragma unroll 1
   for (int i = 0; i < w.n; ++i) acc_contact<FR>(w.slot(i), a[i], bx[i], by[i], f, t);
   double current = sqnorm(f) + w.lambda * sqnorm(t);
   ++ctr.weval;
@@ -110,6 +112,7 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
     bool moved = false;
     for (int bt = 0; bt <= max_bt; ++bt) {
       V3 f2 = v3(0.0, 0.0, 0.0), t2 = v3(0.0, 0.0, 0.0);
+      #pragma unroll 1
       for (int i = 0; i < w.n; ++i) {
         const double* s = w.slot(i);
         double xa = a[i] - step * (2.0 * (dot(force, ld3(s + 3)) + dot(torque, ld3(s + 12))));
@@ -127,6 +130,7 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
       double next = sqnorm(f2) + w.lambda * sqnorm(t2);
       ++ctr.weval;
       if (next <= current) {
+        #pragma unroll 1
         for (int i = 0; i < w.n; ++i) {
           a[i] = ta[i];
           bx[i] = tbx[i];
@@ -154,6 +158,7 @@ __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts
   double* a = st;
   double* bx = st + NC;
   double* by = st + 2 * NC;
+  #pragma unroll 1
   for (int i = 0; i < w.n; ++i) {
     a[i] = warm ? warm[i] : 1.0;
     bx[i] = warm ? warm[NC + i] : 0.0;
