@@ -97,6 +97,7 @@ __device__ __forceinline__ void wchain_build(WChain& C, const int* tlink, int k,
       bool need = false;
       for (int i = 0; i < k; ++i) {
         int t = tlink[i];
+        #pragma unroll 1
         for (int d = 0; d < g_hand.chain_len[t]; ++d) need |= g_hand.chain[t][d] == l;
       }
       // links with no joint on their chain (the palm) have constant frames:
@@ -136,6 +137,7 @@ __device__ __forceinline__ void wchain_static(const int* tlink, int k, double* F
         bool need = false;
         for (int i = 0; i < k; ++i) {
           int t = tlink[i];
+          #pragma unroll 1
           for (int e = 0; e < g_hand.chain_len[t]; ++e) need |= g_hand.chain[t][e] == l;
         }
         if (!need) continue;
@@ -331,6 +333,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
       if (lane >= k && lane < n) {
         double acc = 0.0;
         const double* row = A + lane * ld;
+        #pragma unroll 2
         for (int j = 0; j < k; ++j) acc = acc + row[j] * tmp[j];
         A[lane * ld + k] -= acc;  // lane k: A(k,k); lanes > k: A21
       }
@@ -440,12 +443,14 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       }
       int b = a + rem;
       double s = 0.0;
+      #pragma unroll 2
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
       ws.A[a * ld + b] = s;
       ws.A[b * ld + a] = s;
     }
     if (lane < dof) {
       double s = 0.0;
+      #pragma unroll 1
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + lane] * r[rr];
       ws.x[lane] = s;
     }
@@ -552,6 +557,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
   for (int round = -1; round < rounds; ++round) {
     const bool init = round < 0;
     if (!init) {
+      #pragma unroll 1
       for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
       if (lane < k) Ref.link[lane] = T.link[lane];
       __syncwarp();
@@ -635,6 +641,7 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   C.tslot = C.sol + kMaxLinks;
   C.hdr = C.tslot + kMaxK;
   const double* src = tgt + (size_t)t * tgt_stride;
+  #pragma unroll 1
   for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
   if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
   if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
