@@ -34,7 +34,7 @@ struct PV {
 __device__ __forceinline__ V3 ld3(const double* p) { return v3(p[0], p[1], p[2]); }
 
 // write_slot (contact_opt.cpp:31-35) into a 21-double slot record.
-__device__ __forceinline__ void slot_make(double* o, V3 p, V3 n) {
+__device__ __noinline__ void slot_make(double* o, V3 p, V3 n) {
   V3 tx, ty;
   tangent_basis(n, tx, ty);
   V3 cn = cross(p, n), cx = cross(p, tx), cy = cross(p, ty);
@@ -217,6 +217,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
     if (r < cfg.restarts) {
       const uint64_t* D = draws + (size_t)a * cfg.per_cand + (size_t)r * cfg.per_restart;
       int ids[kMaxK];
+      #pragma unroll 1
       for (int q = 0; q < k; ++q) ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
       if (lane < k) {
         long long e = off[lane] + ids[lane];
@@ -397,6 +398,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
         double* R = res + warp * rstride;
         R[0] = obj;
         R[1] = (double)anchor;
+        #pragma unroll 1
         for (int q = 0; q < k; ++q) R[2 + q] = (double)ids[q];
         for (int c = 0; c < 3 * NC; ++c) R[2 + k + c] = anchor >= 0 ? inc[c] : 0.0;
       }
@@ -421,6 +423,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
     int an = (int)best[1];
     if (!(best[0] < kInf)) an = -1;
     out_anchor[a] = an;
+    #pragma unroll 1
     for (int q = 0; q < k; ++q) out_ids[a * kMaxK + q] = (int)best[2 + q];
     for (int c = 0; c < 3 * kMaxC; ++c) {
       int comp = c / kMaxC, ci = c % kMaxC;  // output keeps the [3][kMaxC] layout
