@@ -178,6 +178,7 @@ __device__ __forceinline__ void wchain_fk(const WChain& C, double* FG, const dou
     ps = C.pslot[j];
   }
   double* Fg = FG + (size_t)g * C.m * kFS;
+  #pragma unroll 1
   for (int d = 0; d <= C.maxlvl; ++d) {
     if (lv == d)
       st_xf(Fg + kFS * j, ps == -1 ? loc
@@ -275,6 +276,7 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
 // x (smem) rhs in / solution out.
 __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, int* tr,
                                             double* tmp, int lane) {
+  #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     // pivot = first index of max |A(i,i)|, i >= k.  Non-negative doubles
     // order like their bit patterns, so the max is two 32-bit warp
@@ -353,6 +355,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
   __syncwarp();
   double xi = lane < n ? x[lane] : 0.0;
   double s = 0.0;
+  #pragma unroll 1
   for (int j = 0; j < n; ++j) {  // forward: L unit lower
     double xj = __shfl_sync(kFull, xi - s, j);
     if (lane == j) xi = xj;
@@ -364,6 +367,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     else xi = 0.0;
   }
   s = 0.0;
+  #pragma unroll 1
   for (int j = n - 1; j >= 0; --j) {  // backward: L^T
     double xj = __shfl_sync(kFull, xi - s, j);
     if (lane == j) xi = xj;
@@ -418,6 +422,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       V3 axis = mul(Fj.R, v3_load(g_hand.axis[lj]));
       bool rev = g_hand.jtype[lj] == 1;
       double cm = 0.0;
+      #pragma unroll 1
       for (int p = 0; p < 2 * k; ++p) {
         bool on = (c_hand.jmask[T.link[p >> 1]] >> lane) & 1u;
         V3 col = v3(0.0, 0.0, 0.0);
