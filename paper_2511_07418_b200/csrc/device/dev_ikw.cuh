@@ -335,7 +335,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
       if (lane >= k && lane < n) {
         double acc = 0.0;
         const double* row = A + lane * ld;
-        #pragma unroll 2
+        #pragma unroll 4
         for (int j = 0; j < k; ++j) acc = acc + row[j] * tmp[j];
         A[lane * ld + k] -= acc;  // lane k: A(k,k); lanes > k: A21
       }
@@ -448,7 +448,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       }
       int b = a + rem;
       double s = 0.0;
-      #pragma unroll 2
+      #pragma unroll 4
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
       ws.A[a * ld + b] = s;
       ws.A[b * ld + a] = s;
