@@ -7,12 +7,6 @@
 
 namespace lgd {
 
-struct Target {
-  V3 op, on;  // object point, inward normal (base frame)
-  int link;
-  V3 hp, hn;  // hand point / outward normal (link frame)
-};
-
 struct IkCfg {
   double beta, step_clamp, residual_tol, damping_scale, damping_min;
   int iterations, max_backtracks;
