@@ -576,6 +576,8 @@ def wrench_solve_batch(ctx, problems, lambda_torque=10.0, mu=0.0, gswo=None, ite
     L = _bind_batch_sigs()
     m = len(problems)
     n = np.array([len(p[0]) for p in problems], dtype=np.int32)
+    if m and (n.min() < 1 or n.max() > 6):
+        raise ValueError("wrench solve: 1..6 contacts")  # as the C-ABI reports it
     pts = np.zeros((m, 6, 3))
     nrm = np.zeros((m, 6, 3))
     for i, (p, q) in enumerate(problems):

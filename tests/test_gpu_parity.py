@@ -238,3 +238,22 @@ def test_patches_device_identical(ctx, hand_name, spc, radius, cap):
     b = _patch_arrays(lg.hand_patches_device(ctx, hand, spc, radius, 7, cap))
     for k in a:
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_device_errors_map_to_reference_exceptions(ctx, four_finger):
+    """Bad arguments raise the reference's exception class with its message
+    (ValueError <- std::invalid_argument) instead of running (SURVEY 8(b))."""
+    p = cfg1(batch=8)
+    hand, patches, raw, _ = lg.prepare_inputs(p)
+    p.k_contacts = 9
+    with pytest.raises(ValueError, match="k_contacts"):
+        lg.run_batch(ctx, hand, patches, raw, p)
+    with pytest.raises(ValueError, match="box width"):
+        lg.ContactFieldIndex.build(ctx, hand, patches, 16, 0.0, 0, 64)
+    with pytest.raises(ValueError, match="1..6 contacts"):
+        lg.api.wrench_solve_batch(ctx, [(np.zeros((7, 3)), np.tile([0.0, 0.0, 1.0], (7, 1)))])
+    with pytest.raises(ValueError, match="no samples|stripped|no object samples"):
+        lg.run_batch(ctx, hand, patches, np.zeros((0, 6)), cfg1(batch=8))
+    # the context stays usable after an error
+    ok = lg.run_batch(ctx, hand, patches, raw, cfg1(batch=8))
+    assert ok.profile["candidates"] == 8
