@@ -257,3 +257,25 @@ def test_device_errors_map_to_reference_exceptions(ctx, four_finger):
     # the context stays usable after an error
     ok = lg.run_batch(ctx, hand, patches, raw, cfg1(batch=8))
     assert ok.profile["candidates"] == 8
+
+
+def test_bench_config_against_oracle_shard():
+    """The bench workload itself (Allegro-class hand, 5 cm box, 10k seeds):
+    the device's full batch, compared candidate by candidate with the
+    oracle's re-run of one 1/40 shard (field built by each side)."""
+    import bench
+    p = bench.params_for("allegro_box")
+    p.want_trace = 1
+    hand, patches, raw, _ = lg.prepare_inputs(p)
+    ctx = lg.Context(0)
+    dev = lg.run_batch(ctx, hand, patches, raw, p)
+    ctx.close()
+    from paper_2511_07418_b200 import dist as ldist
+    sp = ldist.shard_params(p, 7, 40)
+    ref = orc.run_batch(hand.desc, patches.desc, raw, sp, workers=0)
+    lo, hi = ldist.shard_range(p.batch, 7, 40)
+    sub = dev.traces[(dev.traces["c"] >= lo) & (dev.traces["c"] < hi)]
+    assert len(sub) == hi - lo
+    assert mismatched_fields(sub, ref.traces) == {}
+    gsub = dev.grasps[(dev.grasps["g"] >= lo) & (dev.grasps["g"] < hi)]
+    assert mismatched_fields(gsub, ref.grasps, GRASP_FIELDS) == {}
