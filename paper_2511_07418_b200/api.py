@@ -429,17 +429,22 @@ class ContactFieldIndex:
         )
 
 
-def query_domains_batch(ctx, field, group_of_patch, samples, poses, theta_hit):
+def query_domains_batch(ctx, field, group_of_patch, samples, poses, theta_hit,
+                        with_scores=False):
     """query_domains (contact_field.cpp:380-448) for m poses: reachability
-    masks (m, n) uint32, bit g = sample is an element of group g's domain."""
+    masks (m, n) uint32, bit g = sample is an element of group g's domain;
+    with_scores also returns the element scores (m, n) (max over the
+    sample's elements, 0 without one)."""
     s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
     p = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 12)
     g = np.ascontiguousarray(group_of_patch, dtype=np.int32)
     masks = np.zeros((len(p), len(s)), dtype=np.uint32)
+    scores = np.zeros((len(p), len(s))) if with_scores else None
     check(lib().lg_query_domains_batch(ctx._h, field._h, _ip(g), _dp(s), len(s), _dp(p), len(p),
                                        float(theta_hit),
-                                       masks.ctypes.data_as(C.POINTER(C.c_uint32)), None))
-    return masks
+                                       masks.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                       _dp(scores) if with_scores else None))
+    return (masks, scores) if with_scores else masks
 
 
 def preprocess_object(ctx, samples, probe_half_width, depth_threshold):

@@ -391,6 +391,38 @@ k_query3(int Bl, DField f, DSamples fs, const double* pose, const int* accepted,
   for (int g = threadIdx.x; g < G; g += blockDim.x) dom_count[i * G + g] = s_cnt[g];
 }
 
+// Element scores of query_domains (contact_field.cpp:412-445) for
+// lg_query_domains_batch's optional output: per (pose, sample) the max over
+// the sample's domain elements of their score = max over hit boxes of the
+// box's best code score (0 without a hit).  Maxima are order independent.
+__global__ void k_query_scores(int m, DField f, const int* group_of_patch, DSamples fs,
+                               const double* pose, double theta, double* scores) {
+  const int i = blockIdx.x;
+  if (i >= m) return;
+  const Xf x = load_xf(pose + 12 * i);
+  for (int j = threadIdx.x; j < fs.n; j += blockDim.x) {
+    V3 p = xf_apply(x, fs.p(j));
+    V3 n = xf_rotate(x, fs.nrm(j));
+    long long c[3];
+    cell_of(p, f.w, c);
+    int r = find_run(f, c);
+    double sc = 0.0;
+    if (r >= 0)
+      for (int t = f.run_start[r]; t < f.run_start[r] + f.run_count[r]; ++t) {
+        int b = f.cell_box[t];
+        if (group_of_patch[f.box_patch[b]] < 0) continue;
+        double best = -2.0;
+        for (long long q = f.box_code_off[b]; q < f.box_code_off[b + 1]; ++q) {
+          int code = f.codes[q];
+          best = dmax(best, -dot(v3(f.codebook[3 * code], f.codebook[3 * code + 1],
+                                    f.codebook[3 * code + 2]), n));
+        }
+        if (best >= theta) sc = dmax(sc, best);
+      }
+    scores[(size_t)i * fs.n + j] = sc;
+  }
+}
+
 // Per-candidate world AABB of the raw object samples (the broad-phase
 // object box of validate_grasp_collisions, collision.cpp:243-245).
 __global__ void k_obj_aabb(int Bl, DSamples raw, const double* pose, const int* accepted,

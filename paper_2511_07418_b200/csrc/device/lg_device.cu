@@ -1541,8 +1541,14 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
       k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
     check_launch();
     CK(cudaMemcpyAsync(masks, d_mask, sizeof(uint32_t) * m * n, cudaMemcpyDeviceToHost, s));
+    if (scores) {
+      Buf bsc;
+      double* d_sc = dalloc<double>(bsc, (size_t)m * n);
+      k_query_scores<<<m, 256, 0, s>>>(m, f->f, d_g, S, d_pose, theta, d_sc);
+      check_launch();
+      CK(cudaMemcpyAsync(scores, d_sc, sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
-    (void)scores;
   });
 }
 

@@ -45,11 +45,12 @@ def test_query_masks_bit_exact(ctx, four_finger):
     gl, _ = hand.groups()
     gop = gl[patches.link_of_patch()]
     poses = _poses(24)
-    md = lg.query_domains_batch(ctx, f, gop, raw, poses, p.theta_hit)
+    md, sd = lg.query_domains_batch(ctx, f, gop, raw, poses, p.theta_hit, with_scores=True)
     total = 0
     for i, pose in enumerate(poses):
-        mo, _, _ = fo.query(hand.desc, raw, pose, p.theta_hit)
+        mo, so, _ = fo.query(hand.desc, raw, pose, p.theta_hit)
         assert np.array_equal(md[i], mo), i
+        assert np.array_equal(sd[i], so), i  # element scores (contact_field.cpp:443)
         total += int((mo != 0).sum())
     assert total > 0
     # theta_hit = 1.0 admits no hit: empty domains everywhere
