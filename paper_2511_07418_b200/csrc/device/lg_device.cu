@@ -841,7 +841,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     mark("stage2");
     // -------- stage 3: lookup attempts (reverse lookup + realize + filter)
     tm.start();
-    Buf b_have, b_bclear, b_bres, b_bq, b_bused, b_btgt, b_blink, b_batt, b_search, b_runs;
+    Buf b_have, b_bclear, b_bres, b_bq, b_bused, b_btgt, b_blink, b_batt, b_runs;
     int* d_have = dalloc<int>(b_have, (size_t)nA);
     int* d_bclear = dalloc<int>(b_bclear, (size_t)nA);
     double* d_bres = dalloc<double>(b_bres, (size_t)nA);
@@ -850,12 +850,10 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     double* d_btgt = dalloc<double>(b_btgt, (size_t)nA * kMaxK * 12);
     int* d_blink = dalloc<int>(b_blink, (size_t)nA * kMaxK);
     int* d_batt = dalloc<int>(b_batt, (size_t)nA);
-    int* d_search = dalloc<int>(b_search, (size_t)nA);
     CK(cudaMemsetAsync(d_have, 0, sizeof(int) * nA, s));
     CK(cudaMemsetAsync(d_bclear, 0, sizeof(int) * nA, s));
     CK(cudaMemsetAsync(d_bq, 0, sizeof(double) * nA * kMaxDof, s));
     CK(cudaMemsetAsync(d_batt, 0xff, sizeof(int) * nA, s));
-    (void)d_search;
     Buf b_bal_l, b_tgt, b_tl, b_qt, b_res, b_fin, b_used, b_clean, b_on, b_cand, b_err, b_runs_d;
     int* d_err = dalloc<int>(b_err, 1);
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
