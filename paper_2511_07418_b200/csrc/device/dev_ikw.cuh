@@ -559,14 +559,17 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
   double q0 = lane < dof ? q[lane] : 0.0;
   unsigned long long used = 0ull;
   double worst = 0.0;
+  // Ref = T with refreshed hand points.  The refresh at the start of a round
+  // projects at frames(q) exactly as the previous round's (or the initial)
+  // evaluation does, so that evaluation writes the refreshed points and the
+  // round starts from them (a rejected evaluation ends the loop).
+  #pragma unroll 1
+  for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
+  if (lane < k) Ref.link[lane] = T.link[lane];
+  __syncwarp();
   for (int round = -1; round < rounds; ++round) {
     const bool init = round < 0;
     if (!init) {
-      #pragma unroll 1
-      for (int a = lane; a < 12 * k; a += 32) Ref.t[a] = T.t[a];
-      if (lane < k) Ref.link[lane] = T.link[lane];
-      __syncwarp();
-      wproject(Fa, T, k, &Ref, lane);
       if (lane < dof) qs[lane] = q[lane];
       __syncwarp();
     }
@@ -582,7 +585,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
       *used_out = 0ull;
       return false;
     }
-    double w = wproject(Fa, T, k, nullptr, lane);
+    double w = wproject(Fa, T, k, &Ref, lane);
     if (init) {
       worst = w;
       used = su;
