@@ -390,15 +390,20 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
 // joints with a nonzero column.
 __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
                     unsigned long long& used, WarpWs& ws, double* F, const WChain& C, double* FG,
-                    double* rtG, Ctr& ctr, int lane) {
+                    double* rtG, bool have_frames, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   const int ld = dof | 1;  // odd row stride: column accesses hit distinct banks
   const int rows = 6 * k;
   if (lane < dof) q[lane] = dclamp(q[lane], g_hand.jlo[lane], g_hand.jhi[lane]);
   __syncwarp();
   used = 0ull;
-  wchain_fk(C, FG, F, 1, q, nullptr, -1, 0.0, lane);
-  wchain_commit(C, FG, 0, F, lane);
+  // A finetune round starts at the accepted q whose chain frames F already
+  // holds (same FK, same inputs), and q is within its limits, so the clamp
+  // above is the identity; only the first solve needs the FK.
+  if (!have_frames) {
+    wchain_fk(C, FG, F, 1, q, nullptr, -1, 0.0, lane);
+    wchain_commit(C, FG, 0, F, lane);
+  }
   ++ctr.fk;
   if (k == 0) return true;
   bool finite = true;
@@ -576,7 +581,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
     unsigned long long su = 0ull;
     double* qq = init ? q : qs;
     bool ok = wik(qq, init ? T : Ref, k, P, init ? P.iterations : fine_iters, su, ws, Fa, C, FG, rtG,
-                  ctr, lane);
+                  !init, ctr, lane);
     if (!ok) {
       if (!init) break;
       if (lane < dof) q[lane] = q0;
