@@ -625,16 +625,15 @@ __global__ void __launch_bounds__(128, MINB)
 k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, int fine_iters,
                const double* tgt, int tgt_stride, const int* tl, int tl_stride,
                const double* q_init, double* q_out, double* max_res, int* finite,
-               unsigned long long* used) {
+               unsigned long long* used, int* next) {
+  // Persistent warps: each takes the next problem when it finishes one
+  // (problem cost varies by an order of magnitude, and a CTA's shared memory
+  // is held until its slowest warp is done).
   extern __shared__ __align__(16) char s_ik[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (t >= nAct) return;  // warp-uniform
-  const int kt = kk ? kk[t] : k;
   const int dof = c_hand.dof;
   const int nl = c_hand.n_links;
   char* base = s_ik + (size_t)warp * realize_warp_bytes(dof, kmax, nl);
-  WarpWs ws = warp_ws(base, kt, dof);
   double* extra = (double*)(base + warp_ws_bytes(kmax, dof));
   WTargets T, Ref;
   T.t = extra;
@@ -653,25 +652,34 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   C.sol = C.lvl + kMaxLinks;
   C.tslot = C.sol + kMaxLinks;
   C.hdr = C.tslot + kMaxK;
-  const double* src = tgt + (size_t)t * tgt_stride;
-  #pragma unroll 1
-  for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
-  if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
-  if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
-  __syncwarp();
-  wchain_build(C, T.link, kt, lane);
-  wchain_static(T.link, kt, F, lane);
   Ctr ctr = {0, 0, 0, 0, 0};
-  double mr;
-  unsigned long long u;
-  bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, ctr, lane);
-  if (lane == 0) ctr_flush(ctr);
-  if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
-  if (lane == 0) {
-    max_res[t] = mr;
-    finite[t] = fin ? 1 : 0;
-    used[t] = u;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(next, 1);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= nAct) break;  // warp-uniform
+    const int kt = kk ? kk[t] : k;
+    WarpWs ws = warp_ws(base, kt, dof);
+    const double* src = tgt + (size_t)t * tgt_stride;
+    #pragma unroll 1
+    for (int a = lane; a < 12 * kt; a += 32) T.t[a] = src[a];
+    if (lane < kt) T.link[lane] = tl[(size_t)t * tl_stride + lane];
+    if (lane < dof) q[lane] = q_init ? q_init[(size_t)t * kMaxDof + lane] : g_hand.mid[lane];
+    __syncwarp();
+    wchain_build(C, T.link, kt, lane);
+    wchain_static(T.link, kt, F, lane);
+    double mr;
+    unsigned long long u;
+    bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, ctr, lane);
+    if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
+    if (lane == 0) {
+      max_res[t] = mr;
+      finite[t] = fin ? 1 : 0;
+      used[t] = u;
+    }
+    __syncwarp();
   }
+  if (lane == 0) ctr_flush(ctr);
 }
 
 __host__ __forceinline__ size_t realize_warp_smem(int dof, int kmax, int nl, int warps) {

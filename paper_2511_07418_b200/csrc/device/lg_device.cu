@@ -340,8 +340,18 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
     CK(cudaFuncSetAttribute(k_realize_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
   auto kern = minb == 6 ? k_realize_warp<6> : (minb == 5 ? k_realize_warp<5> : k_realize_warp<4>);
-  kern<<<(n + wpb - 1) / wpb, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt, tgt_stride,
-                                                   tl, tl_stride, q_init, q_out, max_res, finite, used);
+  // persistent grid: as many CTAs as fit at once (warps fetch problems)
+  int dev = 0, sms = 0, per_sm = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+  const long long need = (n + wpb - 1) / wpb;
+  const int grid = (int)std::max(1ll, std::min(need, (long long)std::max(1, per_sm) * sms));
+  Buf bnext;
+  int* d_next = dalloc<int>(bnext, 1);
+  CK(cudaMemsetAsync(d_next, 0, sizeof(int), s));
+  kern<<<grid, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt, tgt_stride, tl, tl_stride,
+                                    q_init, q_out, max_res, finite, used, d_next);
 }
 
 // Flattened patch data on the device.
