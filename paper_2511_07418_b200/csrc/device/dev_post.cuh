@@ -125,6 +125,19 @@ k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, c
   }
 }
 
+// Funnel counts over the realised candidates (records of the others are
+// zero) and the kept-grasp flags (valid, not dropped) for the compaction.
+__global__ void k_grasp_flags(int nA, const lg_grasp* g, const int* valid, const int* drop,
+                              uint8_t* keep, int* counts) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nA) return;
+  keep[a] = (valid[a] && !drop[a]) ? 1 : 0;
+  if (drop[a]) return;
+  if (g[a].penetration_free) atomicAdd(counts, 1);
+  if (g[a].ik_converged) atomicAdd(counts + 1, 1);
+  if (g[a].stable) atomicAdd(counts + 2, 1);
+}
+
 // Reverse lookup for (candidate b, attempt, slot) (contact_field.cpp:450-484).
 __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int k, int A, int c_lo,
                               int Bsz, int pass, uint64_t seed, DField f,

@@ -1009,28 +1009,70 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                                  d_valid, d_drop);
     LAUNCH(ctx);
     check_launch();
-    std::vector<int> uatt = ddownload(b_uatt.as<int>(), (size_t)nA, s);
+    std::vector<int> uatt;
     std::vector<double> fq_h;
-    if (cfg.want_trace) fq_h = ddownload(d_fq, (size_t)nA * kMaxDof, s);
-    auto h_grasp = ddownload(d_grasp, (size_t)nA, s);
-    auto h_valid = ddownload(d_valid, (size_t)nA, s);
-    auto h_drop = ddownload(d_drop, (size_t)nA, s);
-    out.profile.postprocessing += tm.stop();
-    for (int a : real_list) {
-      const lg_grasp& g = h_grasp[a];
-      if (!h_drop[a]) {
-        out.profile.penetration_free += g.penetration_free;
-        out.profile.ik_converged += g.ik_converged;
-        out.profile.stable += g.stable;
+    std::vector<lg_grasp> h_grasp;
+    std::vector<int> h_valid, h_drop;
+    if (cfg.want_trace) {
+      uatt = ddownload(b_uatt.as<int>(), (size_t)nA, s);
+      fq_h = ddownload(d_fq, (size_t)nA * kMaxDof, s);
+      h_grasp = ddownload(d_grasp, (size_t)nA, s);
+      h_valid = ddownload(d_valid, (size_t)nA, s);
+      h_drop = ddownload(d_drop, (size_t)nA, s);
+      for (int a : real_list) {
+        const lg_grasp& g = h_grasp[a];
+        if (!h_drop[a]) {
+          out.profile.penetration_free += g.penetration_free;
+          out.profile.ik_converged += g.ik_converged;
+          out.profile.stable += g.stable;
+        }
+      }
+      // kept grasps in candidate order (pipeline.cpp:607-614)
+      for (int a = 0; a < nA; ++a) {
+        if (!h_valid[a] || h_drop[a]) continue;
+        lg_grasp g = h_grasp[a];
+        g.g = (long long)pass * B + c_lo + alive_idx[a];
+        out.grasps.push_back(g);
+      }
+    } else {
+      // funnel counts and the kept grasps compacted on the device (stable
+      // selection keeps candidate order): only the kept records cross PCIe
+      Buf b_keep, b_sel, b_nsel, b_fl;
+      uint8_t* d_keep8 = dalloc<uint8_t>(b_keep, (size_t)nA);
+      int* d_fl = dalloc<int>(b_fl, 3);
+      CK(cudaMemsetAsync(d_fl, 0, 3 * sizeof(int), s));
+      k_grasp_flags<<<grid_for(nA, 256), 256, 0, s>>>(nA, d_grasp, d_valid, d_drop, d_keep8, d_fl);
+      LAUNCH(ctx);
+      check_launch();
+      lg_grasp* d_sel = dalloc<lg_grasp>(b_sel, (size_t)nA);
+      int* d_nsel = dalloc<int>(b_nsel, 1);
+      size_t bytes = 0;
+      CK(cub::DeviceSelect::Flagged(nullptr, bytes, d_grasp, d_keep8, d_sel, d_nsel, nA, s));
+      void* tmp = ctx->tmp(bytes);
+      CK(cub::DeviceSelect::Flagged(tmp, bytes, d_grasp, d_keep8, d_sel, d_nsel, nA, s));
+      LAUNCH(ctx);
+      int counts[4];
+      CK(cudaMemcpyAsync(counts, d_fl, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(counts + 3, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      g_d2h += 4 * sizeof(int);
+      out.profile.penetration_free += counts[0];
+      out.profile.ik_converged += counts[1];
+      out.profile.stable += counts[2];
+      auto sel = ddownload(d_sel, (size_t)counts[3], s);
+      std::vector<int> kept_a;  // candidate index of each kept grasp, in order
+      {
+        auto keep8 = ddownload(d_keep8, (size_t)nA, s);
+        for (int a = 0; a < nA; ++a)
+          if (keep8[a]) kept_a.push_back(a);
+      }
+      for (size_t t = 0; t < sel.size(); ++t) {
+        lg_grasp g = sel[t];
+        g.g = (long long)pass * B + c_lo + alive_idx[kept_a[t]];
+        out.grasps.push_back(g);
       }
     }
-    // kept grasps in candidate order (pipeline.cpp:607-614)
-    for (int a = 0; a < nA; ++a) {
-      if (!h_valid[a] || h_drop[a]) continue;
-      lg_grasp g = h_grasp[a];
-      g.g = (long long)pass * B + c_lo + alive_idx[a];
-      out.grasps.push_back(g);
-    }
+    out.profile.postprocessing += tm.stop();
     if (cfg.want_trace) {
       for (int a : real_list) {
         lg_trace& t = pass_tr[alive_idx[a]];

@@ -280,3 +280,15 @@ def test_bench_config_against_oracle_shard():
     assert mismatched_fields(sub, ref.traces) == {}
     gsub = dev.grasps[(dev.grasps["g"] >= lo) & (dev.grasps["g"] < hi)]
     assert mismatched_fields(gsub, ref.grasps, GRASP_FIELDS) == {}
+
+
+def test_untraced_run_matches_oracle():
+    """The production path (want_trace = 0: funnel counts and kept grasps
+    compacted on the device) returns the same grasps and funnel."""
+    p = cfg1(batch=160, passes=2)
+    p.want_trace = 0
+    dev, ref = _run_both(p)
+    for k in FUNNEL:
+        assert dev.profile[k] == ref.profile[k], k
+    assert len(dev.grasps) > 0
+    assert mismatched_fields(dev.grasps, ref.grasps, GRASP_FIELDS) == {}
