@@ -147,6 +147,7 @@ FUNNEL = ["candidates", "placements_accepted", "contact_sets_balanced", "ik_fini
     dict(batch=64, placement_mode=0),                            # exhaustive placement
     dict(batch=48, static_contact_prob=1.0),                     # every candidate pinned
     dict(batch=32, k_contacts=3),                                # k = 3 of 4 groups
+    dict(batch=32, k_contacts=4, static_contact_prob=0.5),       # k = 4 (+ statics): 5-6 contacts
 ])
 def test_run_batch_stage_traces_bit_exact(case):
     case = dict(case)
