@@ -276,6 +276,10 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
 // x (smem) rhs in / solution out.
 __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, int* tr,
                                             double* tmp, int lane) {
+  (void)tr;
+  // pidx: the transpositions applied so far to the index vector (lane i
+  // holds entry i), so P^T b is a gather and P y a scatter at the end
+  int pidx = lane;
   #pragma unroll 1
   for (int k = 0; k < n; ++k) {
     // pivot = first index of max |A(i,i)|, i >= k.  Non-negative doubles
@@ -304,8 +308,10 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
       }
       big = idx;
     }
-    if (lane == 0) tr[k] = big;
     if (k != big) {
+      const int pk = __shfl_sync(kFull, pidx, k), pb = __shfl_sync(kFull, pidx, big);
+      if (lane == k) pidx = pb;
+      else if (lane == big) pidx = pk;
       if (lane < k) {
         double t = A[k * ld + lane];
         A[k * ld + lane] = A[big * ld + lane];
@@ -345,15 +351,8 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     if (dabs(akk) > 0.0 && lane > k && lane < n) A[lane * ld + k] /= akk;
     __syncwarp();
   }
-  if (lane == 0)
-    #pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-      double t = x[k];
-      x[k] = x[tr[k]];
-      x[tr[k]] = t;
-    }
+  double xi = lane < n ? x[pidx] : 0.0;  // P^T b (the forward transpositions)
   __syncwarp();
-  double xi = lane < n ? x[lane] : 0.0;
   double s = 0.0;
   #pragma unroll 1
   for (int j = 0; j < n; ++j) {  // forward: L unit lower
@@ -373,15 +372,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     if (lane == j) xi = xj;
     if (lane < j) s = s + A[j * ld + lane] * xj;
   }
-  if (lane < n) x[lane] = xi;
-  __syncwarp();
-  if (lane == 0)
-    #pragma unroll 1
-    for (int k = n - 1; k >= 0; --k) {
-      double t = x[k];
-      x[k] = x[tr[k]];
-      x[tr[k]] = t;
-    }
+  if (lane < n) x[pidx] = xi;  // P y (the transpositions in reverse order)
   __syncwarp();
 }
 
