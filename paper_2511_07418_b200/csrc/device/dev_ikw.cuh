@@ -236,7 +236,7 @@ __device__ __forceinline__ double wresidual(const double* F, const WTargets& T, 
   __syncwarp();
   double s = 0.0;
   if (lane == 0)
-    #pragma unroll 1
+    #pragma unroll 4
     for (int i = 0; i < 6 * k; ++i) s = s + r[i] * r[i];
   return __shfl_sync(kFull, s, 0);
 }
@@ -458,7 +458,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     __syncwarp();
     double tr = 0.0;
     if (lane == 0)
-      #pragma unroll 1
+      #pragma unroll 4
       for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * ld + a];
     tr = __shfl_sync(kFull, tr, 0);
     double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
@@ -499,7 +499,7 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       __syncwarp();
       double obj_try = 0.0;
       if (lane < ng)
-        #pragma unroll 1
+        #pragma unroll 4
         for (int i = 0; i < rk; ++i) obj_try = obj_try + rtG[lane * rk + i] * rtG[lane * rk + i];
       unsigned accm = __ballot_sync(kFull, lane < ng && obj_try <= objective);
       if (accm) {
