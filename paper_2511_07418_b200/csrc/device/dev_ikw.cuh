@@ -381,7 +381,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
 // joints with a nonzero column.
 __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
                     unsigned long long& used, WarpWs& ws, double* F, const WChain& C, double* FG,
-                    double* rtG, bool have_frames, Ctr& ctr, int lane) {
+                    double* rtG, bool have_frames, const unsigned short* ab, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   const int ld = dof | 1;  // odd row stride: column accesses hit distinct banks
   const int rows = 6 * k;
@@ -437,12 +437,8 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     __syncwarp();
     // J^T J (upper triangle, mirrored) and J^T r
     const int ne = dof * (dof + 1) / 2;
-    for (int e = lane, a = 0, rem = lane; e < ne; e += 32, rem += 32) {
-      while (rem >= dof - a) {  // row-major upper-triangle index -> (a, b)
-        rem -= dof - a;
-        ++a;
-      }
-      int b = a + rem;
+    for (int e = lane; e < ne; e += 32) {
+      const int a = ab[e] & 0xff, b = ab[e] >> 8;  // row-major upper-triangle entry e
       double s = 0.0;
       #pragma unroll 4
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
@@ -550,7 +546,7 @@ __device__ __noinline__ double wproject(const double* F, const WTargets& T, int 
 __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref, int k,
                          const IkCfg& P, int rounds, int fine_iters, double* max_res,
                          unsigned long long* used_out, WarpWs& ws, double* Fa, const WChain& C,
-                         double* FG, double* rtG, Ctr& ctr, int lane) {
+                         double* FG, double* rtG, const unsigned short* ab, Ctr& ctr, int lane) {
   const int dof = c_hand.dof;
   double q0 = lane < dof ? q[lane] : 0.0;
   unsigned long long used = 0ull;
@@ -572,7 +568,7 @@ __device__ bool wrealize(double* q, double* qs, const WTargets& T, WTargets& Ref
     unsigned long long su = 0ull;
     double* qq = init ? q : qs;
     bool ok = wik(qq, init ? T : Ref, k, P, init ? P.iterations : fine_iters, su, ws, Fa, C, FG, rtG,
-                  !init, ctr, lane);
+                  !init, ab, ctr, lane);
     if (!ok) {
       if (!init) break;
       if (lane < dof) q[lane] = q0;
@@ -621,9 +617,14 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
   // (problem cost varies by an order of magnitude, and a CTA's shared memory
   // is held until its slowest warp is done).
   extern __shared__ __align__(16) char s_ik[];
+  __shared__ unsigned short s_ab[kMaxDof * (kMaxDof + 1) / 2];  // (a, b) of J^T J entry e
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dof = c_hand.dof;
   const int nl = c_hand.n_links;
+  if (threadIdx.x == 0)
+    for (int a = 0, e = 0; a < dof; ++a)
+      for (int b = a; b < dof; ++b) s_ab[e++] = (unsigned short)(a | (b << 8));
+  __syncthreads();
   char* base = s_ik + (size_t)warp * realize_warp_bytes(dof, kmax, nl);
   double* extra = (double*)(base + warp_ws_bytes(kmax, dof));
   WTargets T, Ref;
@@ -661,7 +662,8 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
     wchain_static(T.link, kt, F, lane);
     double mr;
     unsigned long long u;
-    bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, ctr, lane);
+    bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, s_ab, ctr,
+                        lane);
     if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
     if (lane == 0) {
       max_res[t] = mr;
