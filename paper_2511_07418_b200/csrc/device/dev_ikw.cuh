@@ -436,20 +436,24 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     used = __reduce_or_sync(kFull, (unsigned)used);  // dof <= 32: one word
     __syncwarp();
     // J^T J (upper triangle, mirrored) and J^T r
+    // J^T J upper-triangle entries e < ne and J^T r entries ne <= e < ne +
+    // dof share one branch-free loop (same row-ordered dot product: column
+    // a of J against column b of J, or against r)
     const int ne = dof * (dof + 1) / 2;
-    for (int e = lane; e < ne; e += 32) {
-      const int a = ab[e] & 0xff, b = ab[e] >> 8;  // row-major upper-triangle entry e
+    for (int e = lane; e < ne + dof; e += 32) {
+      const bool jj = e < ne;
+      const int a = jj ? (ab[e] & 0xff) : e - ne, b = jj ? (ab[e] >> 8) : 0;
+      const double* o2 = jj ? ws.J + b : r;
+      const int st2 = jj ? dof : 1;
       double s = 0.0;
       #pragma unroll 4
-      for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * ws.J[rr * dof + b];
-      ws.A[a * ld + b] = s;
-      ws.A[b * ld + a] = s;
-    }
-    if (lane < dof) {
-      double s = 0.0;
-      #pragma unroll 1
-      for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + lane] * r[rr];
-      ws.x[lane] = s;
+      for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * o2[rr * st2];
+      if (jj) {
+        ws.A[a * ld + b] = s;
+        ws.A[b * ld + a] = s;
+      } else {
+        ws.x[a] = s;
+      }
     }
     __syncwarp();
     double tr = 0.0;
