@@ -16,6 +16,59 @@
 
 namespace lgd {
 
+// sample_surface (mesh.cpp:297-339) for many meshes at once.  Each sample
+// takes exactly three draws (face, u, v) of its mesh's stream, so one thread
+// per mesh writes the stream and one thread per sample builds the point:
+// face by lower_bound on the cumulative areas, the same corner arithmetic.
+struct SampleSeg {
+  long long tri0, s0;  // first triangle (corners [t][9], normals [t][3], cum [t]) / sample
+  int ntri, count;
+  uint64_t seed;
+};
+
+__global__ void k_sample_draws(int nseg, const SampleSeg* seg, uint64_t* draws) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nseg) return;
+  DRng rng;
+  rng.seed(seg[b].seed);
+  uint64_t* o = draws + 3 * seg[b].s0;
+  for (long long i = 0; i < 3ll * seg[b].count; ++i) o[i] = rng.u64();
+}
+
+__global__ void k_sample_points(long long n, int nseg, const SampleSeg* seg, const long long* sample_seg_start,
+                                const double* corners, const double* fnrm, const double* cum,
+                                const uint64_t* draws, double* pos, double* nrm) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg - 1;  // segment of sample i
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (sample_seg_start[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const SampleSeg S = seg[lo];
+    const uint64_t* d = draws + 3 * i;
+    const double* c = cum + S.tri0;
+    const double pick = u01(d[0]) * c[S.ntri - 1];
+    int a = 0, z = S.ntri;  // lower_bound: first cum >= pick
+    while (a < z) {
+      int m = (a + z) >> 1;
+      if (c[m] < pick) a = m + 1;
+      else z = m;
+    }
+    const int t = a < S.ntri ? a : S.ntri - 1;
+    double u = u01(d[1]), v = u01(d[2]);
+    if (u + v > 1.0) {
+      u = 1.0 - u;
+      v = 1.0 - v;
+    }
+    const double* q = corners + 9 * (S.tri0 + t);
+    V3 A = v3(q[0], q[1], q[2]), B = v3(q[3], q[4], q[5]), Cc = v3(q[6], q[7], q[8]);
+    v3_store(pos + 3 * i, axpy(axpy(A, u, sub(B, A)), v, sub(Cc, A)));
+    v3_store(nrm + 3 * i, v3_load(fnrm + 3 * (S.tri0 + t)));
+  }
+}
+
 constexpr int kCoverThreads = 1024;
 
 // seg b covers samples [off[b], off[b+1]) of one link.  Outputs per segment:
@@ -97,7 +150,7 @@ __global__ void k_patch_fields(int np, const int* gid, const int* msize, const i
     for (int i = 0; i < m; ++i) out[i] = i;
     return;
   }
-  int key[16], val[16], nk = 0;  // pool[key] = val for swapped slots
+  int key[32], val[32], nk = 0;  // pool[key] = val for swapped slots (<= 2 (cap - 1))
   auto get = [&](int s) {
     for (int q = 0; q < nk; ++q)
       if (key[q] == s) return val[q];

@@ -1195,32 +1195,65 @@ int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double spc, double 
   return lgc::guard([&] {
     if (!ctx || !hand || !out) throw std::invalid_argument("lg_hand_patches_device: null argument");
     const auto& H = hand->h;
-    // per-link hand samples, stream 'hnds' (pipeline.cpp:277-285), host side
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    // per-link hand samples, stream 'hnds' (pipeline.cpp:277-285), on the
+    // device: face areas / normals / counts on the host (O(triangles)), the
+    // draws and points on the GPU (k_sample_draws, k_sample_points)
     std::vector<int> seg_link;
     std::vector<long long> off{0};
-    std::vector<double> pos, nrm;
+    std::vector<SampleSeg> segs;
+    std::vector<double> corners, fn, cum;
     for (size_t l = 0; l < H.links.size(); ++l) {
-      if (H.links[l].visual.verts.empty()) continue;
-      auto S = lgh::sample_surface(H.links[l].visual, spc, lgm::mix_seed(seed, 0x686e6473ull, l));
-      if (S.empty()) continue;
-      seg_link.push_back((int)l);
-      for (const auto& x : S) {
-        pos.insert(pos.end(), {x.p.x, x.p.y, x.p.z});
-        nrm.insert(nrm.end(), {x.n.x, x.n.y, x.n.z});
+      const lgh::Mesh& m = H.links[l].visual;
+      if (m.verts.empty() || m.tris.empty()) continue;
+      size_t count = (size_t)std::llround(m.surface_area() * 1e4 * spc);
+      if (count == 0) count = 1;
+      SampleSeg sg;
+      sg.tri0 = (long long)cum.size();
+      sg.s0 = off.back();
+      sg.ntri = (int)m.tris.size();
+      sg.count = (int)count;
+      sg.seed = lgm::mix_seed(seed, 0x686e6473ull, l);
+      double acc = 0.0;
+      for (int t = 0; t < (int)m.tris.size(); ++t) {
+        acc += m.face_area(t);
+        cum.push_back(acc);
+        for (int c = 0; c < 3; ++c) {
+          const V3& v = m.verts[m.tris[t][c]];
+          corners.insert(corners.end(), {v.x, v.y, v.z});
+        }
+        V3 nn = m.face_normal(t);
+        fn.insert(fn.end(), {nn.x, nn.y, nn.z});
       }
-      off.push_back((long long)(pos.size() / 3));
+      segs.push_back(sg);
+      seg_link.push_back((int)l);
+      off.push_back(off.back() + (long long)count);
     }
     if (radius <= 0.0 || cap < 1) throw std::invalid_argument("decompose_patches: bad radius or cap");
     if (cap > 16) throw std::invalid_argument("lg_hand_patches_device: field cap above 16");
     const long long total = off.back();
     if (total == 0) throw std::invalid_argument("decompose_patches: no surface samples");
-    use_ctx(ctx);
-    cudaStream_t s = ctx->stream;
     const int nseg = (int)seg_link.size();
-    Buf bl, bo, bp, ba, bb, bm, bs, bn;
+    Buf bsg, bss, bcr, bfn, bcu, bdr, bp, bnr;
+    const SampleSeg* d_sg = dupload(bsg, segs.data(), segs.size(), s);
+    const long long* d_ss = dupload(bss, off.data(), (size_t)nseg, s);
+    const double* d_cr = dupload(bcr, corners.data(), corners.size(), s);
+    const double* d_fn = dupload(bfn, fn.data(), fn.size(), s);
+    const double* d_cu = dupload(bcu, cum.data(), cum.size(), s);
+    uint64_t* d_dr = dalloc<uint64_t>(bdr, 3 * (size_t)total);
+    double* d_p = dalloc<double>(bp, 3 * (size_t)total);
+    double* d_nr = dalloc<double>(bnr, 3 * (size_t)total);
+    k_sample_draws<<<grid_for(nseg, 32), 32, 0, s>>>(nseg, d_sg, d_dr);
+    check_launch();
+    k_sample_points<<<grid_for(total, 256), 256, 0, s>>>(total, nseg, d_sg, d_ss, d_cr, d_fn, d_cu, d_dr,
+                                                          d_p, d_nr);
+    check_launch();
+    auto pos = ddownload(d_p, 3 * (size_t)total, s);
+    auto nrm = ddownload(d_nr, 3 * (size_t)total, s);
+    Buf bl, bo, ba, bb, bm, bs, bn;
     const int* d_l = dupload(bl, seg_link.data(), seg_link.size(), s);
     const long long* d_o = dupload(bo, off.data(), off.size(), s);
-    const double* d_p = dupload(bp, pos.data(), pos.size(), s);
     int* d_a = dalloc<int>(ba, (size_t)total);
     int* d_b = dalloc<int>(bb, (size_t)total);
     int* d_m = dalloc<int>(bm, (size_t)total);

@@ -232,9 +232,11 @@ def _patch_arrays(pt):
     ("allegro_like.urdf", 30.0, 0.012, 8),
     ("shadow_like.urdf", 1000.0, 0.008, 8),   # config 4: ~810k hand samples
     ("shadow_like.urdf", 200.0, 0.008, 3),
+    ("shadow_like.urdf", 30.0, 0.020, 16),    # large patches: the maximum field cap
 ])
 def test_patches_device_identical(ctx, hand_name, spc, radius, cap):
-    """decompose_patches on the GPU == the host cover."""
+    """Hand sampling + decompose_patches on the GPU ==
+    the host path (sample_surface per link, greedy cover, field subsets)."""
     hand = lg.load_hand(asset("hands", hand_name))
     a = _patch_arrays(lg.hand_patches(hand, spc, radius, 7, cap))
     b = _patch_arrays(lg.hand_patches_device(ctx, hand, spc, radius, 7, cap))
