@@ -284,8 +284,8 @@ uint64_t lg_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
 int lg_hand_patches(const lg_hand* h, double samples_per_cm2,
                     double patch_radius, uint64_t seed, int field_cap,
                     lg_patches** out);
-/* The same patches with decompose_patches' greedy cover and field-point
- * subsets on the GPU (hand sampling stays on the host); identical output. */
+/* The same patches with the hand's surface sampling, decompose_patches'
+ * greedy cover and the field-point subsets on the GPU; identical output. */
 int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double samples_per_cm2,
                            double patch_radius, uint64_t seed, int field_cap,
                            lg_patches** out);

@@ -307,8 +307,8 @@ class Patches:
 
 
 def hand_patches_device(ctx, hand, samples_per_cm2, patch_radius, seed, field_cap=8):
-    """hand_patches with decompose_patches' greedy cover and field-point
-    subsets on the GPU (identical patches)."""
+    """hand_patches on the GPU: the per-link surface sampling, the greedy
+    cover and the field-point subsets (identical patches)."""
     h = C.c_void_p()
     check(lib().lg_hand_patches_device(ctx._h, hand._h, float(samples_per_cm2),
                                        float(patch_radius), C.c_uint64(seed), int(field_cap),
