@@ -281,7 +281,6 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
               const int ne = (int)cnt[q];
               double bd;
               int bi;
-              unsigned long long visited;
               // Every lane scans the same elements (broadcast loads, no
               // divergence): faster than the pruned search for domains of
               // a few thousand elements.
@@ -339,8 +338,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
                   bi = e;
                 }
               }
-              visited = (unsigned long long)ne;
-              ctr.proj += visited;
+              ctr.proj += (unsigned long long)ne;
               cand = bi;
               const long long eg = off[q] + bi;
               slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));

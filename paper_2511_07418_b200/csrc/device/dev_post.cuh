@@ -33,7 +33,8 @@ struct CollWarpSmem {
   int nobj, viol;
 };
 
-__global__ void __launch_bounds__(32 * kCollWarps)
+template <int MINB>
+__global__ void __launch_bounds__(32 * kCollWarps, MINB)
 k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, const double* q_all,
              const double* pose, const double* obj_aabb, int clean_only, uint8_t* clean_out,
              double* maxpen_out) {
