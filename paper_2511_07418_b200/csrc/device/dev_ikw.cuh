@@ -198,11 +198,11 @@ __device__ __forceinline__ void wchain_commit(const WChain& C, const double* FG,
   __syncwarp();
 }
 
-// Warp max of v.  Non-negative finite doubles order like their bit
-// patterns, so the common case is two 32-bit warp reductions; anything else
-// takes the comparison butterfly.
+// Warp max of v.  Finite doubles with a clear sign bit (so not -0.0) order
+// like their bit patterns, so the common case is two 32-bit warp
+// reductions; anything else takes the comparison butterfly.
 __device__ __forceinline__ double warp_max_d(double v) {
-  if (__all_sync(kFull, v >= 0.0 && v <= 1.7976931348623157e308)) {
+  if (__all_sync(kFull, __double_as_longlong(v) >= 0 && v <= 1.7976931348623157e308)) {
     unsigned long long b = (unsigned long long)__double_as_longlong(v);
     unsigned hi = __reduce_max_sync(kFull, (unsigned)(b >> 32));
     unsigned lo = __reduce_max_sync(kFull, (unsigned)(b >> 32) == hi ? (unsigned)b : 0u);
@@ -537,7 +537,11 @@ __device__ __noinline__ double wproject(const double* F, const WTargets& T, int 
     }
   }
   __syncwarp();
-  return warp_max_d(d);
+  // worst = std::max(worst, d) from worst = 0.0: the max of +0.0 and the
+  // non-NaN distances, so clamping each lane first gives the same value
+  // (negative, -0.0 and NaN distances all leave +0.0) and keeps the
+  // reduction on its two-word fast path when contacts penetrate
+  return warp_max_d(0.0 < d ? d : 0.0);
 }
 
 // realize_grasp (pipeline.cpp:185-253) for one warp; q (smem) starts at q0.

@@ -263,6 +263,24 @@ def test_device_errors_map_to_reference_exceptions(ctx, four_finger):
     assert ok.profile["candidates"] == 8
 
 
+def test_empty_batch_matches_oracle(ctx, four_finger):
+    """batch = 0 (or passes = 0) past the config layer: the reference's
+    run_batch builds the field and returns no candidates, no grasps
+    (pipeline.cpp:385 loop never runs); the device does the same."""
+    p = cfg1(batch=8)
+    hand, patches, raw, _ = lg.prepare_inputs(p)
+    for field, val in (("batch", 0), ("passes", 0)):
+        q = cfg1(batch=8)
+        setattr(q, field, val)
+        q.want_trace = 1
+        dev = lg.run_batch(ctx, hand, patches, raw, q)
+        ref = orc.run_batch(hand.desc, patches.desc, raw, q, workers=0)
+        assert len(dev.traces) == len(ref.traces) == 0
+        assert len(dev.grasps) == len(ref.grasps) == 0
+        for k in FUNNEL + ["patches", "boxes", "field_vectors", "object_samples", "field_samples"]:
+            assert dev.profile[k] == ref.profile[k], (field, k)
+
+
 def test_bench_config_against_oracle_shard():
     """The bench workload itself (Allegro-class hand, 5 cm box, 10k seeds):
     the device's full batch, compared candidate by candidate with the
