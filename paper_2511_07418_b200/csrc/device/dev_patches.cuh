@@ -81,7 +81,7 @@ k_patch_cover(int nseg, const int* seg_link, const long long* off, const double*
               int* npatch) {
   typedef cub::BlockScan<int, kCoverThreads> Scan;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_sid, s_tot;
+  __shared__ int s_sid;
   __shared__ double s_c[3];
   const int b = blockIdx.x;
   if (b >= nseg) return;

@@ -189,7 +189,7 @@ LG_HD double xlog(double x) {
   int k = 0;
   if (hx < 0x00100000) {  // x < 2^-1022
     if (((hx & 0x7fffffff) | (int32_t)lx) == 0) return -__builtin_huge_val();  // -inf
-    if (hx < 0) return (x - x) / 0.0;                                  // NaN
+    if (hx < 0) return (x - x) / (x - x);                              // NaN
     k -= 54;
     x *= two54;
     hx = high_word(x);
