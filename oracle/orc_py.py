@@ -14,7 +14,7 @@ import numpy as np
 from paper_2511_07418_b200 import lgabi as A
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liborc.so")
+LIB_PATH = os.environ.get("ORC_LIB", os.path.join(_HERE, "liborc.so"))
 _LIB = None
 
 

@@ -147,6 +147,9 @@ LG_HD double k_cos(double x, double y) {
 }
 
 LG_HD double xsin(double x) {
+#if defined(LG_USE_GLIBC) && !defined(__CUDA_ARCH__)
+  return ::sin(x);
+#endif
   if (!is_finite(x)) return x - x;
   if (dabs(x) < 7.450580596923828125e-09) return x;  // 2^-27
   double y0, y1;
@@ -160,6 +163,9 @@ LG_HD double xsin(double x) {
 }
 
 LG_HD double xcos(double x) {
+#if defined(LG_USE_GLIBC) && !defined(__CUDA_ARCH__)
+  return ::cos(x);
+#endif
   if (!is_finite(x)) return x - x;
   if (dabs(x) < 7.450580596923828125e-09) return 1.0;
   double y0, y1;
@@ -174,6 +180,9 @@ LG_HD double xcos(double x) {
 
 // ---------------------------------------------------------------------- log
 LG_HD double xlog(double x) {
+#if defined(LG_USE_GLIBC) && !defined(__CUDA_ARCH__)
+  return ::log(x);
+#endif
   const double ln2_hi = 6.93147180369123816490e-01;
   const double ln2_lo = 1.90821492927058770002e-10;
   const double two54 = 1.80143985094819840000e+16;
@@ -284,6 +293,9 @@ LG_HD double xatan(double x) {
 }
 
 LG_HD double xatan2(double y, double x) {
+#if defined(LG_USE_GLIBC) && !defined(__CUDA_ARCH__)
+  return ::atan2(y, x);
+#endif
   const double pi_o_4 = 7.8539816339744827900e-01;
   const double pi_o_2 = 1.5707963267948965580e+00;
   const double pi = 3.1415926535897931160e+00;
@@ -339,6 +351,9 @@ LG_HD double xatan2(double y, double x) {
 
 // -------------------------------------------------------------------- hypot
 LG_HD double xhypot(double x, double y) {
+#if defined(LG_USE_GLIBC) && !defined(__CUDA_ARCH__)
+  return ::hypot(x, y);
+#endif
   double a = dabs(x), b = dabs(y);
   if (!is_finite(a) || !is_finite(b)) {
     if (a == 1.0 / 0.0 || b == 1.0 / 0.0) return 1.0 / 0.0;
