@@ -402,6 +402,15 @@ int lg_validation_issues(const lg_hand* hand, const lg_grasp_check* checks, long
                          const lg_run_params* p, char* buf, size_t cap, size_t* needed,
                          long long* n_issues);
 
+/* The hot path's transcendentals on the device (which: 0 sin, 1 cos, 2 log,
+ * 3 atan2(x, y), 4 hypot(x, y)): glibc 2.39's algorithms restated in
+ * csrc/lg_libm.h, used by every kernel that draws Box-Muller normals, builds a
+ * rotation or projects a friction disc (rng.hpp:47-76, hand.cpp:286-288,
+ * geometry.hpp:129-143, wrench.cpp:96).  Exposed for the bit-exactness check
+ * against the host's std:: functions. */
+int lg_libm_eval(lg_ctx* ctx, int which, long long n, const double* x, const double* y,
+                 double* out);
+
 /* run_batch (pipeline.cpp:308-625): the whole forward pass on the device,
  * field build included.  raw_samples = sample_surface of the object. */
 int lg_run_batch(lg_ctx* ctx, const lg_hand_desc* hand,

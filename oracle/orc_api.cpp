@@ -107,6 +107,21 @@ void orc_libm(int which, int n, const double* x, const double* y, double* out) {
   }
 }
 
+// The host glibc itself (std::sin / cos / log / atan2 / hypot, what the
+// reference calls) for the same argument arrays, to check lgm:: (and the
+// device) against it bit for bit.
+void orc_glibc(int which, long long n, const double* x, const double* y, double* out) {
+  for (long long i = 0; i < n; ++i) {
+    switch (which) {
+      case 0: out[i] = std::sin(x[i]); break;
+      case 1: out[i] = std::cos(x[i]); break;
+      case 2: out[i] = std::log(x[i]); break;
+      case 3: out[i] = std::atan2(x[i], y[i]); break;
+      default: out[i] = std::hypot(x[i], y[i]); break;
+    }
+  }
+}
+
 // random_problem of test_wrench.cpp:13-25 (fixture generator): points on a
 // 5 cm sphere, roughly inward unit normals.
 void orc_random_wrench_problem(uint64_t seed, int n, double* pts, double* nrm) {

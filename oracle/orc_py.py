@@ -38,6 +38,7 @@ def lib():
             "orc_rng_unit_vectors": (None, [C.c_uint64, C.c_int, dp]),
             "orc_rng_quaternions": (None, [C.c_uint64, C.c_int, dp]),
             "orc_libm": (None, [C.c_int, C.c_int, dp, dp, dp]),
+            "orc_glibc": (None, [C.c_int, C.c_longlong, dp, dp, dp]),
             "orc_tangent_basis": (C.c_int, [dp, dp, dp]),
             "orc_rotation_between": (C.c_int, [dp, dp, dp]),
             "orc_fk": (C.c_int, [HD, dp, dp]),
@@ -151,6 +152,17 @@ def libm(which, x, y=None):
     out = np.zeros_like(x)
     idx = {"sin": 0, "cos": 1, "log": 2, "atan2": 3, "hypot": 4}[which]
     lib().orc_libm(idx, len(x), _p(x), _p(y), _p(out))
+    return out
+
+
+def glibc(which, x, y=None):
+    """The host glibc's own std::sin/cos/log/atan2/hypot (what the reference
+    calls), evaluated natively over the arrays."""
+    x = _d(x)
+    y = _d(x if y is None else y)
+    out = np.zeros_like(x)
+    idx = {"sin": 0, "cos": 1, "log": 2, "atan2": 3, "hypot": 4}[which]
+    lib().orc_glibc(idx, len(x), _p(x), _p(y), _p(out))
     return out
 
 

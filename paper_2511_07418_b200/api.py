@@ -100,6 +100,7 @@ def lib():
         "lg_result_num_traces": (C.c_longlong, [vp]),
         "lg_result_traces": (P(A.Trace), [vp]),
         "lg_result_destroy": (None, [vp]),
+        "lg_libm_eval": (C.c_int, [vp, C.c_int, C.c_longlong, A.dp, A.dp, A.dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -445,6 +446,16 @@ def query_domains_batch(ctx, field, group_of_patch, samples, poses, theta_hit,
                                        masks.ctypes.data_as(C.POINTER(C.c_uint32)),
                                        _dp(scores) if with_scores else None))
     return (masks, scores) if with_scores else masks
+
+
+def libm_eval(ctx, which, x, y=None):
+    """The device's sin/cos/log/atan2/hypot (glibc's algorithms, lg_libm.h)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    yy = np.ascontiguousarray(x if y is None else y, dtype=np.float64)
+    out = np.zeros_like(x)
+    idx = {"sin": 0, "cos": 1, "log": 2, "atan2": 3, "hypot": 4}[which]
+    check(lib().lg_libm_eval(ctx._h, idx, len(x), _dp(x), _dp(yy), _dp(out)))
+    return out
 
 
 def preprocess_object(ctx, samples, probe_half_width, depth_threshold):

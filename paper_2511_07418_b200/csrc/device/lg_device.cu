@@ -1667,6 +1667,45 @@ int lg_preprocess(lg_ctx* ctx, const double* samples, int n, double h, double d,
   });
 }
 
+namespace lgd {
+// The hot path's transcendentals (csrc/lg_libm.h) evaluated on the device, for
+// the bit-exactness check against the host glibc (tests/test_libm.py).
+__global__ void k_libm_eval(int which, int n, const double* x, const double* y, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a = x[i], r;
+  switch (which) {
+    case 0: r = lgm::xsin(a); break;
+    case 1: r = lgm::xcos(a); break;
+    case 2: r = lgm::xlog(a); break;
+    case 3: r = lgm::xatan2(a, y[i]); break;
+    default: r = lgm::xhypot(a, y[i]); break;
+  }
+  out[i] = r;
+}
+}  // namespace lgd
+
+int lg_libm_eval(lg_ctx* ctx, int which, long long n, const double* x, const double* y,
+                 double* out) {
+  return lgc::guard([&] {
+    if (!ctx || !x || !out || n < 0 || which < 0 || which > 4 || (which >= 3 && !y))
+      throw std::invalid_argument("lg_libm_eval: bad argument");
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    Buf bx, by, bo;
+    dupload(bx, x, (size_t)n, s);
+    if (which >= 3) dupload(by, y, (size_t)n, s);
+    double* d_out = dalloc<double>(bo, (size_t)n);
+    lgd::k_libm_eval<<<grid_for((int)n, 256), 256, 0, s>>>(which, (int)n, (const double*)bx.p,
+                                                           which >= 3 ? (const double*)by.p : nullptr,
+                                                           d_out);
+    check_launch();
+    LAUNCH(ctx);
+    CK(cudaMemcpyAsync(out, d_out, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
 int lg_run_batch_field(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches,
                        lg_field* field, const double* raw, int n_raw, const lg_run_params* p,
                        lg_result** out) {
