@@ -1671,17 +1671,17 @@ namespace lgd {
 // The hot path's transcendentals (csrc/lg_libm.h) evaluated on the device, for
 // the bit-exactness check against the host glibc (tests/test_libm.py).
 __global__ void k_libm_eval(int which, int n, const double* x, const double* y, double* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double a = x[i], r;
-  switch (which) {
-    case 0: r = lgm::xsin(a); break;
-    case 1: r = lgm::xcos(a); break;
-    case 2: r = lgm::xlog(a); break;
-    case 3: r = lgm::xatan2(a, y[i]); break;
-    default: r = lgm::xhypot(a, y[i]); break;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a = x[i], r;
+    switch (which) {
+      case 0: r = lgm::xsin(a); break;
+      case 1: r = lgm::xcos(a); break;
+      case 2: r = lgm::xlog(a); break;
+      case 3: r = lgm::xatan2(a, y[i]); break;
+      default: r = lgm::xhypot(a, y[i]); break;
+    }
+    out[i] = r;
   }
-  out[i] = r;
 }
 }  // namespace lgd
 

@@ -46,6 +46,8 @@ def ref_inputs(cfg, hand, obj, batch, extra="", workers=8):
 def grasp_mismatches(a, b):
     assert len(a) == len(b), (len(a), len(b))
     bad = {}
+    if len(a) == 0:
+        return bad
     for f in GRASP_FIELDS:
         x = np.ascontiguousarray(a[f]).view(np.uint8).reshape(len(a), -1)
         y = np.ascontiguousarray(b[f]).view(np.uint8).reshape(len(b), -1)
@@ -123,7 +125,7 @@ GPU_CASES = CPU_CASES + [
     ("allegro.cfg", "allegro_like.urdf", "cylinder_r025_l100.obj", 256, ""),
     # configs[2] (LEAP-class on tools) at leap.cfg as written
     ("leap.cfg", "leap_like.urdf", "mug.obj", 192, ""),
-    ("leap.cfg", "leap_like.urdf", "drill.obj", 128, ""),
+    ("leap.cfg", "leap_like.urdf", "drill.obj", 256, ""),
 ]
 
 
