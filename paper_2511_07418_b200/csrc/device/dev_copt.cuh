@@ -58,8 +58,8 @@ __device__ __forceinline__ void proj_one(bool is_anchor, double mu, double& a, d
     return;
   }
   double cap = mu * a;
-  double r = lgm::xhypot(bx, by);
-  if (r > cap) {
+  double r;
+  if (lgl::hypot_exceeds(bx, by, cap, &r)) {
     if (cap <= 0.0 || r <= 0.0) {
       bx = 0.0;
       by = 0.0;
@@ -269,9 +269,10 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             int cand = -1, an = -1;
             if (m < cfg.n_inner) {
               const uint64_t* d2 = M + 2 * ((long long)(outer * k + q) * cfg.n_inner + m);
-              double z1, z2;
-              box_muller(d2[0], d2[1], &z1, &z2);
-              V3 cp = axpy(axpy(cur_p, cfg.sigma * z1, tx), cfg.sigma * z2, ty);
+              // (sigma z1, sigma z2), precomputed by k_copt_normals
+              const double u = __longlong_as_double((long long)d2[0]);
+              const double vv = __longlong_as_double((long long)d2[1]);
+              V3 cp = axpy(axpy(cur_p, u, tx), vv, ty);
               // project_to_domain (contact_opt.cpp:11-25): nearest element,
               // first index among equal distances.  Every lane scans the same
               // elements (broadcast loads, no divergence); pruned searches

@@ -508,8 +508,8 @@ __device__ __forceinline__ void wproject(const WProb& w, int anchor, bool fr, WS
         s.by[i] = 0.0;
       } else {
         double cap = w.mu * s.a[i];
-        double r = lgm::xhypot(s.bx[i], s.by[i]);
-        if (r > cap) {
+        double r;
+        if (lgl::hypot_exceeds(s.bx[i], s.by[i], cap, &r)) {
           if (cap <= 0.0 || r <= 0.0) {
             s.bx[i] = 0.0;
             s.by[i] = 0.0;

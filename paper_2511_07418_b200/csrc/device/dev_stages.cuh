@@ -536,6 +536,26 @@ __global__ void k_copt_draws(int nA, const int* alive_idx, int c_lo, int B, int 
   for (long long d = 0; d < per_cand; ++d) o[d] = mt_next(g);
 }
 
+// The mutation draws of every restart as the tangent-plane offsets the
+// search consumes: each (u64, u64) pair becomes (sigma * z1, sigma * z2) with
+// (z1, z2) the Box-Muller pair of rng.hpp:47-61 — u = sigma * normal(),
+// v = sigma * normal() of contact_opt.cpp:108-109 (the second normal() call
+// returns the cached spare).  In place, bit-cast into the u64 buffer; one
+// thread per pair, so the transcendentals stay out of the search kernel.
+__global__ void k_copt_normals(long long n_pairs, int per_restart_pairs, int k,
+                               long long per_restart, double sigma, uint64_t* draws) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_pairs;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long rr = t / per_restart_pairs;  // (candidate, restart) index
+    int j = (int)(t - rr * per_restart_pairs);
+    uint64_t* d2 = draws + rr * per_restart + k + 2 * j;
+    double z1, z2;
+    box_muller(d2[0], d2[1], &z1, &z2);
+    d2[0] = (uint64_t)__double_as_longlong(sigma * z1);
+    d2[1] = (uint64_t)__double_as_longlong(sigma * z2);
+  }
+}
+
 // ------------------------------------------------------ optimize_contacts
 struct CoptCfg {
   int k, n_outer, n_inner, restarts;

@@ -784,6 +784,15 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     k_copt_draws<<<grid_for(nA, 64), 64, 0, s>>>(nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, d_draws);
     LAUNCH(ctx);
     check_launch();
+    {
+      const int prp = cfg.n_outer * k * cfg.n_inner;  // Box-Muller pairs per restart
+      const long long np = (long long)nA * R * prp;
+      if (np > 0) {
+        k_copt_normals<<<grid_for(np, 256), 256, 0, s>>>(np, prp, k, per_restart, cfg.sigma, d_draws);
+        LAUNCH(ctx);
+        check_launch();
+      }
+    }
     int* d_oid = dalloc<int>(b_oid, (size_t)nA * kMaxK);
     double* d_oobj = dalloc<double>(b_oobj, (size_t)nA);
     int* d_oan = dalloc<int>(b_oan, (size_t)nA);
