@@ -48,10 +48,11 @@ UNIT = "valid grasps/s"
 
 
 def params_for(workload, batch=None):
+    import caller as lc
     import paper_2511_07418_b200 as lg
     w = WORKLOADS[workload]
     a = os.path.join(ROOT, "assets")
-    p = lg.parse_config(os.path.join(a, w["cfg"]), hand=os.path.join(a, w["hand"]),
+    p = lc.parse_config(os.path.join(a, w["cfg"]), hand=os.path.join(a, w["hand"]),
                         object=os.path.join(a, w["obj"]), batch=batch)
     p.want_trace = 0
     return p
@@ -173,9 +174,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import caller as lc
     import paper_2511_07418_b200 as lg
     p = params_for(args.workload, args.batch)
-    hand, patches, raw, _ = lg.prepare_inputs(p)
+    hand, patches, raw, _ = lc.prepare_inputs(p)
     vals = []
     for _ in range(args.warmup + args.steps):
         vals.append(cpu_baseline(args.workload, p.batch, args.sample_frac, hand, patches, raw, p))
@@ -199,6 +201,7 @@ def run_reference(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
+    import caller as lc
     import paper_2511_07418_b200 as lg
     from paper_2511_07418_b200 import dist as ldist
 
@@ -212,7 +215,7 @@ def run_b200(args):
     torch.cuda.set_device(dev)
 
     p = params_for(args.workload, args.batch)
-    hand, patches, raw, _ = lg.prepare_inputs(p)
+    hand, patches, raw, _ = lc.prepare_inputs(p)
     sp = ldist.shard_params(p, rank, world) if world > 1 else p
     ctx = lg.Context(local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

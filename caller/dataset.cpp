@@ -10,7 +10,7 @@
 #include <sstream>
 #include <stdexcept>
 
-#include "host.hpp"
+#include "caller.hpp"
 
 namespace lgh {
 

@@ -1,13 +1,15 @@
 /*
  * lg.h — C-ABI drop-in boundary of the B200-native Lightning Grasp forward pass.
  *
- * Everything the reference keeps on the caller side (URDF/mesh loaders, surface
- * sampling, patch decomposition, config parsing, the JSONL result format) is
- * exposed here as host functions so that a C++ caller can keep its own types
- * and hand flat, caller-owned SoA arrays across.  Everything on the hot path
- * (reference proj/src/pipeline.cpp:308-625 and the L2-L5 modules it calls)
- * runs on the GPU behind lg_field_build / lg_query_domains_batch /
- * lg_run_batch and the stage-level batch entry points.
+ * Everything on the hot path (reference proj/src/pipeline.cpp:308-625 and the
+ * L2-L5 modules it calls) runs on the GPU behind lg_run_batch, lg_field_build
+ * and the stage-level batch entry points below.  What the reference keeps on
+ * the caller side (load_hand, load_mesh, sample_surface, decompose_patches,
+ * parse_config, write_dataset — SURVEY.md 8(b)) stays with the caller, which
+ * hands flat, caller-owned SoA views across: lg_hand_desc, lg_visual_desc,
+ * lg_patches_desc, sample arrays and lg_run_params.  This library exports no
+ * loader of its own (the repository's stand-in caller is caller/, outside the
+ * product).
  *
  * Conventions:
  *   - every entry point returns an int status: LG_OK or a negative code that
@@ -46,9 +48,13 @@ extern "C" {
 
 #define LG_MAX_K 5          /* k_contacts range [2,5] (config.cpp:107-112) */
 #define LG_MAX_CONTACTS 6   /* k slots + at most one static contact       */
-#define LG_MAX_DOF 32
+#define LG_MAX_DOF 32       /* joint slots in the result records           */
 #define LG_MAX_GROUPS 32    /* reachability mask is one uint32 per sample */
-#define LG_MAX_LINKS 64
+/* Hands the device accepts (larger ones return LG_ERR_INVALID_ARGUMENT): */
+#define LG_DEVICE_MAX_DOF 24    /* actuated joints                        */
+#define LG_DEVICE_MAX_LINKS 32  /* links                                  */
+#define LG_DEVICE_MAX_PARTS 63  /* convex collision parts                 */
+#define LG_DEVICE_MAX_CHAIN 10  /* links on a root -> link chain          */
 
 /* Copies the calling thread's last error message; returns its length. */
 int lg_last_error(char* buf, size_t cap);
@@ -83,6 +89,16 @@ typedef struct lg_hand_desc {
   const double* part_planes; /* [*][4] (unit outward normal, offset) */
   const double* part_bounds; /* [n_parts][6] (min xyz, max xyz) */
 } lg_hand_desc;
+
+/* Visual meshes of the links (HandModel Link::visual, hand.hpp:27), link-local,
+ * CSR over links: the input of the hand's surface sampling (pipeline.cpp:277-285). */
+typedef struct lg_visual_desc {
+  int n_links;
+  const int* vert_off;  /* [n_links+1] */
+  const double* verts;  /* [*][3] */
+  const int* tri_off;   /* [n_links+1] */
+  const int* tris;      /* [*][3] vertex indices local to the link */
+} lg_visual_desc;
 
 /* ContactPatch list (reference contact_field.hpp:20-30); ids are dense. */
 typedef struct lg_patches_desc {
@@ -148,15 +164,6 @@ typedef struct lg_run_params {
   int want_trace; /* fill one lg_trace per (pass, candidate) */
 } lg_run_params;
 
-/* Fills the reference defaults (config.hpp:15-77). */
-void lg_run_params_default(lg_run_params* p);
-/* parse_config (config.cpp:339-401): defaults, then file (may be NULL), then
- * the non-NULL overrides; throws-equivalent LG_ERR_RUNTIME on bad input. */
-int lg_config_parse(const char* path, const char* hand, const char* object,
-                    const char* out, const long long* seed, const int* batch,
-                    const int* workers, lg_run_params* p);
-/* index_cache_key (config.cpp:403-417). */
-int lg_index_cache_key(const lg_run_params* p, uint64_t* key);
 
 /* ---- results ----------------------------------------------------------- */
 
@@ -239,62 +246,11 @@ long long lg_result_num_traces(const lg_result* r);
 const lg_trace* lg_result_traces(const lg_result* r);
 void lg_result_destroy(lg_result* r);
 
-/* ---- host side: loaders and caller-side steps (stay on the host) -------- */
-
-typedef struct lg_hand lg_hand;
-typedef struct lg_mesh lg_mesh;
-typedef struct lg_patches lg_patches;
 typedef struct lg_ctx lg_ctx;
+typedef struct lg_patches lg_patches;
 
-typedef struct lg_load_report {
-  long long triangles_read, triangles_kept, degenerate_dropped;
-} lg_load_report;
-
-/* load_hand (hand.cpp:265-414). */
-int lg_hand_load(const char* urdf_path, double scale, lg_hand** out);
-int lg_hand_export(const lg_hand* h, lg_hand_desc* out);
-int lg_hand_link_name(const lg_hand* h, int link, char* buf, size_t cap);
-/* dependency_groups (hand.cpp:515-552): group id per link (-1 static). */
-int lg_hand_groups(const lg_hand* h, int* group_of_link, int* n_groups);
-/* Visual mesh of one link (link-local). */
-int lg_hand_link_visual(const lg_hand* h, int link, lg_mesh** out);
-void lg_hand_destroy(lg_hand* h);
-
-/* load_mesh (mesh.cpp:161-167) and the primitive generators. */
-int lg_mesh_load(const char* path, lg_load_report* report, lg_mesh** out);
-int lg_mesh_box(double sx, double sy, double sz, lg_mesh** out);
-int lg_mesh_icosphere(double radius, int subdivisions, lg_mesh** out);
-int lg_mesh_cylinder(double radius, double length, int segments, lg_mesh** out);
-int lg_mesh_from_arrays(const double* verts, int n_verts, const int* tris,
-                        int n_tris, lg_mesh** out);
-int lg_mesh_scale(lg_mesh* m, double scale);
-int lg_mesh_info(const lg_mesh* m, int* n_verts, int* n_tris, double* area);
-int lg_mesh_arrays(const lg_mesh* m, const double** verts, const int** tris);
-int lg_mesh_save_obj(const lg_mesh* m, const char* path);
-void lg_mesh_destroy(lg_mesh* m);
-
-/* sample_surface (mesh.cpp:297-339). Two-call size query: pass out=NULL to
- * get the count in *n. */
-int lg_sample_surface(const lg_mesh* m, double samples_per_cm2, uint64_t seed,
-                      double* out, size_t cap, size_t* n);
+/* splitmix mix_seed (rng.hpp:25-28), the per-stream seed of every draw. */
 uint64_t lg_mix_seed(uint64_t seed, uint64_t a, uint64_t b);
-
-/* build_field's host steps (pipeline.cpp:277-285): per-link surface sampling
- * with stream 'hnds' and decompose_patches (contact_field.cpp:26-99). */
-int lg_hand_patches(const lg_hand* h, double samples_per_cm2,
-                    double patch_radius, uint64_t seed, int field_cap,
-                    lg_patches** out);
-/* The same patches with the hand's surface sampling, decompose_patches'
- * greedy cover and the field-point subsets on the GPU; identical output. */
-int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double samples_per_cm2,
-                           double patch_radius, uint64_t seed, int field_cap,
-                           lg_patches** out);
-int lg_patches_export(const lg_patches* p, lg_patches_desc* out);
-void lg_patches_destroy(lg_patches* p);
-
-/* write_dataset JSONL (dataset.cpp:23-56) and profile JSON (113-131). */
-int lg_write_dataset(const char* path, const lg_grasp* grasps, long long n);
-int lg_write_profile(const char* path, const lg_profile* p);
 
 /* ---- device side (sm_100a) ---------------------------------------------- */
 
@@ -303,6 +259,16 @@ typedef struct lg_field lg_field;
 int lg_device_count(int* n);
 int lg_ctx_create(int device, lg_ctx** out);
 void lg_ctx_destroy(lg_ctx* ctx);
+
+/* build_field's hand steps (pipeline.cpp:277-285) on the GPU: per-link
+ * sample_surface with stream 'hnds' (mesh.cpp:297-339), decompose_patches'
+ * greedy cover and field-point subsets (contact_field.cpp:26-99).  Output is
+ * identical to the reference's patches; read it with lg_patches_export. */
+int lg_hand_patches_device(lg_ctx* ctx, const lg_hand_desc* hand, const lg_visual_desc* visual,
+                           double samples_per_cm2, double patch_radius, uint64_t seed,
+                           int field_cap, lg_patches** out);
+int lg_patches_export(const lg_patches* p, lg_patches_desc* out);
+void lg_patches_destroy(lg_patches* p);
 
 /* ContactFieldIndex::build (contact_field.cpp:306-334) on the GPU. */
 int lg_field_build(lg_ctx* ctx, const lg_hand_desc* hand,
@@ -316,6 +282,9 @@ void lg_field_destroy(lg_field* f);
  * LG_OK) when the file is missing, malformed, or keyed differently — the
  * reference's std::nullopt. */
 int lg_field_save(lg_field* f, const char* path, uint64_t key);
+/* index_cache_key (config.cpp:403-417): the cache key of params (FNV-1a of
+ * the hand file named by params->hand and the index-shaping parameters). */
+int lg_index_cache_key(const lg_run_params* params, uint64_t* key);
 int lg_field_load(lg_ctx* ctx, const lg_hand_desc* hand, const char* path,
                   uint64_t key, lg_field** out);
 
@@ -398,7 +367,8 @@ int lg_validate_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_grasp* gra
  * "<grasp>\t<message>\n" line each, message text as validate.cpp words it.
  * Writes at most cap bytes (NUL-terminated) and the required size to
  * *needed; *n_issues receives the issue count. */
-int lg_validation_issues(const lg_hand* hand, const lg_grasp_check* checks, long long n,
+int lg_validation_issues(const char* const* joint_names, int n_links,
+                         const lg_grasp_check* checks, long long n,
                          const lg_run_params* p, char* buf, size_t cap, size_t* needed,
                          long long* n_issues);
 

@@ -271,6 +271,14 @@ struct ref_result {
   std::vector<lg_grasp> grasps;
 };
 
+struct ref_hand {
+  HandModel model;
+  DependencyGroups groups;
+  FlatHand flat;
+  std::vector<int> vis_vert_off{0}, vis_tri_off{0}, vis_tris, group_of_link;
+  std::vector<double> vis_verts;
+};
+
 struct ref_field {
   ContactFieldIndex idx;
   std::vector<int> patch_link, box_off{0};
@@ -395,6 +403,50 @@ int ref_link_visual(const ref_inputs* in, int link, int* nv, int* nt, double* ve
 int ref_index_cache_key(const ref_inputs* in, uint64_t* key) {
   return guard([&] { *key = index_cache_key(in->cfg); });
 }
+
+// ---- load_hand (hand.cpp:124-273) alone: the reference's HandModel (with
+// its quickhull collision parts) flattened, its visual meshes and its
+// dependency groups (hand.cpp:374-411).  Used to write the caller-side hand
+// fixtures (tools/prepare_hands.py).
+int ref_hand_load(const char* urdf, double scale, ref_hand** out) {
+  return guard([&] {
+    auto h = std::make_unique<ref_hand>();
+    h->model = load_hand(urdf, scale);
+    h->groups = dependency_groups(h->model);
+    h->flat.build(h->model);
+    for (std::size_t l = 0; l < h->model.links.size(); ++l) {
+      const TriMesh& m = h->model.links[l].visual;
+      for (const Vec3& v : m.vertices) h->vis_verts.insert(h->vis_verts.end(), {v.x(), v.y(), v.z()});
+      for (const auto& t : m.triangles) h->vis_tris.insert(h->vis_tris.end(), {t[0], t[1], t[2]});
+      h->vis_vert_off.push_back(static_cast<int>(h->vis_verts.size() / 3));
+      h->vis_tri_off.push_back(static_cast<int>(h->vis_tris.size() / 3));
+      h->group_of_link.push_back(h->groups.group_of(static_cast<int>(l)));
+    }
+    *out = h.release();
+  });
+}
+int ref_hand_desc_of(const ref_hand* h, lg_hand_desc* d) {
+  return guard([&] { *d = h->flat.d; });
+}
+// visual meshes as CSR over links; group id per link; counts first.
+int ref_hand_visual(const ref_hand* h, const int** vert_off, const double** verts, const int** tri_off,
+                    const int** tris, const int** group_of_link, int* n_groups) {
+  return guard([&] {
+    *vert_off = h->vis_vert_off.data();
+    *verts = h->vis_verts.data();
+    *tri_off = h->vis_tri_off.data();
+    *tris = h->vis_tris.data();
+    *group_of_link = h->group_of_link.data();
+    *n_groups = static_cast<int>(h->groups.groups.size());
+  });
+}
+int ref_hand_link_name(const ref_hand* h, int link, char* buf, size_t cap) {
+  return guard([&] { std::snprintf(buf, cap, "%s", h->model.links.at(link).name.c_str()); });
+}
+int ref_hand_joint_name(const ref_hand* h, int link, char* buf, size_t cap) {
+  return guard([&] { std::snprintf(buf, cap, "%s", h->model.links.at(link).joint_name.c_str()); });
+}
+void ref_hand_destroy(ref_hand* h) { delete h; }
 
 // ---- the whole forward pass: the reference's own run_batch(cfg)
 int ref_run_batch(const ref_inputs* in, ref_result** out) {

@@ -49,6 +49,12 @@ def lib():
             "ref_link_visual": (C.c_int, [vp, C.c_int, ip, ip, dp, ip]),
             "ref_index_cache_key": (C.c_int, [vp, P(u64)]),
             "ref_run_batch": (C.c_int, [vp, P(vp)]),
+            "ref_hand_load": (C.c_int, [C.c_char_p, C.c_double, P(vp)]),
+            "ref_hand_desc_of": (C.c_int, [vp, P(A.HandDesc)]),
+            "ref_hand_visual": (C.c_int, [vp, P(ip), P(dp), P(ip), P(ip), P(ip), ip]),
+            "ref_hand_link_name": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t]),
+            "ref_hand_joint_name": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t]),
+            "ref_hand_destroy": (None, [vp]),
             "ref_result_num_grasps": (C.c_longlong, [vp]),
             "ref_result_grasps": (vp, [vp]),
             "ref_result_profile": (C.c_int, [vp, P(A.Profile)]),
@@ -174,6 +180,60 @@ class RefInputs:
 
     def field(self, N=0):
         return RefField(self, N)
+
+
+def load_hand_arrays(urdf, scale=1.0):
+    """The reference's load_hand + dependency_groups as plain numpy arrays
+    (lg_hand_desc fields, visual meshes, link names, group ids)."""
+    L = lib()
+    h = C.c_void_p()
+    check(L.ref_hand_load(str(urdf).encode(), float(scale), C.byref(h)))
+    try:
+        d = A.HandDesc()
+        check(L.ref_hand_desc_of(h, C.byref(d)))
+        nl, npart = d.n_links, d.n_parts
+
+        def arr(ptr, n, dt):
+            return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt).copy() if n else np.zeros(0, dt)
+
+        out = {"n_links": nl, "dof": d.dof, "root": d.root,
+               "parent": arr(d.parent, nl, np.int32), "joint_type": arr(d.joint_type, nl, np.int32),
+               "joint_index": arr(d.joint_index, nl, np.int32),
+               "topo_order": arr(d.topo_order, nl, np.int32),
+               "origin_R": arr(d.origin_R, 9 * nl, np.float64),
+               "origin_t": arr(d.origin_t, 3 * nl, np.float64),
+               "axis": arr(d.axis, 3 * nl, np.float64),
+               "limit_lo": arr(d.limit_lo, nl, np.float64), "limit_hi": arr(d.limit_hi, nl, np.float64),
+               "part_link": arr(d.part_link, npart, np.int32),
+               "part_vert_off": arr(d.part_vert_off, npart + 1, np.int32),
+               "part_tri_off": arr(d.part_tri_off, npart + 1, np.int32),
+               "part_plane_off": arr(d.part_plane_off, npart + 1, np.int32)}
+        out["part_verts"] = arr(d.part_verts, 3 * int(out["part_vert_off"][-1]), np.float64)
+        out["part_tris"] = arr(d.part_tris, 3 * int(out["part_tri_off"][-1]), np.int32)
+        out["part_planes"] = arr(d.part_planes, 4 * int(out["part_plane_off"][-1]), np.float64)
+        out["part_bounds"] = arr(d.part_bounds, 6 * npart, np.float64)
+        vo, vv, to, tt, gl = A.ip(), A.dp(), A.ip(), A.ip(), A.ip()
+        ng = C.c_int(0)
+        check(L.ref_hand_visual(h, C.byref(vo), C.byref(vv), C.byref(to), C.byref(tt), C.byref(gl),
+                                C.byref(ng)))
+        out["vis_vert_off"] = arr(vo, nl + 1, np.int32)
+        out["vis_tri_off"] = arr(to, nl + 1, np.int32)
+        out["vis_verts"] = arr(vv, 3 * int(out["vis_vert_off"][-1]), np.float64)
+        out["vis_tris"] = arr(tt, 3 * int(out["vis_tri_off"][-1]), np.int32)
+        out["group_of_link"] = arr(gl, nl, np.int32)
+        out["n_groups"] = ng.value
+        names, jnames = [], []
+        for l in range(nl):
+            buf = C.create_string_buffer(256)
+            check(L.ref_hand_link_name(h, l, buf, len(buf)))
+            names.append(buf.value.decode())
+            check(L.ref_hand_joint_name(h, l, buf, len(buf)))
+            jnames.append(buf.value.decode())
+        out["link_names"] = np.array(names)
+        out["joint_names"] = np.array(jnames)
+        return out
+    finally:
+        L.ref_hand_destroy(h)
 
 
 class RefResult:

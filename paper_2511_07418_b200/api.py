@@ -43,34 +43,10 @@ def lib():
     sig = {
         "lg_last_error": (C.c_int, [C.c_char_p, C.c_size_t]),
         "lg_version": (C.c_char_p, []),
-        "lg_run_params_default": (None, [P(A.RunParams)]),
-        "lg_config_parse": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
-                                      P(C.c_longlong), P(C.c_int), P(C.c_int), P(A.RunParams)]),
         "lg_index_cache_key": (C.c_int, [P(A.RunParams), P(C.c_uint64)]),
         "lg_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
-        "lg_hand_load": (C.c_int, [C.c_char_p, C.c_double, P(vp)]),
-        "lg_hand_export": (C.c_int, [vp, P(A.HandDesc)]),
-        "lg_hand_link_name": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t]),
-        "lg_hand_groups": (C.c_int, [vp, A.ip, A.ip]),
-        "lg_hand_link_visual": (C.c_int, [vp, C.c_int, P(vp)]),
-        "lg_hand_destroy": (None, [vp]),
-        "lg_mesh_load": (C.c_int, [C.c_char_p, P(A.LoadReport), P(vp)]),
-        "lg_mesh_box": (C.c_int, [C.c_double, C.c_double, C.c_double, P(vp)]),
-        "lg_mesh_icosphere": (C.c_int, [C.c_double, C.c_int, P(vp)]),
-        "lg_mesh_cylinder": (C.c_int, [C.c_double, C.c_double, C.c_int, P(vp)]),
-        "lg_mesh_from_arrays": (C.c_int, [A.dp, C.c_int, A.ip, C.c_int, P(vp)]),
-        "lg_mesh_scale": (C.c_int, [vp, C.c_double]),
-        "lg_mesh_info": (C.c_int, [vp, A.ip, A.ip, A.dp]),
-        "lg_mesh_arrays": (C.c_int, [vp, P(A.dp), P(A.ip)]),
-        "lg_mesh_save_obj": (C.c_int, [vp, C.c_char_p]),
-        "lg_mesh_destroy": (None, [vp]),
-        "lg_sample_surface": (C.c_int, [vp, C.c_double, C.c_uint64, A.dp, C.c_size_t,
-                                        P(C.c_size_t)]),
-        "lg_hand_patches": (C.c_int, [vp, C.c_double, C.c_double, C.c_uint64, C.c_int, P(vp)]),
         "lg_patches_export": (C.c_int, [vp, P(A.PatchesDesc)]),
         "lg_patches_destroy": (None, [vp]),
-        "lg_write_dataset": (C.c_int, [C.c_char_p, P(A.Grasp), C.c_longlong]),
-        "lg_write_profile": (C.c_int, [C.c_char_p, P(A.Profile)]),
         "lg_device_count": (C.c_int, [A.ip]),
         "lg_ctx_create": (C.c_int, [C.c_int, P(vp)]),
         "lg_ctx_destroy": (None, [vp]),
@@ -80,12 +56,16 @@ def lib():
         "lg_field_save": (C.c_int, [vp, C.c_char_p, C.c_uint64]),
         "lg_field_load": (C.c_int, [vp, P(A.HandDesc), C.c_char_p, C.c_uint64, P(vp)]),
         "lg_field_destroy": (None, [vp]),
-        "lg_hand_patches_device": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_uint64, C.c_int,
-                                             P(vp)]),
+        "lg_hand_patches_device": (C.c_int, [vp, P(A.HandDesc), vp, C.c_double, C.c_double,
+                                             C.c_uint64, C.c_int, P(vp)]),
+        "lg_patches_export": (C.c_int, [vp, P(A.PatchesDesc)]),
+        "lg_patches_destroy": (None, [vp]),
+        "lg_index_cache_key": (C.c_int, [P(A.RunParams), P(C.c_uint64)]),
         "lg_validate_batch": (C.c_int, [vp, P(A.HandDesc), vp, C.c_longlong, A.dp, C.c_int, A.ip,
                                         C.c_int, A.dp, C.c_int, P(A.RunParams), vp]),
-        "lg_validation_issues": (C.c_int, [vp, vp, C.c_longlong, P(A.RunParams), C.c_char_p,
-                                           C.c_size_t, P(C.c_size_t), P(C.c_longlong)]),
+        "lg_validation_issues": (C.c_int, [P(C.c_char_p), C.c_int, vp, C.c_longlong,
+                                           P(A.RunParams), C.c_char_p, C.c_size_t, P(C.c_size_t),
+                                           P(C.c_longlong)]),
         "lg_query_domains_batch": (C.c_int, [vp, vp, A.ip, A.dp, C.c_int, A.dp, C.c_int,
                                              C.c_double, P(C.c_uint32), A.dp]),
         "lg_preprocess": (C.c_int, [vp, A.dp, C.c_int, C.c_double, C.c_double,
@@ -144,150 +124,15 @@ def mix_seed(seed, a, b=0):
     return int(lib().lg_mix_seed(C.c_uint64(seed), C.c_uint64(a), C.c_uint64(b)))
 
 
-# ------------------------------------------------------------------ meshes
-class Mesh:
-    """TriMesh (mesh.hpp:13-21), owned by the library."""
-
-    def __init__(self, handle, report=None):
-        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
-        self.report = report
-
-    def __del__(self):
-        if getattr(self, "_h", None) and _LIB is not None:
-            _LIB.lg_mesh_destroy(self._h)
-            self._h = None
-
-    @staticmethod
-    def _make(fn, *args):
-        h = C.c_void_p()
-        check(fn(*args, C.byref(h)))
-        return Mesh(h)
-
-    @classmethod
-    def box(cls, size):
-        return cls._make(lib().lg_mesh_box, *map(float, size))
-
-    @classmethod
-    def icosphere(cls, radius, subdivisions):
-        return cls._make(lib().lg_mesh_icosphere, float(radius), int(subdivisions))
-
-    @classmethod
-    def cylinder(cls, radius, length, segments=24):
-        return cls._make(lib().lg_mesh_cylinder, float(radius), float(length), int(segments))
-
-    @classmethod
-    def from_arrays(cls, verts, tris):
-        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 3)
-        t = np.ascontiguousarray(tris, dtype=np.int32).reshape(-1, 3)
-        return cls._make(lib().lg_mesh_from_arrays, _dp(v), len(v), _ip(t), len(t))
-
-    def info(self):
-        nv, nt, area = C.c_int(), C.c_int(), C.c_double()
-        check(lib().lg_mesh_info(self._h, C.byref(nv), C.byref(nt), C.byref(area)))
-        return nv.value, nt.value, area.value
-
-    def arrays(self):
-        nv, nt, _ = self.info()
-        v, t = A.dp(), A.ip()
-        check(lib().lg_mesh_arrays(self._h, C.byref(v), C.byref(t)))
-        verts = np.ctypeslib.as_array(v, shape=(nv * 3,)).reshape(nv, 3).copy() if nv else np.zeros((0, 3))
-        tris = np.ctypeslib.as_array(t, shape=(nt * 3,)).reshape(nt, 3).copy() if nt else np.zeros((0, 3), np.int32)
-        return verts, tris
-
-    def scale(self, s):
-        check(lib().lg_mesh_scale(self._h, float(s)))
-        return self
-
-    def save_obj(self, path):
-        check(lib().lg_mesh_save_obj(self._h, path.encode()))
+def index_cache_key(params):
+    """index_cache_key (config.cpp:403-417), the GGCF cache key."""
+    k = C.c_uint64()
+    check(lib().lg_index_cache_key(C.byref(params), C.byref(k)))
+    return k.value
 
 
-def load_mesh(path):
-    """load_mesh (mesh.cpp:161-167); returns (Mesh, LoadReport dict)."""
-    rep = A.LoadReport()
-    h = C.c_void_p()
-    check(lib().lg_mesh_load(str(path).encode(), C.byref(rep), C.byref(h)))
-    m = Mesh(h)
-    m.report = dict(triangles_read=rep.triangles_read, triangles_kept=rep.triangles_kept,
-                    degenerate_dropped=rep.degenerate_dropped)
-    return m
-
-
-def sample_surface(mesh, samples_per_cm2, seed):
-    """sample_surface (mesh.cpp:297-339) -> float64 array (n, 6) = (p, n)."""
-    L = lib()
-    n = C.c_size_t()
-    check(L.lg_sample_surface(mesh._h, float(samples_per_cm2), C.c_uint64(seed), None, 0,
-                              C.byref(n)))
-    out = np.zeros((n.value, 6), dtype=np.float64)
-    check(L.lg_sample_surface(mesh._h, float(samples_per_cm2), C.c_uint64(seed), _dp(out),
-                              n.value, C.byref(n)))
-    return out
-
-
-# -------------------------------------------------------------------- hand
-class HandModel:
-    """HandModel (hand.hpp:37-46) with its flat lg_hand_desc view."""
-
-    def __init__(self, handle):
-        self._h = handle
-        self.desc = A.HandDesc()
-        check(lib().lg_hand_export(self._h, C.byref(self.desc)))
-
-    def __del__(self):
-        if getattr(self, "_h", None) and _LIB is not None:
-            _LIB.lg_hand_destroy(self._h)
-            self._h = None
-
-    @property
-    def n_links(self):
-        return self.desc.n_links
-
-    @property
-    def dof(self):
-        return self.desc.dof
-
-    def link_name(self, l):
-        buf = C.create_string_buffer(256)
-        check(lib().lg_hand_link_name(self._h, int(l), buf, 256))
-        return buf.value.decode()
-
-    def groups(self):
-        """dependency_groups (hand.cpp:515-552): (group id per link, n_groups)."""
-        g = np.zeros(self.n_links, dtype=np.int32)
-        n = C.c_int()
-        check(lib().lg_hand_groups(self._h, _ip(g), C.byref(n)))
-        return g, n.value
-
-    def link_visual(self, l):
-        h = C.c_void_p()
-        check(lib().lg_hand_link_visual(self._h, int(l), C.byref(h)))
-        return Mesh(h)
-
-    def limits(self):
-        d = self.desc
-        lo = np.zeros(d.dof)
-        hi = np.zeros(d.dof)
-        for l in range(d.n_links):
-            j = d.joint_index[l]
-            if j >= 0:
-                lo[j], hi[j] = d.limit_lo[l], d.limit_hi[l]
-        return lo, hi
-
-    def mid_config(self):
-        lo, hi = self.limits()
-        return 0.5 * (lo + hi)
-
-
-def load_hand(path, scale=1.0):
-    """load_hand (hand.cpp:265-414)."""
-    h = C.c_void_p()
-    check(lib().lg_hand_load(str(path).encode(), float(scale), C.byref(h)))
-    return HandModel(h)
-
-
-class Patches:
-    """decompose_patches output (contact_field.hpp:20-36) as lg_patches_desc."""
+class DevicePatches:
+    """decompose_patches output built on the device (lg_hand_patches_device)."""
 
     def __init__(self, handle):
         self._h = handle
@@ -308,48 +153,15 @@ class Patches:
 
 
 def hand_patches_device(ctx, hand, samples_per_cm2, patch_radius, seed, field_cap=8):
-    """hand_patches on the GPU: the per-link surface sampling, the greedy
-    cover and the field-point subsets (identical patches)."""
+    """build_field's hand steps (pipeline.cpp:277-285) on the GPU: the
+    per-link surface sampling, the greedy cover and the field-point subsets
+    (identical patches).  `hand` carries .desc (lg_hand_desc) and
+    .visual_desc (lg_visual_desc)."""
     h = C.c_void_p()
-    check(lib().lg_hand_patches_device(ctx._h, hand._h, float(samples_per_cm2),
-                                       float(patch_radius), C.c_uint64(seed), int(field_cap),
-                                       C.byref(h)))
-    return Patches(h)
-
-
-def hand_patches(hand, samples_per_cm2, patch_radius, seed, field_cap=8):
-    """build_field's host steps (pipeline.cpp:277-285): per-link samples with
-    stream 'hnds' then decompose_patches (contact_field.cpp:26-99)."""
-    h = C.c_void_p()
-    check(lib().lg_hand_patches(hand._h, float(samples_per_cm2), float(patch_radius),
-                                C.c_uint64(seed), int(field_cap), C.byref(h)))
-    return Patches(h)
-
-
-# ------------------------------------------------------------------ config
-def default_config():
-    p = A.RunParams()
-    lib().lg_run_params_default(C.byref(p))
-    return p
-
-
-def parse_config(path=None, hand=None, object=None, out=None, seed=None, batch=None,
-                 workers=None):
-    """parse_config (config.cpp:339-401) with CLI-style overrides."""
-    p = A.RunParams()
-    enc = lambda s: None if s is None else str(s).encode()
-    sd = None if seed is None else C.byref(C.c_longlong(int(seed)))
-    bt = None if batch is None else C.byref(C.c_int(int(batch)))
-    wk = None if workers is None else C.byref(C.c_int(int(workers)))
-    check(lib().lg_config_parse(enc(path), enc(hand), enc(object), enc(out), sd, bt, wk,
-                                C.byref(p)))
-    return p
-
-
-def index_cache_key(params):
-    k = C.c_uint64()
-    check(lib().lg_index_cache_key(C.byref(params), C.byref(k)))
-    return k.value
+    check(lib().lg_hand_patches_device(ctx._h, C.byref(hand.desc), C.byref(hand.visual_desc),
+                                       float(samples_per_cm2), float(patch_radius),
+                                       C.c_uint64(seed), int(field_cap), C.byref(h)))
+    return DevicePatches(h)
 
 
 # ------------------------------------------------------------------ device
@@ -509,7 +321,7 @@ def validate_batch(ctx, hand, grasps, mesh, samples, params):
     """validate_dataset (validate.cpp:56-175) on the GPU: per-grasp checks
     (structured array of lg_grasp_check)."""
     g = np.ascontiguousarray(np.asarray(grasps).astype(A.grasp_dtype()))
-    v, t = mesh.arrays()
+    v, t = mesh.arrays() if hasattr(mesh, "arrays") else mesh
     v = np.ascontiguousarray(v, dtype=np.float64)
     t = np.ascontiguousarray(t, dtype=np.int32)
     s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
@@ -520,48 +332,23 @@ def validate_batch(ctx, hand, grasps, mesh, samples, params):
     return out
 
 
-def validation_issues(hand, checks, params):
+def validation_issues(joint_names, checks, params):
     """ValidationReport.issues as [(grasp, message)], texts as validate.cpp
-    words them."""
+    words them; joint_names = joint name per link (Link::joint_name)."""
     c = np.ascontiguousarray(checks)
+    names = (C.c_char_p * max(1, len(joint_names)))(*[str(n).encode() for n in joint_names])
     need, cnt = C.c_size_t(0), C.c_longlong(0)
-    check(lib().lg_validation_issues(hand._h, c.ctypes.data_as(C.c_void_p), len(c),
+    check(lib().lg_validation_issues(names, len(joint_names), c.ctypes.data_as(C.c_void_p), len(c),
                                      C.byref(params), None, 0, C.byref(need), C.byref(cnt)))
     buf = C.create_string_buffer(need.value)
-    check(lib().lg_validation_issues(hand._h, c.ctypes.data_as(C.c_void_p), len(c),
-                                     C.byref(params), buf, need.value, C.byref(need), C.byref(cnt)))
+    check(lib().lg_validation_issues(names, len(joint_names), c.ctypes.data_as(C.c_void_p), len(c),
+                                     C.byref(params), buf, need.value, C.byref(need),
+                                     C.byref(cnt)))
     out = []
     for line in buf.value.decode().splitlines():
         gi, what = line.split("\t", 1)
         out.append((int(gi), what))
     return out
-
-
-def write_dataset(path, grasps):
-    """write_dataset (dataset.cpp:50-56): JSONL in the reference format."""
-    g = np.ascontiguousarray(grasps)
-    check(lib().lg_write_dataset(str(path).encode(), g.ctypes.data_as(C.POINTER(A.Grasp)),
-                                 len(g)))
-
-
-def write_profile(path, profile_struct):
-    check(lib().lg_write_profile(str(path).encode(), C.byref(profile_struct)))
-
-
-TAG_OBJECT_SAMPLES = 0x6F626A73  # pipeline.cpp:19
-
-
-def prepare_inputs(params):
-    """Caller-side steps of run_batch/build_field (pipeline.cpp:273-330):
-    load the hand and its patches, load + scale the object, sample it."""
-    hand = load_hand(params.hand.decode(), params.hand_scale)
-    patches = hand_patches(hand, params.samples_per_cm2, params.patch_radius, params.seed,
-                           params.field_points_per_patch)
-    mesh = load_mesh(params.object.decode())
-    if params.object_scale != 1.0:
-        mesh.scale(params.object_scale)
-    raw = sample_surface(mesh, params.samples_per_cm2, mix_seed(params.seed, TAG_OBJECT_SAMPLES))
-    return hand, patches, raw, mesh
 
 
 def _bind_batch_sigs():

@@ -24,7 +24,6 @@
 #include "dev_post.cuh"
 #include "dev_validate.cuh"
 #include "dev_patches.cuh"
-#include "../host/capi_types.hpp"
 
 using namespace lgd;
 
@@ -1211,11 +1210,61 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
   });
 }
 
-int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double spc, double radius,
-                           uint64_t seed, int cap, lg_patches** out) {
+// decompose_patches output (contact_field.hpp:20-30) owned by the library.
+struct lg_patches {
+  std::vector<int> link, point_off, fp_off, fps;
+  std::vector<double> pts, nrm;
+};
+
+namespace {
+// TriMesh face quantities (mesh.cpp:16-31) on one link's visual mesh.
+struct VisMesh {
+  const lg_visual_desc* d;
+  int l;
+  V3 vert(int t, int c) const {
+    const int v = d->vert_off[l] + d->tris[3 * (d->tri_off[l] + t) + c];
+    return v3_load(d->verts + 3 * v);
+  }
+  int ntri() const { return d->tri_off[l + 1] - d->tri_off[l]; }
+  int nvert() const { return d->vert_off[l + 1] - d->vert_off[l]; }
+  V3 face_normal(int t) const {
+    V3 n = cross(sub(vert(t, 1), vert(t, 0)), sub(vert(t, 2), vert(t, 0)));
+    double len = norm(n);
+    if (len < 1e-300) return v3(0, 0, 1);
+    return divs(n, len);
+  }
+  double face_area(int t) const {
+    return 0.5 * norm(cross(sub(vert(t, 1), vert(t, 0)), sub(vert(t, 2), vert(t, 0))));
+  }
+  double surface_area() const {
+    double a = 0.0;
+    for (int t = 0; t < ntri(); ++t) a += face_area(t);
+    return a;
+  }
+};
+}  // namespace
+
+int lg_patches_export(const lg_patches* p, lg_patches_desc* d) {
   return lgc::guard([&] {
-    if (!ctx || !hand || !out) throw std::invalid_argument("lg_hand_patches_device: null argument");
-    const auto& H = hand->h;
+    if (!p || !d) throw std::invalid_argument("lg_patches_export: null argument");
+    d->n_patches = (int)p->link.size();
+    d->link = p->link.data();
+    d->point_off = p->point_off.data();
+    d->points = p->pts.data();
+    d->normals = p->nrm.data();
+    d->fp_off = p->fp_off.data();
+    d->field_points = p->fps.data();
+  });
+}
+void lg_patches_destroy(lg_patches* p) { delete p; }
+
+int lg_hand_patches_device(lg_ctx* ctx, const lg_hand_desc* hand, const lg_visual_desc* visual,
+                           double spc, double radius, uint64_t seed, int cap, lg_patches** out) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !visual || !out)
+      throw std::invalid_argument("lg_hand_patches_device: null argument");
+    if (visual->n_links != hand->n_links)
+      throw std::invalid_argument("decompose_patches: per-link sample mismatch");
     use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     // per-link hand samples, stream 'hnds' (pipeline.cpp:277-285), on the
@@ -1225,30 +1274,30 @@ int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double spc, double 
     std::vector<long long> off{0};
     std::vector<SampleSeg> segs;
     std::vector<double> corners, fn, cum;
-    for (size_t l = 0; l < H.links.size(); ++l) {
-      const lgh::Mesh& m = H.links[l].visual;
-      if (m.verts.empty() || m.tris.empty()) continue;
+    for (int l = 0; l < hand->n_links; ++l) {
+      VisMesh m{visual, l};
+      if (m.nvert() == 0 || m.ntri() == 0) continue;
       size_t count = (size_t)std::llround(m.surface_area() * 1e4 * spc);
       if (count == 0) count = 1;
       SampleSeg sg;
       sg.tri0 = (long long)cum.size();
       sg.s0 = off.back();
-      sg.ntri = (int)m.tris.size();
+      sg.ntri = m.ntri();
       sg.count = (int)count;
-      sg.seed = lgm::mix_seed(seed, 0x686e6473ull, l);
+      sg.seed = lgm::mix_seed(seed, 0x686e6473ull, (uint64_t)l);
       double acc = 0.0;
-      for (int t = 0; t < (int)m.tris.size(); ++t) {
+      for (int t = 0; t < m.ntri(); ++t) {
         acc += m.face_area(t);
         cum.push_back(acc);
         for (int c = 0; c < 3; ++c) {
-          const V3& v = m.verts[m.tris[t][c]];
+          const V3 v = m.vert(t, c);
           corners.insert(corners.end(), {v.x, v.y, v.z});
         }
         V3 nn = m.face_normal(t);
         fn.insert(fn.end(), {nn.x, nn.y, nn.z});
       }
       segs.push_back(sg);
-      seg_link.push_back((int)l);
+      seg_link.push_back(l);
       off.push_back(off.back() + (long long)count);
     }
     if (radius <= 0.0 || cap < 1) throw std::invalid_argument("decompose_patches: bad radius or cap");
@@ -1290,7 +1339,7 @@ int lg_hand_patches_device(lg_ctx* ctx, const lg_hand* hand, double spc, double 
     std::vector<int> msize, fp_off{0};
     auto* P = new lg_patches;
     std::unique_ptr<lg_patches> own(P);
-    lgh::Patches& R = P->p;
+    lg_patches& R = *P;
     R.point_off.push_back(0);
     R.fp_off.push_back(0);
     for (int b = 0; b < nseg; ++b) {

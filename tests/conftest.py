@@ -38,18 +38,21 @@ def asset(*parts):
 
 @pytest.fixture(scope="session")
 def four_finger():
+    import caller as lc
     import paper_2511_07418_b200 as lg
-    return lg.load_hand(asset("hands", "four_finger.urdf"))
+    return lc.load_hand(asset("hands", "four_finger.urdf"))
 
 
 @pytest.fixture(scope="session")
 def two_finger():
+    import caller as lc
     import paper_2511_07418_b200 as lg
-    return lg.load_hand(asset("hands", "two_finger.urdf"))
+    return lc.load_hand(asset("hands", "two_finger.urdf"))
 
 
 @pytest.fixture(scope="session")
 def ctx():
+    import caller as lc
     import paper_2511_07418_b200 as lg
     c = lg.Context(0)
     yield c
@@ -58,8 +61,9 @@ def ctx():
 
 def cfg1(batch=64, passes=1, obj="sphere_r030.obj", hand="four_finger", **over):
     """Config 1: bundled hand + primitive object, reference cfg."""
+    import caller as lc
     import paper_2511_07418_b200 as lg
-    p = lg.parse_config(asset("configs", f"{hand}.cfg"), hand=asset("hands", f"{hand}.urdf"),
+    p = lc.parse_config(asset("configs", f"{hand}.cfg"), hand=asset("hands", f"{hand}.urdf"),
                         object=asset("objects", obj), batch=batch)
     p.passes = passes
     p.want_trace = 1

@@ -10,6 +10,7 @@ import os
 import numpy as np
 import pytest
 
+import caller as lc
 import paper_2511_07418_b200 as lg
 from oracle import orc_py as orc
 from conftest import cfg1, mismatched_fields
@@ -17,7 +18,7 @@ import ggcf
 
 
 def _oracle_field(p, N=64, C=64):
-    hand, patches, _, _ = lg.prepare_inputs(p)
+    hand, patches, _, _ = lc.prepare_inputs(p)
     return hand, patches, orc.OrcField(hand.desc, patches.desc, N, p.box_width, p.seed, C)
 
 
@@ -84,7 +85,7 @@ def test_cache_key_tracks_config():  # config.cpp:403-417
 @pytest.mark.parametrize("hand_name,N,C", [("four_finger", 256, 256), ("two_finger", 64, 64)])
 def test_device_file_bytes_equal_oracle(ctx, tmp_path, hand_name, N, C):
     p = cfg1(hand=hand_name)
-    hand, patches, _, _ = lg.prepare_inputs(p)
+    hand, patches, _, _ = lc.prepare_inputs(p)
     key = lg.index_cache_key(p)
     fd = lg.ContactFieldIndex.build(ctx, hand, patches, N, p.box_width, p.seed, C)
     fo = orc.OrcField(hand.desc, patches.desc, N, p.box_width, p.seed, C)
@@ -106,7 +107,7 @@ def test_device_file_bytes_equal_oracle(ctx, tmp_path, hand_name, N, C):
     # a loaded index answers queries exactly like the built one
     gl, _ = hand.groups()
     gop = gl[patches.link_of_patch()]
-    _, _, raw_s, _ = lg.prepare_inputs(p)
+    _, _, raw_s, _ = lc.prepare_inputs(p)
     poses = np.tile(np.concatenate([np.eye(3).ravel(), [0, 0, 0.05]]), (4, 1))
     poses[:, 9:] += np.random.default_rng(3).normal(scale=0.01, size=(4, 3))
     assert np.array_equal(lg.query_domains_batch(ctx, ld, gop, raw_s, poses, p.theta_hit),
@@ -118,7 +119,7 @@ def test_run_batch_cache_mode(tmp_path):
     p = cfg1(batch=96)
     p.cache = 1
     p.out = os.fsencode(str(tmp_path / "out"))
-    hand, patches, raw, _ = lg.prepare_inputs(p)
+    hand, patches, raw, _ = lc.prepare_inputs(p)
     ctx = lg.Context(0)
     first = lg.run_batch(ctx, hand, patches, raw, p)
     assert first.profile["index_from_cache"] == 0

@@ -23,6 +23,7 @@ def _worker(rank, world, port, outdir):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch.distributed as dist
+    import caller as lc
     import paper_2511_07418_b200 as lg
     from paper_2511_07418_b200 import dist as ldist
     from oracle import orc_py as orc
@@ -32,7 +33,7 @@ def _worker(rank, world, port, outdir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     p = mk(batch=20, passes=2, field_configs=40)
-    hand, patches, raw, _ = lg.prepare_inputs(p)
+    hand, patches, raw, _ = lc.prepare_inputs(p)
     sp = ldist.shard_params(p, rank, world)
     r = orc.run_batch(hand.desc, patches.desc, raw, sp, workers=1)
     g = ldist.merge_grasps(ldist.gather_records(r.grasps))
@@ -45,6 +46,7 @@ def _worker(rank, world, port, outdir):
 
 def test_seed_sharding_is_result_invariant(tmp_path):
     import torch.multiprocessing as mp
+    import caller as lc
     import paper_2511_07418_b200 as lg
     from oracle import orc_py as orc
 
@@ -53,7 +55,7 @@ def test_seed_sharding_is_result_invariant(tmp_path):
     g = np.load(tmp_path / "grasps.npy")
     t = np.load(tmp_path / "traces.npy")
     p = cfg1(batch=20, passes=2, field_configs=40)
-    hand, patches, raw, _ = lg.prepare_inputs(p)
+    hand, patches, raw, _ = lc.prepare_inputs(p)
     full = orc.run_batch(hand.desc, patches.desc, raw, p, workers=2)
     # traces: rank order = (rank, pass, c); reorder by (pass, c) before comparing
     order = np.lexsort((t["c"], t["pass_"]))

@@ -9,6 +9,7 @@ every grasp the pipeline marks valid passes validation."""
 import numpy as np
 import pytest
 
+import caller as lc
 import paper_2511_07418_b200 as lg
 from oracle import orc_py as orc
 from conftest import cfg1, mismatched_fields
@@ -17,7 +18,7 @@ from conftest import cfg1, mismatched_fields
 def _inputs(batch=96):
     p = cfg1(batch=batch)
     p.want_trace = 0
-    hand, patches, raw, mesh = lg.prepare_inputs(p)
+    hand, patches, raw, mesh = lc.prepare_inputs(p)
     return p, hand, patches, raw, mesh
 
 
@@ -47,14 +48,14 @@ def test_oracle_validation_messages():
     assert len(ref.grasps) > 0
     v, t = mesh.arrays()
     checks = orc.validate(hand.desc, ref.grasps, v, t, raw, p)
-    issues = lg.validation_issues(hand, checks, p)
+    issues = lg.validation_issues(hand.joint_names, checks, p)
     # every grasp the pipeline flags valid passes the independent check
     flagged = set(gi for gi, _ in issues)
     for gi, g in enumerate(ref.grasps):
         if g["penetration_free"] and g["stable"] and g["ik_converged"]:
             assert gi not in flagged, [w for i, w in issues if i == gi]
     bad = _crafted(ref.grasps, hand)
-    msgs = lg.validation_issues(hand, orc.validate(hand.desc, bad, v, t, raw, p), p)
+    msgs = lg.validation_issues(hand.joint_names, orc.validate(hand.desc, bad, v, t, raw, p), p)
     by = {}
     for gi, what in msgs:
         by.setdefault(gi, []).append(what)
@@ -82,4 +83,4 @@ def test_validate_batch_bit_exact():
     ctx.close()
     want = orc.validate(hand.desc, grasps, v, t, raw, p)
     assert mismatched_fields(got, want) == {}
-    assert lg.validation_issues(hand, got, p) == lg.validation_issues(hand, want, p)
+    assert lg.validation_issues(hand.joint_names, got, p) == lg.validation_issues(hand.joint_names, want, p)

@@ -3,16 +3,17 @@ import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
+import caller as lc
 import paper_2511_07418_b200 as lg
 from oracle import orc_py as orc
 
 A = os.path.join(ROOT, "assets")
 batch = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-p = lg.parse_config(f"{A}/configs/four_finger.cfg", hand=f"{A}/hands/four_finger.urdf",
+p = lc.parse_config(f"{A}/configs/four_finger.cfg", hand=f"{A}/hands/four_finger.urdf",
                     object=f"{A}/objects/sphere_r030.obj", batch=batch)
 p.passes = 2
 p.want_trace = 1
-hand, patches, raw, _ = lg.prepare_inputs(p)
+hand, patches, raw, _ = lc.prepare_inputs(p)
 ctx = lg.Context(0)
 t = time.time()
 f = lg.ContactFieldIndex.build(ctx, hand, patches, p.field_configs, p.box_width, p.seed, p.codebook_size)

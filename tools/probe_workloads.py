@@ -9,6 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
+import caller as lc  # noqa: E402
 import paper_2511_07418_b200 as lg  # noqa: E402
 
 
@@ -19,7 +20,7 @@ def main():
     for name in names:
         p = bench.params_for(name, batch)
         t0 = time.perf_counter()
-        hand, patches, raw, _ = lg.prepare_inputs(p)
+        hand, patches, raw, _ = lc.prepare_inputs(p)
         t_prep = time.perf_counter() - t0
         r = lg.run_batch(ctx, hand, patches, raw, p)
         r = lg.run_batch(ctx, hand, patches, raw, p)

@@ -19,6 +19,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+import caller as lc  # noqa: E402
 import paper_2511_07418_b200 as lg  # noqa: E402
 
 LOW_DIVERSITY = dict(restarts=1, lookup_attempts=1, unused_attempts=4)
@@ -29,11 +30,11 @@ def make_object(o):
     rng = np.random.default_rng(o)
     kind = o % 3
     if kind == 0:
-        return "box", lg.Mesh.box(tuple(rng.uniform(0.03, 0.07, size=3)))
+        return "box", lc.Mesh.box(tuple(rng.uniform(0.03, 0.07, size=3)))
     if kind == 1:
-        return "cylinder", lg.Mesh.cylinder(float(rng.uniform(0.015, 0.03)),
+        return "cylinder", lc.Mesh.cylinder(float(rng.uniform(0.015, 0.03)),
                                             float(rng.uniform(0.06, 0.12)), 24)
-    return "sphere", lg.Mesh.icosphere(float(rng.uniform(0.02, 0.035)), 3)
+    return "sphere", lc.Mesh.icosphere(float(rng.uniform(0.02, 0.035)), 3)
 
 
 def main():
@@ -52,14 +53,14 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     a = os.path.join(ROOT, "assets")
-    p = lg.parse_config(os.path.join(a, "configs", "allegro.cfg"),
+    p = lc.parse_config(os.path.join(a, "configs", "allegro.cfg"),
                         hand=os.path.join(a, "hands", "allegro_like.urdf"),
                         object=os.path.join(a, "objects", "box_050.obj"), batch=args.batch)
     p.want_trace = 0
     if not args.full_diversity:
         for k, v in LOW_DIVERSITY.items():
             setattr(p, k, v)
-    hand, patches, _, _ = lg.prepare_inputs(p)
+    hand, patches, _, _ = lc.prepare_inputs(p)
     ctx = lg.Context(local)
     field = lg.ContactFieldIndex.build(ctx, hand, patches, p.field_configs, p.box_width, p.seed,
                                        p.codebook_size)
@@ -67,7 +68,7 @@ def main():
     dev_s, valid, cand, t0 = 0.0, 0, 0, time.perf_counter()
     for o in mine:
         _, mesh = make_object(o)
-        raw = lg.sample_surface(mesh, p.samples_per_cm2, lg.mix_seed(p.seed, 0x6f626a73))
+        raw = lc.sample_surface(mesh, p.samples_per_cm2, lg.mix_seed(p.seed, 0x6f626a73))
         r = lg.run_batch(ctx, hand, patches, raw, p, field=field)
         dev_s += r.profile["device_seconds"]
         valid += int(r.profile["valid"])
