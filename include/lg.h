@@ -392,6 +392,27 @@ int lg_run_batch_field(lg_ctx* ctx, const lg_hand_desc* hand,
                        const double* raw_samples, int n_raw,
                        const lg_run_params* params, lg_result** out);
 
+/* ---- multi-GPU -------------------------------------------
+ * Seed sharding: rank r of R calls lg_run_batch with shard_rank = r,
+ * shard_count = R on its own context/GPU (candidates [rB/R, (r+1)B/R)); the
+ * shards are independent and their union is the single-GPU result.  The only
+ * collective is the final gather of the kept grasps to rank 0 over NCCL
+ * (NVLink/NVSwitch inside a box).  It replaces the reference's parallel_for
+ * over candidate chunks (parallel.hpp:24-56).  NCCL (libnccl.so.2) is bound at
+ * run time by lg_comm_unique_id / lg_comm_init. */
+#define LG_COMM_ID_BYTES 128
+typedef struct lg_comm lg_comm;
+/* Rank 0 creates the id; the caller distributes the bytes to every rank. */
+int lg_comm_unique_id(unsigned char* id);
+int lg_comm_init(lg_ctx* ctx, const unsigned char* id, int rank, int world, lg_comm** out);
+void lg_comm_destroy(lg_comm* c);
+/* Every rank passes its shard's kept grasps and profile.  Rank 0 receives all
+ * grasps ordered by g (run_batch's kept order) in library-owned storage valid
+ * until the next gather or lg_comm_destroy, and the merged profile (funnel
+ * counts summed, stage seconds = max over ranks); other ranks get NULL / 0. */
+int lg_comm_gather(lg_comm* c, const lg_grasp* grasps, long long n, const lg_profile* profile,
+                   const lg_grasp** all, long long* n_all, lg_profile* merged);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,11 @@ def lib():
         "lg_result_traces": (P(A.Trace), [vp]),
         "lg_result_destroy": (None, [vp]),
         "lg_libm_eval": (C.c_int, [vp, C.c_int, C.c_longlong, A.dp, A.dp, A.dp]),
+        "lg_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+        "lg_comm_init": (C.c_int, [vp, C.POINTER(C.c_ubyte), C.c_int, C.c_int, P(vp)]),
+        "lg_comm_destroy": (None, [vp]),
+        "lg_comm_gather": (C.c_int, [vp, P(A.Grasp), C.c_longlong, P(A.Profile),
+                                     P(P(A.Grasp)), P(C.c_longlong), P(A.Profile)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

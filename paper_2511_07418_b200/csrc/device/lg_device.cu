@@ -37,18 +37,20 @@ namespace {
   } while (0)
 
 // ---------------------------------------------------------------- buffers
-// Stream-ordered allocations from the device's default pool (release
-// threshold raised at context creation), so per-call scratch is recycled
-// without device-wide synchronisation.
+// Device scratch comes from cudaMalloc through a per-stream block cache: a
+// pass allocates the same buffer sizes every call, so released blocks are
+// kept and handed back (stream order makes reuse on the same stream safe).
+// The cache of a stream is bounded (kCacheCap bytes; the largest blocks are
+// returned to the driver first) and is dropped entirely, then the allocation
+// retried once, when cudaMalloc reports out-of-memory.
 thread_local cudaStream_t g_alloc_stream = nullptr;
 std::mutex g_streams_mu;
 std::set<cudaStream_t> g_live_streams;  // streams of live contexts
-
-// Per-stream block cache: a pass allocates the same buffer sizes every call,
-// so released blocks are kept and handed back (stream order makes reuse on
-// the same stream safe); nothing is returned to the driver until the
-// context goes away.
 std::map<cudaStream_t, std::multimap<size_t, void*>> g_cache;
+std::map<cudaStream_t, size_t> g_cache_bytes;
+constexpr size_t kCacheCap = size_t(16) << 30;
+
+void drop_cache(cudaStream_t s);
 
 void* cached_alloc(size_t bytes, cudaStream_t s) {
   {
@@ -58,13 +60,21 @@ void* cached_alloc(size_t bytes, cudaStream_t s) {
       auto it = c.lower_bound(bytes);
       if (it != c.end() && it->first <= 2 * bytes + 4096) {
         void* p = it->second;
+        g_cache_bytes[s] -= it->first;
         c.erase(it);
         return p;
       }
     }
   }
   void* p = nullptr;
-  CK(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    (void)cudaGetLastError();
+    CK(cudaStreamSynchronize(s));
+    drop_cache(s);
+    e = cudaMalloc(&p, bytes);
+  }
+  CK(e);
   return p;
 }
 
@@ -72,7 +82,17 @@ void free_on(void* p, size_t bytes, cudaStream_t s) {
   {
     std::lock_guard<std::mutex> lk(g_streams_mu);
     if (g_live_streams.count(s)) {
-      g_cache[s].emplace(bytes, p);
+      auto& c = g_cache[s];
+      size_t& held = g_cache_bytes[s];
+      c.emplace(bytes, p);
+      held += bytes;
+      // bounded: return the largest blocks to the driver first
+      while (held > kCacheCap && !c.empty()) {
+        auto last = std::prev(c.end());
+        held -= last->first;
+        cudaFree(last->second);
+        c.erase(last);
+      }
       return;
     }
   }
@@ -87,6 +107,7 @@ void drop_cache(cudaStream_t s) {
   if (it == g_cache.end()) return;
   for (auto& kv : it->second) cudaFree(kv.second);
   g_cache.erase(it);
+  g_cache_bytes.erase(s);
 }
 
 struct Buf {
@@ -125,7 +146,9 @@ T* dalloc(Buf& b, size_t count) {
   return b.as<T>();
 }
 // PCIe traffic accounting (reported as h2d_bytes / d2h_bytes per run)
-long long g_h2d = 0, g_d2h = 0;
+// PCIe bytes moved by the current call, per host thread (one in-flight call
+// per context, one context per driving thread).
+thread_local long long g_h2d = 0, g_d2h = 0;
 
 template <typename T>
 T* dupload(Buf& b, const T* src, size_t count, cudaStream_t s) {
@@ -237,6 +260,24 @@ void use_ctx(lg_ctx* ctx) {
 #define LAUNCH(ctx) ++(ctx)->launches
 
 void check_launch() { CK(cudaGetLastError()); }
+
+// Dynamic shared memory for a query kernel's codebook copy ([C][3] doubles),
+// or 0 to read it from global memory: opts the kernel in above the default
+// 48 KiB when needed, within the device's per-block limit minus the kernel's
+// static shared memory.
+template <typename K>
+size_t codebook_smem(K kern, int C) {
+  const size_t need = 3 * (size_t)C * sizeof(double);
+  cudaFuncAttributes a;
+  CK(cudaFuncGetAttributes(&a, kern));
+  int dev = 0, optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (need + a.sharedSizeBytes > (size_t)optin || need > (size_t)(64 << 10)) return 0;
+  if (need > (size_t)a.maxDynamicSharedSizeBytes)
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+  return need;
+}
 
 // Binds a hand description to constant memory (one hand per call).
 void bind_hand(lg_ctx* ctx, const lg_hand_desc& d) {
@@ -681,17 +722,19 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                          d_acc, d_pen);
       LAUNCH(ctx);
       check_launch();
-      int cb_smem = 3 * F.C <= 6144 ? 1 : 0;
-      size_t qsm = cb_smem ? 3 * (size_t)F.C * sizeof(double) : 0;
-      if (ensure_dirlists(field, cfg.theta_hit))
-        k_query3<<<Bl, 256, qsm, s>>>(Bl, field->f, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
+      if (ensure_dirlists(field, cfg.theta_hit)) {
+        size_t qsm = codebook_smem(k_query3, F.C);
+        k_query3<<<Bl, 256, qsm, s>>>(Bl, field->f, FS, d_pose, d_acc, cfg.theta_hit, G, qsm > 0,
                                       d_mask, d_cnt);
-      else if (F.grid_ok)
-        k_query2<<<Bl, 256, qsm, s>>>(Bl, F, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem, d_mask,
+      } else if (F.grid_ok) {
+        size_t qsm = codebook_smem(k_query2, F.C);
+        k_query2<<<Bl, 256, qsm, s>>>(Bl, F, FS, d_pose, d_acc, cfg.theta_hit, G, qsm > 0, d_mask,
                                       d_cnt);
-      else
-        k_query<<<Bl, 256, qsm, s>>>(Bl, F, d_gop, FS, d_pose, d_acc, cfg.theta_hit, G, cb_smem,
+      } else {
+        size_t qsm = codebook_smem(k_query, F.C);
+        k_query<<<Bl, 256, qsm, s>>>(Bl, F, d_gop, FS, d_pose, d_acc, cfg.theta_hit, G, qsm > 0,
                                      d_mask, d_cnt);
+      }
       LAUNCH(ctx);
       check_launch();
       k_obj_aabb<<<Bl, 256, 0, s>>>(Bl, RS, d_pose, d_acc, d_aabb);
@@ -1684,14 +1727,15 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
     int G = 0;
     for (int p = 0; p < f->f.P; ++p) G = std::max(G, group_of_patch[p] + 1);
     int* d_cnt = dalloc<int>(bc, (size_t)m * std::max(G, 1));
-    int cb_smem = 3 * f->f.C <= 6144 ? 1 : 0;
-    size_t qsm = cb_smem ? 3 * (size_t)f->f.C * sizeof(double) : 0;
     DField fq = f->f;  // the dense path bakes the field's own groups into rec
     if (!std::equal(f->h_gop.begin(), f->h_gop.end(), group_of_patch)) fq.grid_ok = 0;
-    if (fq.grid_ok && ensure_dirlists(f, theta))
-      k_query3<<<m, 256, qsm, s>>>(m, f->f, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
-    else
-      k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, cb_smem, d_mask, d_cnt);
+    if (fq.grid_ok && ensure_dirlists(f, theta)) {
+      size_t qsm = codebook_smem(k_query3, f->f.C);
+      k_query3<<<m, 256, qsm, s>>>(m, f->f, S, d_pose, d_acc, theta, G, qsm > 0, d_mask, d_cnt);
+    } else {
+      size_t qsm = codebook_smem(k_query, f->f.C);
+      k_query<<<m, 256, qsm, s>>>(m, fq, d_g, S, d_pose, d_acc, theta, G, qsm > 0, d_mask, d_cnt);
+    }
     check_launch();
     CK(cudaMemcpyAsync(masks, d_mask, sizeof(uint32_t) * m * n, cudaMemcpyDeviceToHost, s));
     if (scores) {
@@ -1790,5 +1834,233 @@ const lg_grasp* lg_result_grasps(const lg_result* r) { return r->r.grasps.data()
 long long lg_result_num_traces(const lg_result* r) { return (long long)r->r.traces.size(); }
 const lg_trace* lg_result_traces(const lg_result* r) { return r->r.traces.data(); }
 void lg_result_destroy(lg_result* r) { delete r; }
+
+}  // extern "C"
+
+// ===================================================================== multi-GPU
+// Seed sharding: rank r of R runs lg_run_batch with
+// shard_rank = r, shard_count = R on its own GPU (every per-candidate RNG
+// stream depends only on (seed, tag, c or g), so the shards are independent
+// and the union is the single-GPU result).  The only collective is the final
+// gather of the kept grasps to rank 0 over NCCL: one ncclAllGather of a fixed
+// per-rank header (grasp count, funnel counters, stage times), then grouped
+// ncclSend / ncclRecv of the packed lg_grasp records to rank 0, which orders
+// them by g = pass*batch + c — run_batch's `kept` order (pipeline.cpp:607-614).
+// This replaces the reference's only parallelism, parallel_for over chunks of
+// candidates (parallel.hpp:24-56, pipeline.cpp:382-391).
+//
+// NCCL is bound at run time (dlopen of libnccl.so.2, reusing an already-loaded
+// copy such as the one PyTorch brings), so the library has no link-time NCCL
+// dependency and single-GPU callers never load it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.h = h;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.send = (decltype(api.send))dlsym(h, "ncclSend");
+    api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+    api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+  });
+  if (!api.h || !api.commInitRank || !api.allGather || !api.send || !api.recv)
+    throw lgc::cuda_error("NCCL (libnccl.so.2) is not available");
+  return api;
+}
+
+void NK(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw lgc::cuda_error(std::string(what) + ": " +
+                          (nccl().errorString ? nccl().errorString(r) : "NCCL error"));
+}
+
+// Per-rank header exchanged by the all-gather (int64 slots; doubles bit-cast).
+enum : int {
+  kHdrGrasps = 0, kHdrCandidates, kHdrPlaced, kHdrBalanced, kHdrIkFinite, kHdrPenFree,
+  kHdrIkConv, kHdrStable, kHdrValid, kHdrLaunches, kHdrDevSec, kHdrTotal, kHdrPlacementS,
+  kHdrContactS, kHdrKinS, kHdrPostS, kHdrFieldS, kHdrN = 20
+};
+long long dbits(double v) {
+  long long b;
+  std::memcpy(&b, &v, 8);
+  return b;
+}
+double bitsd(long long b) {
+  double v;
+  std::memcpy(&v, &b, 8);
+  return v;
+}
+}  // namespace
+
+struct lg_comm {
+  lg_ctx* ctx = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  std::vector<lg_grasp> merged;
+};
+
+extern "C" {
+
+int lg_comm_unique_id(unsigned char* id) {
+  return lgc::guard([&] {
+    if (!id) throw std::invalid_argument("lg_comm_unique_id: null argument");
+    static_assert(sizeof(ncclUniqueId) == LG_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId u;
+    NK(nccl().getUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int lg_comm_init(lg_ctx* ctx, const unsigned char* id, int rank, int world, lg_comm** out) {
+  return lgc::guard([&] {
+    if (!ctx || !id || !out || world < 1 || rank < 0 || rank >= world)
+      throw std::invalid_argument("lg_comm_init: bad argument");
+    use_ctx(ctx);
+    auto c = std::make_unique<lg_comm>();
+    c->ctx = ctx;
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    NK(nccl().commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+    *out = c.release();
+  });
+}
+
+void lg_comm_destroy(lg_comm* c) {
+  if (!c) return;
+  if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
+  delete c;
+}
+
+int lg_comm_gather(lg_comm* c, const lg_grasp* grasps, long long n, const lg_profile* profile,
+                   const lg_grasp** all, long long* n_all, lg_profile* merged) {
+  return lgc::guard([&] {
+    if (!c || (!grasps && n) || !profile || !all || !n_all)
+      throw std::invalid_argument("lg_comm_gather: null argument");
+    use_ctx(c->ctx);
+    cudaStream_t s = c->ctx->stream;
+    NcclApi& api = nccl();
+    const int R = c->world;
+    // 1. headers
+    std::vector<long long> hdr(kHdrN, 0);
+    const lg_profile& p = *profile;
+    hdr[kHdrGrasps] = n;
+    hdr[kHdrCandidates] = p.candidates;
+    hdr[kHdrPlaced] = p.placements_accepted;
+    hdr[kHdrBalanced] = p.contact_sets_balanced;
+    hdr[kHdrIkFinite] = p.ik_finite;
+    hdr[kHdrPenFree] = p.penetration_free;
+    hdr[kHdrIkConv] = p.ik_converged;
+    hdr[kHdrStable] = p.stable;
+    hdr[kHdrValid] = p.valid;
+    hdr[kHdrLaunches] = p.gpu_launches;
+    hdr[kHdrDevSec] = dbits(p.device_seconds);
+    hdr[kHdrTotal] = dbits(p.total);
+    hdr[kHdrPlacementS] = dbits(p.placement_domains);
+    hdr[kHdrContactS] = dbits(p.contact_optimization);
+    hdr[kHdrKinS] = dbits(p.kinematics_optimization);
+    hdr[kHdrPostS] = dbits(p.postprocessing);
+    hdr[kHdrFieldS] = dbits(p.field_build);
+    Buf bh, ba;
+    long long* d_h = dupload(bh, hdr.data(), hdr.size(), s);
+    long long* d_all = dalloc<long long>(ba, (size_t)kHdrN * R);
+    NK(api.allGather(d_h, d_all, kHdrN, ncclInt64, c->comm, s), "ncclAllGather");
+    std::vector<long long> H = ddownload(d_all, (size_t)kHdrN * R, s);
+    // 2. records to rank 0
+    const size_t rec = sizeof(lg_grasp);
+    std::vector<long long> off(R + 1, 0);
+    for (int r = 0; r < R; ++r) off[r + 1] = off[r] + H[(size_t)r * kHdrN + kHdrGrasps];
+    Buf bs, br;
+    uint8_t* d_send = nullptr;
+    uint8_t* d_recv = nullptr;
+    if (c->rank != 0 && n > 0) d_send = dupload(bs, (const uint8_t*)grasps, (size_t)n * rec, s);
+    if (c->rank == 0 && off[R] - n > 0) d_recv = dalloc<uint8_t>(br, (size_t)(off[R] - n) * rec);
+    NK(api.groupStart(), "ncclGroupStart");
+    if (c->rank == 0) {
+      for (int r = 1; r < R; ++r) {
+        long long cnt = off[r + 1] - off[r];
+        if (cnt > 0)
+          NK(api.recv(d_recv + (size_t)(off[r] - n) * rec, (size_t)cnt * rec, ncclUint8, r, c->comm, s),
+             "ncclRecv");
+      }
+    } else if (n > 0) {
+      NK(api.send(d_send, (size_t)n * rec, ncclUint8, 0, c->comm, s), "ncclSend");
+    }
+    NK(api.groupEnd(), "ncclGroupEnd");
+    CK(cudaStreamSynchronize(s));
+    if (c->rank != 0) {
+      *all = nullptr;
+      *n_all = 0;
+      if (merged) std::memset(merged, 0, sizeof(*merged));
+      return;
+    }
+    // 3. merge on rank 0: kept order = ascending g (stable)
+    c->merged.assign(grasps, grasps + n);
+    if (off[R] > n) {
+      std::vector<uint8_t> h = ddownload(d_recv, (size_t)(off[R] - n) * rec, s);
+      const lg_grasp* g = (const lg_grasp*)h.data();
+      c->merged.insert(c->merged.end(), g, g + (off[R] - n));
+    }
+    std::stable_sort(c->merged.begin(), c->merged.end(),
+                     [](const lg_grasp& a, const lg_grasp& b) { return a.g < b.g; });
+    *all = c->merged.data();
+    *n_all = (long long)c->merged.size();
+    if (merged) {
+      *merged = p;
+      auto sum = [&](int k) {
+        long long t = 0;
+        for (int r = 0; r < R; ++r) t += H[(size_t)r * kHdrN + k];
+        return t;
+      };
+      auto mx = [&](int k) {
+        double t = 0.0;
+        for (int r = 0; r < R; ++r) t = std::max(t, bitsd(H[(size_t)r * kHdrN + k]));
+        return t;
+      };
+      merged->candidates = sum(kHdrCandidates);
+      merged->placements_accepted = sum(kHdrPlaced);
+      merged->contact_sets_balanced = sum(kHdrBalanced);
+      merged->ik_finite = sum(kHdrIkFinite);
+      merged->penetration_free = sum(kHdrPenFree);
+      merged->ik_converged = sum(kHdrIkConv);
+      merged->stable = sum(kHdrStable);
+      merged->valid = sum(kHdrValid);
+      merged->gpu_launches = sum(kHdrLaunches);
+      merged->device_seconds = mx(kHdrDevSec);
+      merged->total = mx(kHdrTotal);
+      merged->placement_domains = mx(kHdrPlacementS);
+      merged->contact_optimization = mx(kHdrContactS);
+      merged->kinematics_optimization = mx(kHdrKinS);
+      merged->postprocessing = mx(kHdrPostS);
+      merged->field_build = mx(kHdrFieldS);
+      merged->grasps_per_second = merged->total > 0.0 ? merged->valid / merged->total : 0.0;
+    }
+  });
+}
 
 }  // extern "C"

@@ -4,9 +4,12 @@
 Rank r of R owns candidates c in [r*B/R, (r+1)*B/R) for every pass; every
 per-candidate RNG stream depends only on (seed, tag, c or g), so the union of
 the shards is the single-GPU result.  The only collective is the final
-gather: per-rank grasp records as byte tensors, padded to the largest rank,
-all-gathered once (NCCL on GPUs, gloo in the CPU tests), then sorted by
-g = pass*batch + c to reproduce run_batch's `kept` order (pipeline.cpp:607-614).
+gather of the kept grasps to rank 0, done by the library over NCCL behind the
+C-ABI (lg_comm_gather: an all-gather of per-rank headers, then grouped
+send/recv of the packed records); rank 0 gets them ordered by
+g = pass*batch + c, run_batch's `kept` order (pipeline.cpp:607-614).  The
+caller only distributes the 128-byte NCCL id (any transport: torch.distributed
+in bench.py, MPI, a shared file).
 """
 from __future__ import annotations
 
@@ -29,26 +32,51 @@ def shard_range(batch, rank, world):
     return batch * rank // world, batch * (rank + 1) // world
 
 
-def gather_records(records, device=None, group=None):
-    """All-gather a structured numpy array from every rank; returns the
-    concatenation in rank order (every rank receives it)."""
-    import torch
-    import torch.distributed as dist
+class Comm:
+    """NCCL communicator of one rank behind the C-ABI (lg_comm_*)."""
 
-    world = dist.get_world_size(group)
-    raw = np.ascontiguousarray(records).view(np.uint8).reshape(-1)
-    n = torch.tensor([raw.size], dtype=torch.int64, device=device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    cap = int(max(s.item() for s in sizes))
-    buf = torch.zeros(max(cap, 1), dtype=torch.uint8, device=device)
-    if raw.size:
-        buf[:raw.size] = torch.from_numpy(raw.copy()).to(buf.device)
-    outs = [torch.zeros_like(buf) for _ in range(world)]
-    dist.all_gather(outs, buf, group=group)
-    parts = [o[:int(s.item())].cpu().numpy() for o, s in zip(outs, sizes)]
-    cat = np.concatenate(parts) if parts else np.zeros(0, np.uint8)
-    return cat.view(records.dtype)
+    def __init__(self, ctx, rank, world, uid):
+        from .api import lib, check
+        L = lib()
+        self._ctx = ctx
+        self.rank, self.world = int(rank), int(world)
+        buf = (C.c_ubyte * A.LG_COMM_ID_BYTES).from_buffer_copy(bytes(uid))
+        self._h = C.c_void_p()
+        check(L.lg_comm_init(ctx._h, buf, self.rank, self.world, C.byref(self._h)))
+
+    @staticmethod
+    def unique_id():
+        from .api import lib, check
+        buf = (C.c_ubyte * A.LG_COMM_ID_BYTES)()
+        check(lib().lg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def gather(self, result):
+        """Rank 0: (all grasps in g order, merged profile dict); else (None, None)."""
+        from .api import lib, check, _copy_structs
+        g = np.ascontiguousarray(result.grasps)
+        out = C.POINTER(A.Grasp)()
+        n_all = C.c_longlong(0)
+        merged = A.Profile()
+        check(lib().lg_comm_gather(self._h, g.ctypes.data_as(C.POINTER(A.Grasp)), len(g),
+                                   C.byref(result.profile_struct), C.byref(out), C.byref(n_all),
+                                   C.byref(merged)))
+        if self.rank != 0:
+            return None, None
+        grasps = _copy_structs(out, n_all.value, A.grasp_dtype())
+        return grasps, {n: getattr(merged, n) for n, _ in A.Profile._fields_}
+
+    def close(self):
+        from .api import lib
+        if self._h:
+            lib().lg_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def merge_grasps(grasps):

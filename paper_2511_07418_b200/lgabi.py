@@ -9,6 +9,7 @@ LG_MAX_K = 5
 LG_MAX_CONTACTS = 6
 LG_MAX_DOF = 32
 LG_MAX_GROUPS = 32
+LG_COMM_ID_BYTES = 128
 
 LG_OK = 0
 LG_ERR_INVALID_ARGUMENT = -1

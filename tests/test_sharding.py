@@ -19,6 +19,26 @@ def _free_port():
     return port
 
 
+def gather_records(records):
+    """All-gather a structured array over the process group (gloo here; the
+    device path gathers over NCCL behind the C-ABI, lg_comm_gather)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    raw = np.ascontiguousarray(records).view(np.uint8).reshape(-1)
+    n = torch.tensor([raw.size], dtype=torch.int64)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    cap = int(max(s.item() for s in sizes))
+    buf = torch.zeros(max(cap, 1), dtype=torch.uint8)
+    if raw.size:
+        buf[:raw.size] = torch.from_numpy(raw.copy())
+    outs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    parts = [o[:int(s.item())].numpy() for o, s in zip(outs, sizes)]
+    return np.concatenate(parts).view(records.dtype)
+
+
 def _worker(rank, world, port, outdir):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -36,8 +56,8 @@ def _worker(rank, world, port, outdir):
     hand, patches, raw, _ = lc.prepare_inputs(p)
     sp = ldist.shard_params(p, rank, world)
     r = orc.run_batch(hand.desc, patches.desc, raw, sp, workers=1)
-    g = ldist.merge_grasps(ldist.gather_records(r.grasps))
-    t = ldist.gather_records(r.traces)
+    g = ldist.merge_grasps(gather_records(r.grasps))
+    t = gather_records(r.traces)
     if rank == 0:
         np.save(os.path.join(outdir, "grasps.npy"), g)
         np.save(os.path.join(outdir, "traces.npy"), t)
