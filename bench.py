@@ -60,7 +60,7 @@ WORKLOADS = {
 }
 METRIC = "valid grasps/sec per object at 1/2/4/8 B200; forward-pass seconds"
 UNIT = "valid grasps/s"
-REF_SAMPLE = 160  # candidates per reference step (bounded CPU sample, ~10 s on 16 cores)
+REF_SAMPLE = 320  # candidates per reference step (bounded CPU sample, ~9 s on 16 cores)
 
 
 def asset(*p):

@@ -301,7 +301,8 @@ def test_bench_config_against_oracle_shard():
     the device's full batch, compared candidate by candidate with the
     oracle's re-run of one 1/40 shard (field built by each side)."""
     import bench
-    p = bench.params_for("allegro_box")
+    cfg, hand_path, obj = bench.workload_paths("allegro_box")
+    p = lc.parse_config(cfg, hand=hand_path, object=obj)
     p.want_trace = 1
     hand, patches, raw, _ = lc.prepare_inputs(p)
     ctx = lg.Context(0)
