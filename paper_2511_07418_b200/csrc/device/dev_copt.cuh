@@ -179,13 +179,278 @@ constexpr int copt_lane() { return (kSlot + 9 * NC) | 1; }
 template <int NC>
 constexpr int copt_per_warp() { return NC * kSlot + 6 * NC + 32 * copt_lane<NC>(); }
 
+// ----------------------------------------------- spatial chunk index
+// project_to_domain (contact_opt.cpp:11-25) returns the element with the
+// smallest (squared distance, index) pair: the reference scans every element.
+// The device keeps a Morton-ordered structure-of-arrays copy of each domain,
+// split into chunks of 32 elements (one per lane) grouped into super-chunks
+// of 32 chunks, each with its bounding box.  A warp answers its 32 mutation
+// queries one after another, cooperatively: lanes test box lower bounds in
+// parallel, ballot the boxes that can still hold the minimum, and evaluate a
+// needed chunk with one element per lane (coalesced loads).  A box is dropped
+// only when its lower bound exceeds the best distance found so far by a
+// relative guard of 2^-40, which covers the roundings of the bound and of the
+// distances: a dropped box can hold neither a closer element nor a tie.  All
+// candidates compare lexicographically on (d2, element index), so the result
+// is the reference's first minimum whatever the visit order.
+constexpr int kChunk = 32;
+// Domains below this size keep the plain broadcast scan (every lane reads the
+// same element: one load serves the warp), which is faster when the whole
+// domain sits in L1; the cooperative search pays off on large domains.
+constexpr int kCoopMin = 4096;
+
+struct DomIdx {
+  const double* sx;         // sorted element positions, SoA [nel]
+  const double* sy;
+  const double* sz;
+  const int* si;            // sorted -> element index within its domain
+  const double* cb;         // chunk boxes [6][cstride] (min xyz, max xyz)
+  long long cstride;
+  const double* sb;         // super-chunk boxes [6][sstride]
+  long long sstride;
+  const long long* choff;   // first chunk of each (candidate, slot) domain
+  const long long* suoff;   // first super-chunk of each domain
+};
+
+__device__ __forceinline__ uint32_t morton_spread10(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+// Morton keys of the domain elements, quantised inside the candidate's posed
+// object box (k_obj_aabb); value = element index within the domain.
+__global__ void k_dom_keys(int nA, int k, const int* alive_idx, const double* aabb,
+                           const long long* el_off, const double* el_p, uint32_t* keys, int* vals) {
+  const int seg = blockIdx.x;
+  if (seg >= nA * k) return;
+  const int i = alive_idx[seg / k];
+  const long long b = el_off[seg], e = el_off[seg + 1];
+  double lo[3], sc[3];
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = aabb[6 * i + c];
+    const double ext = aabb[6 * i + 3 + c] - lo[c];
+    sc[c] = ext > 0.0 ? 1023.0 / ext : 0.0;
+  }
+  for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
+    uint32_t q[3];
+    for (int c = 0; c < 3; ++c) {
+      double v = (el_p[3 * t + c] - lo[c]) * sc[c];
+      v = v < 0.0 ? 0.0 : (v > 1023.0 ? 1023.0 : v);
+      q[c] = (uint32_t)v;
+    }
+    keys[t] = morton_spread10(q[0]) | (morton_spread10(q[1]) << 1) | (morton_spread10(q[2]) << 2);
+    vals[t] = (int)(t - b);
+  }
+}
+
+// Sorted SoA copy of each domain, its chunk boxes and super-chunk boxes
+// (block per domain).
+__global__ void k_dom_chunks(int nseg, const long long* el_off, const long long* ch_off,
+                             const long long* su_off, const int* vals_sorted, const double* el_p,
+                             DomIdx d) {
+  const int seg = blockIdx.x;
+  if (seg >= nseg) return;
+  double* sx = const_cast<double*>(d.sx);
+  double* sy = const_cast<double*>(d.sy);
+  double* sz = const_cast<double*>(d.sz);
+  int* si = const_cast<int*>(d.si);
+  double* cb = const_cast<double*>(d.cb);
+  double* sb = const_cast<double*>(d.sb);
+  const long long b = el_off[seg], e = el_off[seg + 1];
+  for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
+    const int o = vals_sorted[t];
+    const long long src = b + o;
+    sx[t] = el_p[3 * src];
+    sy[t] = el_p[3 * src + 1];
+    sz[t] = el_p[3 * src + 2];
+    si[t] = o;
+  }
+  __syncthreads();
+  const long long c0 = ch_off[seg];
+  const int nch = (int)(ch_off[seg + 1] - c0);
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    const long long j0 = b + (long long)c * kChunk;
+    const long long j1 = j0 + kChunk < e ? j0 + kChunk : e;
+    double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
+    for (long long j = j0; j < j1; ++j) {
+      const double v[3] = {sx[j], sy[j], sz[j]};
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = dmin(mn[a], v[a]);
+        mx[a] = dmax(mx[a], v[a]);
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      cb[a * d.cstride + c0 + c] = mn[a];
+      cb[(3 + a) * d.cstride + c0 + c] = mx[a];
+    }
+  }
+  __syncthreads();
+  const long long s0 = su_off[seg];
+  const int nsu = (int)(su_off[seg + 1] - s0);
+  for (int t = threadIdx.x; t < nsu; t += blockDim.x) {
+    const int c1 = (t + 1) * 32 < nch ? (t + 1) * 32 : nch;
+    double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
+    for (int c = t * 32; c < c1; ++c)
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = dmin(mn[a], cb[a * d.cstride + c0 + c]);
+        mx[a] = dmax(mx[a], cb[(3 + a) * d.cstride + c0 + c]);
+      }
+    for (int a = 0; a < 3; ++a) {
+      sb[a * d.sstride + s0 + t] = mn[a];
+      sb[(3 + a) * d.sstride + s0 + t] = mx[a];
+    }
+  }
+}
+
+__device__ __forceinline__ double box_lb(const double* B, long long stride, long long i, V3 p) {
+  const double ex = dmax(dmax(B[i] - p.x, p.x - B[3 * stride + i]), 0.0);
+  const double ey = dmax(dmax(B[stride + i] - p.y, p.y - B[4 * stride + i]), 0.0);
+  const double ez = dmax(dmax(B[2 * stride + i] - p.z, p.z - B[5 * stride + i]), 0.0);
+  return ex * ex + ey * ey + ez * ez;
+}
+
+// (d, idx) lexicographic minimum over the warp.
+__device__ __forceinline__ void warp_lexmin(double& d, int& o) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const double od = __shfl_xor_sync(kFull, d, s);
+    const int oo = __shfl_xor_sync(kFull, o, s);
+    if (od < d || (od == d && oo < o)) {
+      d = od;
+      o = oo;
+    }
+  }
+}
+
+// The 32 lanes' projections (each lane's own query point cp / act), answered
+// cooperatively one query at a time.  seg = (candidate, slot) domain, cur =
+// the incumbent element (index, position), a member of the domain.
+__device__ int project_coop(const DomIdx& D, long long seg, long long base, int ne, V3 cp_own,
+                            bool act_own, int cur_id, V3 cur_p, int lane,
+                            unsigned long long& evals) {
+  const int nch = (ne + kChunk - 1) / kChunk;
+  const int nsu = (nch + 31) / 32;
+  const long long c0 = D.choff[seg], s0 = D.suoff[seg];
+  const double* SX = D.sx + base;
+  const double* SY = D.sy + base;
+  const double* SZ = D.sz + base;
+  const int* SI = D.si + base;
+  int res = cur_id;
+  const unsigned actm = __ballot_sync(kFull, act_own);
+  for (int m = 0; m < 32; ++m) {
+    if (!((actm >> m) & 1u)) continue;
+    const V3 cp = v3(__shfl_sync(kFull, cp_own.x, m), __shfl_sync(kFull, cp_own.y, m),
+                     __shfl_sync(kFull, cp_own.z, m));
+    // pass 1: the chunk with the smallest lower bound, evaluated first
+    int sbest = 0;
+    if (nsu > 1) {
+      double l = kInf;
+      int s = 0x7fffffff;
+      for (int t = lane; t < nsu; t += 32) {
+        const double v = box_lb(D.sb, D.sstride, s0 + t, cp);
+        if (v < l) {
+          l = v;
+          s = t;
+        }
+      }
+      warp_lexmin(l, s);
+      sbest = s;
+    }
+    double lc = kInf;
+    int cbest = 0x7fffffff;
+    {
+      const int c = sbest * 32 + lane;
+      if (c < nch) {
+        lc = box_lb(D.cb, D.cstride, c0 + c, cp);
+        cbest = c;
+      }
+      warp_lexmin(lc, cbest);
+    }
+    double bd = sqnorm(sub(cur_p, cp));
+    int bi = cur_id;
+    {
+      const int j = cbest * kChunk + lane;
+      if (j < ne) {
+        const double d = sqnorm(sub(v3(SX[j], SY[j], SZ[j]), cp));
+        const int o = SI[j];
+        if (d < bd || (d == bd && o < bi)) {
+          bd = d;
+          bi = o;
+        }
+      }
+      warp_lexmin(bd, bi);
+    }
+    unsigned long long ev = (unsigned long long)(ne - cbest * kChunk < kChunk ? ne - cbest * kChunk : kChunk);
+    // pass 2: every other box whose lower bound does not exceed the best
+    const double thr = bd * (1.0 + 0x1p-40);
+    double dl = bd;
+    int ol = bi;
+    for (int tb = 0; tb < nsu; tb += 32) {
+      const int t = tb + lane;
+      const bool ns = t < nsu && (nsu == 1 || !(box_lb(D.sb, D.sstride, s0 + t, cp) > thr));
+      unsigned ms = __ballot_sync(kFull, ns);
+      while (ms) {
+        const int ss = tb + __ffs(ms) - 1;
+        ms &= ms - 1;
+        const int c2 = ss * 32 + lane;
+        const bool nc = c2 < nch && c2 != cbest && !(box_lb(D.cb, D.cstride, c0 + c2, cp) > thr);
+        unsigned mc = __ballot_sync(kFull, nc);
+        ev += (unsigned long long)__popc(mc) * kChunk;
+        // up to four needed chunks at a time: their loads are independent
+        // (the large domains stream from L2/HBM), the comparisons follow
+        while (mc) {
+          int jj[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            jj[u] = -1;
+            if (mc) {
+              jj[u] = (ss * 32 + __ffs(mc) - 1) * kChunk + lane;
+              mc &= mc - 1;
+            }
+          }
+          double px[4], py[4], pz[4];
+          int po[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool ok = jj[u] >= 0 && jj[u] < ne;
+            const int j = ok ? jj[u] : 0;
+            px[u] = ok ? SX[j] : 0.0;
+            py[u] = ok ? SY[j] : 0.0;
+            pz[u] = ok ? SZ[j] : 0.0;
+            po[u] = ok ? SI[j] : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (po[u] < 0) continue;
+            const double d = sqnorm(sub(v3(px[u], py[u], pz[u]), cp));
+            if (d < dl || (d == dl && po[u] < ol)) {
+              dl = d;
+              ol = po[u];
+            }
+          }
+        }
+      }
+    }
+    warp_lexmin(dl, ol);
+    if (lane == m) {
+      res = ol;
+      evals += ev;
+    }
+  }
+  return res;
+}
+
 // Block per candidate, warp per restart, lanes over the n_inner mutations.
 // NC = compile-time bound on k + statics (sizes the shared-memory layout).
 template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
-               const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
+               DomIdx dom, const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
                double* out_sol, double eps_stable, int* balanced) {
   extern __shared__ __align__(16) double s_co[];
   const int a = blockIdx.x;
@@ -265,81 +530,87 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
           int best_id = -1, best_anchor = -1;
           for (int mb = 0; mb < cfg.n_inner; mb += 32) {
             const int m = mb + lane;
+            const bool act = m < cfg.n_inner;
             double v = kInf;
             int cand = -1, an = -1;
-            if (m < cfg.n_inner) {
+            V3 cp = cur_p;
+            if (act) {
               const uint64_t* d2 = M + 2 * ((long long)(outer * k + q) * cfg.n_inner + m);
               // (sigma z1, sigma z2), precomputed by k_copt_normals
               const double u = __longlong_as_double((long long)d2[0]);
               const double vv = __longlong_as_double((long long)d2[1]);
-              V3 cp = axpy(axpy(cur_p, u, tx), vv, ty);
-              // project_to_domain (contact_opt.cpp:11-25): nearest element,
-              // first index among equal distances.  Every lane scans the same
-              // elements (broadcast loads, no divergence); pruned searches
-              // (x-sorted, object-frame grid) evaluate far fewer distances but
-              // diverge and measured slower.
-              const double* P = el_p + 3 * off[q];
-              const int ne = (int)cnt[q];
-              double bd;
-              int bi;
-              // Every lane scans the same elements (broadcast loads, no
-              // divergence): faster than the pruned search for domains of
-              // a few thousand elements.
-              bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
-              bi = 0;
-              int e = 1;
-              // peel to an even global element (16-byte aligned pairs)
-              if (e < ne && ((off[q] + e) & 1)) {
-                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                if (d2v < bd) {
-                  bd = d2v;
-                  bi = e;
+              cp = axpy(axpy(cur_p, u, tx), vv, ty);
+            }
+            const int ne = (int)cnt[q];
+            double bd;
+            int bi;
+            if (dom.sx && ne >= kCoopMin) {
+              unsigned long long evals = 0;
+              bi = project_coop(dom, (long long)a * k + q, off[q], ne, cp, act, ids[q], cur_p, lane,
+                                evals);
+              if (act) ctr.proj += evals;
+            } else if (act) {
+                const double* P = el_p + 3 * off[q];
+                // Every lane scans the same elements (broadcast loads, no
+                // divergence): faster than the pruned search for domains of
+                // a few thousand elements.
+                bd = sqnorm(sub(v3(P[0], P[1], P[2]), cp));
+                bi = 0;
+                int e = 1;
+                // peel to an even global element (16-byte aligned pairs)
+                if (e < ne && ((off[q] + e) & 1)) {
+                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  if (d2v < bd) {
+                    bd = d2v;
+                    bi = e;
+                  }
+                  ++e;
                 }
-                ++e;
-              }
-              // eight independent distances in flight (twelve 16-byte
-              // loads: the domain streams from L2), compared in index order
-              for (; e + 8 <= ne; e += 8) {
-                const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
-                double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
-                double2 b0 = Q[6], b1 = Q[7], b2 = Q[8], b3 = Q[9], b4 = Q[10], b5 = Q[11];
-                double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
-                double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
-                double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
-                double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
-                double d4 = sqnorm(sub(v3(b0.x, b0.y, b1.x), cp));
-                double d5 = sqnorm(sub(v3(b1.y, b2.x, b2.y), cp));
-                double d6 = sqnorm(sub(v3(b3.x, b3.y, b4.x), cp));
-                double d7 = sqnorm(sub(v3(b4.y, b5.x, b5.y), cp));
-                if (d0 < bd) { bd = d0; bi = e; }
-                if (d1 < bd) { bd = d1; bi = e + 1; }
-                if (d2 < bd) { bd = d2; bi = e + 2; }
-                if (d3 < bd) { bd = d3; bi = e + 3; }
-                if (d4 < bd) { bd = d4; bi = e + 4; }
-                if (d5 < bd) { bd = d5; bi = e + 5; }
-                if (d6 < bd) { bd = d6; bi = e + 6; }
-                if (d7 < bd) { bd = d7; bi = e + 7; }
-              }
-              for (; e + 4 <= ne; e += 4) {
-                const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
-                double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
-                double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
-                double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
-                double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
-                double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
-                if (d0 < bd) { bd = d0; bi = e; }
-                if (d1 < bd) { bd = d1; bi = e + 1; }
-                if (d2 < bd) { bd = d2; bi = e + 2; }
-                if (d3 < bd) { bd = d3; bi = e + 3; }
-              }
-              for (; e < ne; ++e) {
-                double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
-                if (d2v < bd) {
-                  bd = d2v;
-                  bi = e;
+                // eight independent distances in flight (twelve 16-byte
+                // loads: the domain streams from L2), compared in index order
+                for (; e + 8 <= ne; e += 8) {
+                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                  double2 b0 = Q[6], b1 = Q[7], b2 = Q[8], b3 = Q[9], b4 = Q[10], b5 = Q[11];
+                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
+                  double d4 = sqnorm(sub(v3(b0.x, b0.y, b1.x), cp));
+                  double d5 = sqnorm(sub(v3(b1.y, b2.x, b2.y), cp));
+                  double d6 = sqnorm(sub(v3(b3.x, b3.y, b4.x), cp));
+                  double d7 = sqnorm(sub(v3(b4.y, b5.x, b5.y), cp));
+                  if (d0 < bd) { bd = d0; bi = e; }
+                  if (d1 < bd) { bd = d1; bi = e + 1; }
+                  if (d2 < bd) { bd = d2; bi = e + 2; }
+                  if (d3 < bd) { bd = d3; bi = e + 3; }
+                  if (d4 < bd) { bd = d4; bi = e + 4; }
+                  if (d5 < bd) { bd = d5; bi = e + 5; }
+                  if (d6 < bd) { bd = d6; bi = e + 6; }
+                  if (d7 < bd) { bd = d7; bi = e + 7; }
                 }
-              }
+                for (; e + 4 <= ne; e += 4) {
+                  const double2* Q = reinterpret_cast<const double2*>(P + 3 * e);
+                  double2 a0 = Q[0], a1 = Q[1], a2 = Q[2], a3 = Q[3], a4 = Q[4], a5 = Q[5];
+                  double d0 = sqnorm(sub(v3(a0.x, a0.y, a1.x), cp));
+                  double d1 = sqnorm(sub(v3(a1.y, a2.x, a2.y), cp));
+                  double d2 = sqnorm(sub(v3(a3.x, a3.y, a4.x), cp));
+                  double d3 = sqnorm(sub(v3(a4.y, a5.x, a5.y), cp));
+                  if (d0 < bd) { bd = d0; bi = e; }
+                  if (d1 < bd) { bd = d1; bi = e + 1; }
+                  if (d2 < bd) { bd = d2; bi = e + 2; }
+                  if (d3 < bd) { bd = d3; bi = e + 3; }
+                }
+                for (; e < ne; ++e) {
+                  double d2v = sqnorm(sub(v3(P[3 * e], P[3 * e + 1], P[3 * e + 2]), cp));
+                  if (d2v < bd) {
+                    bd = d2v;
+                    bi = e;
+                  }
+                }
               ctr.proj += (unsigned long long)ne;
+            }
+            if (act) {
               cand = bi;
               const long long eg = off[q] + bi;
               slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include "../capi_common.hpp"
 #include "dev_copt.cuh"
 #include "dev_post.cuh"
@@ -821,6 +823,57 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                          d_elp, d_eln);
     LAUNCH(ctx);
     check_launch();
+    // Morton-ordered copy of every domain + chunk boxes for the exact pruned
+    // projection (dev_copt.cuh DomIdx); LG_PROJ=brute keeps the plain scan.
+    static const bool proj_brute = [] {
+      const char* e = std::getenv("LG_PROJ");
+      return e && std::string(e) == "brute";
+    }();
+    Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff;
+    DomIdx dom{};
+    long long max_dom = 0;
+    for (size_t t = 0; t + 1 < eloff.size(); ++t) max_dom = std::max(max_dom, eloff[t + 1] - eloff[t]);
+    if (!proj_brute && max_dom >= kCoopMin) {
+      const int nseg = nA * k;
+      std::vector<long long> choff((size_t)nseg + 1, 0), suoff((size_t)nseg + 1, 0);
+      for (int t = 0; t < nseg; ++t) {
+        const long long nch = (eloff[t + 1] - eloff[t] + kChunk - 1) / kChunk;
+        choff[t + 1] = choff[t] + nch;
+        suoff[t + 1] = suoff[t] + (nch + 31) / 32;
+      }
+      long long* d_choff = dupload(b_choff, choff.data(), choff.size(), s);
+      long long* d_suoff = dupload(b_suoff, suoff.data(), suoff.size(), s);
+      uint32_t* d_k = dalloc<uint32_t>(b_keys, (size_t)nel);
+      uint32_t* d_k2 = dalloc<uint32_t>(b_keys2, (size_t)nel);
+      int* d_v = dalloc<int>(b_vals, (size_t)nel);
+      int* d_v2 = dalloc<int>(b_vals2, (size_t)nel);
+      k_dom_keys<<<nseg, 256, 0, s>>>(nA, k, d_aidx, d_aabb, d_eloff, d_elp, d_k, d_v);
+      LAUNCH(ctx);
+      check_launch();
+      size_t tb = 0;
+      CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, d_k, d_k2, d_v, d_v2, (int)nel, nseg,
+                                             d_eloff, d_eloff + 1, s));
+      CK(cub::DeviceSegmentedSort::SortPairs(ctx->tmp(tb), tb, d_k, d_k2, d_v, d_v2, (int)nel, nseg,
+                                             d_eloff, d_eloff + 1, s));
+      LAUNCH(ctx);
+      double* d_sp = dalloc<double>(b_sp, 3 * (size_t)nel);
+      const long long cs = std::max(choff.back(), 1ll), ss = std::max(suoff.back(), 1ll);
+      double* d_cb = dalloc<double>(b_cb, 6 * (size_t)cs);
+      double* d_sb = dalloc<double>(b_sb, 6 * (size_t)ss);
+      dom.sx = d_sp;
+      dom.sy = d_sp + nel;
+      dom.sz = d_sp + 2 * nel;
+      dom.si = reinterpret_cast<int*>(d_k);  // the key buffer is free after the sort
+      dom.cb = d_cb;
+      dom.cstride = cs;
+      dom.sb = d_sb;
+      dom.sstride = ss;
+      dom.choff = d_choff;
+      dom.suoff = d_suoff;
+      k_dom_chunks<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_choff, d_suoff, d_v2, d_elp, dom);
+      LAUNCH(ctx);
+      check_launch();
+    }
     Buf b_draws, b_oid, b_oobj, b_oan, b_osol, b_bal;
     uint64_t* d_draws = dalloc<uint64_t>(b_draws, (size_t)nA * per_cand);
     k_copt_draws<<<grid_for(nA, 64), 64, 0, s>>>(nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, d_draws);
@@ -875,7 +928,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                               : k_contact_opt2<kMaxC, 4>;
     size_t co_smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
     co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln,
-                                         d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
+                                         dom, d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
                                          d_bal);
     LAUNCH(ctx);
     check_launch();
