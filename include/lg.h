@@ -298,6 +298,83 @@ int lg_query_domains_batch(lg_ctx* ctx, lg_field* f, const int* group_of_patch,
                            int m, double theta_hit, uint32_t* masks,
                            double* scores);
 
+/* query_domains (contact_field.cpp:380-448; contact_field.hpp:98-109,147-150)
+ * for ONE pose (R row-major, t): the ContactDomain of every dependency group
+ * 0..n_groups-1 (group_of_patch maps patch id -> group, -1 static).  Elements
+ * are in sample order within a group; each carries its sample index, posed
+ * position and normal, score (max(0, best -code.n over its hits)) and its
+ * hits (patch id, box id within the patch) sorted by patch.  Read with
+ * lg_domains_group / lg_domains_elements; the arrays stay valid until
+ * lg_domains_destroy. */
+typedef struct lg_domains lg_domains;
+int lg_query_domains_elements(lg_ctx* ctx, lg_field* f, const int* group_of_patch, int n_groups,
+                              const double* samples, int n, const double* pose, double theta_hit,
+                              lg_domains** out);
+/* elements [*first, *first + *count) belong to group `group` */
+int lg_domains_group(const lg_domains* d, int group, long long* first, long long* count);
+/* all elements of all groups: hits of element e are [hit_off[e], hit_off[e+1]) */
+int lg_domains_elements(const lg_domains* d, long long* n_elements, const int** sample,
+                        const double** pos, const double** nrm, const double** score,
+                        const long long** hit_off, const int** hit_patch, const int** hit_box);
+void lg_domains_destroy(lg_domains* d);
+
+/* reverse_lookup (contact_field.cpp:450-484; contact_field.hpp:154-156) for m
+ * domain elements: element t has hits [hit_off[t], hit_off[t+1]) (patch id,
+ * box id) and outward normal normals[t]; seeds[t] is its choice seed.
+ * Writes the IndexRep: link, link-local point and normal.  An element without
+ * hits or with a box outside the index returns LG_ERR_OUT_OF_RANGE, as the
+ * reference throws std::out_of_range. */
+int lg_reverse_lookup_batch(lg_ctx* ctx, lg_field* f, int m, const long long* hit_off,
+                            const int* hit_patch, const int* hit_box, const double* normals,
+                            const uint64_t* seeds, int* link, double* point, double* normal);
+
+/* place_object (pipeline.cpp:122-183; pipeline.hpp:103-106) for candidates
+ * c in [c0, c0+m): stream mix_seed(params->seed, 'plac', c), statics from
+ * collect_static_surface, verdict against the preprocessed raw samples.
+ * Writes pose [m][12] (R row-major, t), accepted, penetration and the static
+ * contact (n_static[m] in {0,1}; static_p/n [m][3], static_link [m]).  field
+ * may be NULL (built from params). */
+int lg_place_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches,
+                   lg_field* field, const double* raw, int n_raw, const lg_run_params* params,
+                   int c0, int m, double* pose, int* accepted, double* penetration,
+                   int* n_static, double* static_p, double* static_n, int* static_link);
+
+/* optimize_contacts (contact_opt.cpp:45-142; contact_opt.hpp:49-52) for m
+ * problems of k domains each: domain (i, q) is elements
+ * [dom_off[i*k+q], dom_off[i*k+q+1]) of dom_pos / dom_nrm (element positions
+ * and outward normals, [*][3]); n_static[i] in {0,1} static contacts
+ * (static_p / static_n [m][3], normal = inward force direction); params gives
+ * n_outer, n_inner, restarts, sigma, lambda_torque, mu and the PGD settings;
+ * seeds[i] the problem's stream seed.  Writes element_ids [m][k], the
+ * objective, the solution (anchor; alpha / beta_x / beta_y [m][6] over
+ * [slot contacts..., static]) and the number of wrench solves. */
+int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_off,
+                               const double* dom_pos, const double* dom_nrm, const int* n_static,
+                               const double* static_p, const double* static_n,
+                               const lg_run_params* params, const uint64_t* seeds,
+                               int* element_ids, double* objective, int* anchor, double* alpha,
+                               double* beta_x, double* beta_y, long long* evaluations);
+
+/* realize_grasp's final projection (pipeline.cpp:196-221,250; RealizeResult
+ * pipeline.hpp:108-115): for configuration q[i] and problem i's k[i] targets
+ * (link, world object point; CSR like lg_realize_batch), the realized contact
+ * on the hand surface (world position, outward normal, link) and the
+ * position residual per target. */
+int lg_realized_contacts_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                               const double* q, const int* links, const double* object_points,
+                               double* realized_p, double* realized_n, int* realized_link,
+                               double* residuals);
+
+/* validate_grasp_collisions' full CollisionReport (collision.cpp:230-288;
+ * collision.hpp:57-65) for m configurations: violations deduplicated per
+ * link pair in the reference's pair order (link_b = -1: the object; depth 0
+ * for hand-hand), up to cap per configuration ([m][cap]); n_violations[i]
+ * is the full count; max_penetration and the broad-phase pair count. */
+int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const double* q,
+                              const double* poses, const double* samples, int n, double margin,
+                              int cap, int* n_violations, int* link_a, int* link_b, double* depth,
+                              double* max_penetration, int* broad_pairs);
+
 /* preprocess_object (pipeline.cpp:71-98): keep[i] = 1 when sample i survives. */
 int lg_preprocess(lg_ctx* ctx, const double* samples, int n,
                   double probe_half_width, double depth_threshold,

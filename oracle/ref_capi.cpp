@@ -779,7 +779,7 @@ int ref_realize(const ref_inputs* in, const double* q0, int k, const double* obj
 // max penetration and the violation list (link_b = -1 for the object).
 int ref_collision(const ref_inputs* in, const double* q, const double* pose12, const double* samples,
                   int n, double margin, int* clean, double* max_penetration, int* n_viol, int cap,
-                  int* viol_a, int* viol_b, double* viol_depth) {
+                  int* viol_a, int* viol_b, double* viol_depth, int* broad_pairs) {
   return guard([&] {
     const int dof = in->model.actuated_count;
     Eigen::VectorXd qv(dof);
@@ -788,6 +788,7 @@ int ref_collision(const ref_inputs* in, const double* q, const double* pose12, c
     CollisionReport r = validate_grasp_collisions(in->model, qv, s, get_pose12(pose12), margin);
     *clean = r.clean() ? 1 : 0;
     *max_penetration = r.max_penetration;
+    if (broad_pairs) *broad_pairs = static_cast<int>(r.broad_pairs);
     *n_viol = static_cast<int>(r.violations.size());
     for (int i = 0; i < *n_viol && i < cap; ++i) {
       const CollisionViolation& v = r.violations[i];

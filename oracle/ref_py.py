@@ -80,7 +80,7 @@ def lib():
                                       C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, dp, dp,
                                       ip, P(C.c_ulonglong), dp, dp, ip, dp]),
             "ref_collision": (C.c_int, [vp, dp, dp, dp, C.c_int, C.c_double, ip, dp, ip, C.c_int,
-                                        ip, ip, dp]),
+                                        ip, ip, dp, ip]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -406,12 +406,13 @@ def realize(inputs, q0, targets, beta=0.01, iterations=30, step_clamp=0.2, resid
 
 def collision(inputs, q, pose12, samples, margin=0.002, cap=256):
     s = _d(samples).reshape(-1, 6)
-    clean, mp, nv = C.c_int(0), C.c_double(0), C.c_int(0)
+    clean, mp, nv, bp = C.c_int(0), C.c_double(0), C.c_int(0), C.c_int(0)
     va, vb = np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
     vd = np.zeros(cap)
     check(lib().ref_collision(inputs._h, _p(_d(q)), _p(_d(pose12)), _p(s), len(s), float(margin),
                               C.byref(clean), C.byref(mp), C.byref(nv), cap, _i(va), _i(vb),
-                              _p(vd)))
+                              _p(vd), C.byref(bp)))
     n = min(nv.value, cap)
     return {"clean": clean.value, "max_penetration": mp.value, "n_violations": nv.value,
+            "broad_pairs": bp.value,
             "violations": list(zip(va[:n].tolist(), vb[:n].tolist(), vd[:n].tolist()))}

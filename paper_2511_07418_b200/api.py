@@ -81,6 +81,25 @@ def lib():
         "lg_result_traces": (P(A.Trace), [vp]),
         "lg_result_destroy": (None, [vp]),
         "lg_libm_eval": (C.c_int, [vp, C.c_int, C.c_longlong, A.dp, A.dp, A.dp]),
+        "lg_query_domains_elements": (C.c_int, [vp, vp, A.ip, C.c_int, A.dp, C.c_int, A.dp,
+                                                C.c_double, P(vp)]),
+        "lg_domains_group": (C.c_int, [vp, C.c_int, P(C.c_longlong), P(C.c_longlong)]),
+        "lg_domains_elements": (C.c_int, [vp, P(C.c_longlong), P(A.ip), P(A.dp), P(A.dp), P(A.dp),
+                                          P(A.llp), P(A.ip), P(A.ip)]),
+        "lg_domains_destroy": (None, [vp]),
+        "lg_reverse_lookup_batch": (C.c_int, [vp, vp, C.c_int, A.llp, A.ip, A.ip, A.dp,
+                                              P(C.c_uint64), A.ip, A.dp, A.dp]),
+        "lg_place_batch": (C.c_int, [vp, P(A.HandDesc), P(A.PatchesDesc), vp, A.dp, C.c_int,
+                                     P(A.RunParams), C.c_int, C.c_int, A.dp, A.ip, A.dp, A.ip,
+                                     A.dp, A.dp, A.ip]),
+        "lg_optimize_contacts_batch": (C.c_int, [vp, C.c_int, C.c_int, A.llp, A.dp, A.dp, A.ip,
+                                                 A.dp, A.dp, P(A.RunParams), P(C.c_uint64), A.ip,
+                                                 A.dp, A.ip, A.dp, A.dp, A.dp, A.llp]),
+        "lg_realized_contacts_batch": (C.c_int, [vp, P(A.HandDesc), C.c_int, A.ip, A.dp, A.ip,
+                                                 A.dp, A.dp, A.dp, A.ip, A.dp]),
+        "lg_collision_report_batch": (C.c_int, [vp, P(A.HandDesc), C.c_int, A.dp, A.dp, A.dp,
+                                                C.c_int, C.c_double, C.c_int, A.ip, A.ip, A.ip,
+                                                A.dp, A.dp, A.ip]),
         "lg_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "lg_comm_init": (C.c_int, [vp, C.POINTER(C.c_ubyte), C.c_int, C.c_int, P(vp)]),
         "lg_comm_destroy": (None, [vp]),
@@ -444,3 +463,157 @@ def realize_batch(ctx, hand, q0, problems, beta=0.01, iterations=30, step_clamp=
                              int(finetune_iterations), _dp(q), _dp(mr), _ip(fin),
                              used.ctypes.data_as(C.POINTER(C.c_ulonglong))))
     return q, mr, fin.astype(bool), used
+
+
+# ------------------------------------------------ stage-level entry points
+def _llp(a):
+    return a.ctypes.data_as(A.llp)
+
+
+def query_domains_elements(ctx, field, group_of_patch, n_groups, samples, pose12, theta_hit):
+    """query_domains (contact_field.cpp:380-448) for one pose: list over
+    groups of element dicts {sample, pos, nrm, score, hits: [(patch, box)]}."""
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    g = np.ascontiguousarray(group_of_patch, dtype=np.int32)
+    pose = np.ascontiguousarray(pose12, dtype=np.float64).reshape(12)
+    L = lib()
+    h = C.c_void_p()
+    check(L.lg_query_domains_elements(ctx._h, field._h, _ip(g), int(n_groups), _dp(s), len(s),
+                                      _dp(pose), float(theta_hit), C.byref(h)))
+    try:
+        n = C.c_longlong(0)
+        sp, pp, nn, sc, ho, hp, hb = (A.ip(), A.dp(), A.dp(), A.dp(), A.llp(), A.ip(), A.ip())
+        check(L.lg_domains_elements(h, C.byref(n), C.byref(sp), C.byref(pp), C.byref(nn),
+                                    C.byref(sc), C.byref(ho), C.byref(hp), C.byref(hb)))
+        E = n.value
+        arr = np.ctypeslib.as_array
+        off = arr(ho, shape=(E + 1,)).copy() if E else np.zeros(1, np.int64)
+        H = int(off[-1])
+        sample = arr(sp, shape=(E,)).copy() if E else np.zeros(0, np.int32)
+        pos = arr(pp, shape=(3 * E,)).reshape(-1, 3).copy() if E else np.zeros((0, 3))
+        nrm = arr(nn, shape=(3 * E,)).reshape(-1, 3).copy() if E else np.zeros((0, 3))
+        score = arr(sc, shape=(E,)).copy() if E else np.zeros(0)
+        hpa = arr(hp, shape=(H,)).copy() if H else np.zeros(0, np.int32)
+        hba = arr(hb, shape=(H,)).copy() if H else np.zeros(0, np.int32)
+        out = []
+        for grp in range(int(n_groups)):
+            f, c = C.c_longlong(0), C.c_longlong(0)
+            check(L.lg_domains_group(h, grp, C.byref(f), C.byref(c)))
+            els = []
+            for e in range(f.value, f.value + c.value):
+                els.append({"sample": int(sample[e]), "pos": pos[e], "nrm": nrm[e],
+                            "score": float(score[e]),
+                            "hits": list(zip(hpa[off[e]:off[e + 1]].tolist(),
+                                             hba[off[e]:off[e + 1]].tolist()))})
+            out.append(els)
+        return out
+    finally:
+        L.lg_domains_destroy(h)
+
+
+def reverse_lookup_batch(ctx, field, elements, seeds):
+    """reverse_lookup (contact_field.cpp:450-484) for elements (dicts with
+    'hits' and 'nrm') -> (links, points, normals)."""
+    m = len(elements)
+    off = np.zeros(m + 1, dtype=np.int64)
+    for i, e in enumerate(elements):
+        off[i + 1] = off[i] + len(e["hits"])
+    hp = np.array([h[0] for e in elements for h in e["hits"]] or [0], dtype=np.int32)
+    hb = np.array([h[1] for e in elements for h in e["hits"]] or [0], dtype=np.int32)
+    nr = np.ascontiguousarray([e["nrm"] for e in elements], dtype=np.float64).reshape(-1, 3)
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    link = np.zeros(m, dtype=np.int32)
+    pt, nn = np.zeros((m, 3)), np.zeros((m, 3))
+    check(lib().lg_reverse_lookup_batch(ctx._h, field._h, m, _llp(off), _ip(hp), _ip(hb), _dp(nr),
+                                        sd.ctypes.data_as(C.POINTER(C.c_uint64)), _ip(link),
+                                        _dp(pt), _dp(nn)))
+    return link, pt, nn
+
+
+def place_batch(ctx, hand, patches, raw_samples, params, c0, m, field=None):
+    """place_object (pipeline.cpp:122-183) for candidates [c0, c0+m)."""
+    raw = np.ascontiguousarray(raw_samples, dtype=np.float64).reshape(-1, 6)
+    pose = np.zeros((m, 12))
+    acc, nst, stl = (np.zeros(m, np.int32) for _ in range(3))
+    pen = np.zeros(m)
+    stp, stn = np.zeros((m, 3)), np.zeros((m, 3))
+    check(lib().lg_place_batch(ctx._h, C.byref(hand.desc), C.byref(patches.desc),
+                               field._h if field is not None else None, _dp(raw), len(raw),
+                               C.byref(params), int(c0), int(m), _dp(pose), _ip(acc), _dp(pen),
+                               _ip(nst), _dp(stp), _dp(stn), _ip(stl)))
+    return dict(pose=pose, accepted=acc, penetration=pen, n_static=nst, static_p=stp,
+                static_n=stn, static_link=stl)
+
+
+def optimize_contacts_batch(ctx, problems, params, seeds):
+    """optimize_contacts (contact_opt.cpp:45-142); problems = [(domains,
+    statics)] with domains = [(positions [n,3], normals [n,3])] * k and
+    statics = [] or [(p, n)]."""
+    m = len(problems)
+    k = len(problems[0][0])
+    off = [0]
+    P, N = [], []
+    nst = np.zeros(m, np.int32)
+    sp, sn = np.zeros((m, 3)), np.zeros((m, 3))
+    for i, (doms, st) in enumerate(problems):
+        assert len(doms) == k
+        for pos, nrm in doms:
+            pos = np.asarray(pos, dtype=np.float64).reshape(-1, 3)
+            P.append(pos)
+            N.append(np.asarray(nrm, dtype=np.float64).reshape(-1, 3))
+            off.append(off[-1] + len(pos))
+        if st:
+            nst[i] = 1
+            sp[i], sn[i] = st[0][0], st[0][1]
+    off = np.array(off, dtype=np.int64)
+    P = np.ascontiguousarray(np.concatenate(P))
+    N = np.ascontiguousarray(np.concatenate(N))
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    ids = np.zeros((m, k), np.int32)
+    obj = np.zeros(m)
+    anc = np.zeros(m, np.int32)
+    al, bx, by = np.zeros((m, 6)), np.zeros((m, 6)), np.zeros((m, 6))
+    ev = np.zeros(m, np.int64)
+    check(lib().lg_optimize_contacts_batch(ctx._h, m, k, _llp(off), _dp(P), _dp(N), _ip(nst), _dp(sp),
+                                           _dp(sn), C.byref(params),
+                                           sd.ctypes.data_as(C.POINTER(C.c_uint64)), _ip(ids),
+                                           _dp(obj), _ip(anc), _dp(al), _dp(bx), _dp(by),
+                                           _llp(ev)))
+    return dict(element_ids=ids, objective=obj, anchor=anc, alpha=al, beta_x=bx, beta_y=by,
+                evaluations=ev)
+
+
+def realized_contacts_batch(ctx, hand, q, problems):
+    """realize_grasp's final projection: problems = [[(link, object_point)]]."""
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(len(problems), -1)
+    k = np.array([len(t) for t in problems], np.int32)
+    links = np.array([l for t in problems for l, _ in t], np.int32)
+    op = np.ascontiguousarray([p for t in problems for _, p in t], dtype=np.float64).reshape(-1, 3)
+    n = len(links)
+    rp, rn, rs = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(n)
+    rl = np.zeros(n, np.int32)
+    check(lib().lg_realized_contacts_batch(ctx._h, C.byref(hand.desc), len(problems), _ip(k), _dp(q),
+                                           _ip(links), _dp(op), _dp(rp), _dp(rn), _ip(rl), _dp(rs)))
+    return rp, rn, rl, rs
+
+
+def collision_report_batch(ctx, hand, q, poses, samples, margin=0.002, cap=64):
+    """validate_grasp_collisions' CollisionReport for each configuration."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    m = q.shape[0]
+    poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(m, 12)
+    s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
+    nv, bp = np.zeros(m, np.int32), np.zeros(m, np.int32)
+    la, lb = np.zeros((m, cap), np.int32), np.zeros((m, cap), np.int32)
+    dd, mp = np.zeros((m, cap)), np.zeros(m)
+    check(lib().lg_collision_report_batch(ctx._h, C.byref(hand.desc), m, _dp(q), _dp(poses), _dp(s),
+                                          len(s), float(margin), int(cap), _ip(nv), _ip(la),
+                                          _ip(lb), _dp(dd), _dp(mp), _ip(bp)))
+    out = []
+    for i in range(m):
+        n = min(nv[i], cap)
+        out.append(dict(n_violations=int(nv[i]), max_penetration=float(mp[i]),
+                        broad_pairs=int(bp[i]),
+                        violations=list(zip(la[i, :n].tolist(), lb[i, :n].tolist(),
+                                            dd[i, :n].tolist()))))
+    return out

@@ -489,9 +489,17 @@ DSamples make_samples(Buf* cols, int n) {
   return d;
 }
 
+// place_object for candidates [c0, c0 + m) only (lg_place_batch): run_batch's
+// stage-1 placement, then return the records.
+struct PlaceOnly {
+  int c0 = 0, m = 0;
+  std::vector<double> pose, pen, stp, stn;
+  std::vector<int> acc, nst, stl;
+};
+
 void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc& pd,
                       lg_field* field_in, const double* raw, int n_raw, const lg_run_params& cfg,
-                      RunOut& out) {
+                      RunOut& out, PlaceOnly* place_only = nullptr) {
   auto wall0 = std::chrono::steady_clock::now();
   cudaStream_t s = ctx->stream;
   std::memset(&out.profile, 0, sizeof(out.profile));
@@ -643,6 +651,10 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     c_lo = (int)((long long)cfg.shard_rank * B / cfg.shard_count);
     c_hi = (int)((long long)(cfg.shard_rank + 1) * B / cfg.shard_count);
   }
+  if (place_only) {
+    c_lo = place_only->c0;
+    c_hi = place_only->c0 + place_only->m;
+  }
   const int Bl = c_hi - c_lo;
   const int k = cfg.k_contacts;
   out.profile.candidates = (long long)cfg.passes * Bl;
@@ -724,6 +736,16 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                          d_acc, d_pen);
       LAUNCH(ctx);
       check_launch();
+      if (place_only) {
+        place_only->pose = ddownload(d_pose, 12 * (size_t)Bl, s);
+        place_only->acc = ddownload(d_acc, (size_t)Bl, s);
+        place_only->pen = ddownload(d_pen, (size_t)Bl, s);
+        place_only->nst = ddownload(d_nst, (size_t)Bl, s);
+        place_only->stl = ddownload(d_stl, (size_t)Bl, s);
+        place_only->stp = ddownload(d_stp, 3 * (size_t)Bl, s);
+        place_only->stn = ddownload(d_stn, 3 * (size_t)Bl, s);
+        return;
+      }
       if (ensure_dirlists(field, cfg.theta_hit)) {
         size_t qsm = codebook_smem(k_query3, F.C);
         k_query3<<<Bl, 256, qsm, s>>>(Bl, field->f, FS, d_pose, d_acc, cfg.theta_hit, G, qsm > 0,
@@ -2112,6 +2134,628 @@ int lg_comm_gather(lg_comm* c, const lg_grasp* grasps, long long n, const lg_pro
       merged->postprocessing = mx(kHdrPostS);
       merged->field_build = mx(kHdrFieldS);
       merged->grasps_per_second = merged->total > 0.0 ? merged->valid / merged->total : 0.0;
+    }
+  });
+}
+
+}  // extern "C"
+
+// ================================================== stage-level entry points
+// The reference's public hot-path functions, batched:
+// place_object, query_domains (full ContactDomain elements with hits),
+// reverse_lookup, optimize_contacts, realize_grasp's final projection, and
+// validate_grasp_collisions' full report.  Each reuses the kernels of
+// run_batch; the parity tests call them against the reference's own
+// functions (oracle/_ref) on identical inputs.
+namespace lgd {
+
+// query_domains (contact_field.cpp:380-448), one pose: pass 1 counts each
+// sample's hits per dependency group, pass 2 writes the elements.
+__global__ void k_qe_count(int n, DField f, DSamples S, Xf x, double theta, const int* gop, int G,
+                           int* cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 p = xf_apply(x, S.p(i)), nn = xf_rotate(x, S.nrm(i));
+  sample_hits(f, f.codebook, p, nn, theta, [&](int patch, int, double) {
+    int g = gop[patch];
+    if (g >= 0 && g < G) ++cnt[(size_t)g * n + i];
+  });
+}
+
+__global__ void k_qe_fill(int n, DField f, DSamples S, Xf x, double theta, const int* gop, int G,
+                          const long long* elem_of, const long long* hit_of, long long* hit_off,
+                          int* sample, double* pos, double* nrm, double* score, int* hit_patch,
+                          int* hit_box) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 p = xf_apply(x, S.p(i)), nn = xf_rotate(x, S.nrm(i));
+  for (int g = 0; g < G; ++g) {
+    long long e = elem_of[(size_t)g * n + i];
+    if (e < 0) continue;
+    long long h = hit_of[(size_t)g * n + i];
+    hit_off[e] = h;
+    sample[e] = i;
+    v3_store(pos + 3 * e, p);
+    v3_store(nrm + 3 * e, nn);
+    double sc = 0.0;  // DomainElement::score starts at 0.0 (contact_field.hpp:104)
+    sample_hits(f, f.codebook, p, nn, theta, [&](int patch, int b, double) {
+      if (gop[patch] != g) return;
+      double best = -2.0;
+      for (long long q = f.box_code_off[b]; q < f.box_code_off[b + 1]; ++q) {
+        int c = f.codes[q];
+        best = dmax(best, -dot(v3(f.codebook[3 * c], f.codebook[3 * c + 1], f.codebook[3 * c + 2]), nn));
+      }
+      sc = dmax(sc, best);
+      hit_patch[h] = patch;
+      hit_box[h] = b - f.patch_box_off[patch];
+      ++h;
+    });
+    score[e] = sc;
+  }
+}
+
+// reverse_lookup (contact_field.cpp:450-484) per element.
+__global__ void k_reverse_lookup(int m, DField f, const long long* hit_off, const int* hit_patch,
+                                 const int* hit_box, const double* nrm, const uint64_t* seeds,
+                                 int* link, double* point, double* normal, int* err) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  long long h0 = hit_off[t], nh = hit_off[t + 1] - h0;
+  if (nh <= 0) {
+    atomicMax(err, 1);
+    return;
+  }
+  DRng rng;
+  rng.seed(seeds[t]);
+  long long pick = (long long)rng.index((uint64_t)nh);
+  int patch = hit_patch[h0 + pick], box = hit_box[h0 + pick];
+  if (patch < 0 || patch >= f.P || box < 0 || box >= f.patch_box_off[patch + 1] - f.patch_box_off[patch]) {
+    atomicMax(err, 2);
+    return;
+  }
+  long long b = f.patch_box_off[patch] + box;
+  V3 n = v3_load(nrm + 3 * t);
+  int best = -1;
+  double best_dot = -2.0;
+  long long q0 = f.box_code_off[b], q1 = f.box_code_off[b + 1];
+  for (long long q = q0; q < q1; ++q) {
+    int c = f.codes[q];
+    double d = -dot(v3(f.codebook[3 * c], f.codebook[3 * c + 1], f.codebook[3 * c + 2]), n);
+    if (d > best_dot) {
+      best_dot = d;
+      best = (int)(q - q0);
+    }
+  }
+  const double* rp = f.rep_pn + 6 * (q0 + best);
+  v3_store(point + 3 * t, v3_load(rp));
+  v3_store(normal + 3 * t, v3_load(rp + 3));
+  link[t] = f.rep_link[q0 + best];
+}
+
+// optimize_contacts' stream draws from explicit seeds (contact_opt.cpp:61).
+__global__ void k_copt_draws_seeded(int m, const uint64_t* seeds, long long per_cand, uint64_t* out) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  Mt64 g;
+  mt_seed(g, seeds[a]);
+  uint64_t* o = out + (size_t)a * per_cand;
+  for (long long d = 0; d < per_cand; ++d) o[d] = mt_next(g);
+}
+
+// realize_grasp's final projection (pipeline.cpp:196-221, 250): realized
+// contact and position residual per target at configuration q.
+__global__ void k_realized(int m, int kmax, const int* k, const double* q, int dof, const int* links,
+                           const double* obj_p, double* rp, double* rn, int* rl, double* res) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * kmax) return;
+  int i = t / kmax, c = t % kmax;
+  if (c >= k[i]) return;
+  double qq[kMaxDof];
+  for (int j = 0; j < dof; ++j) qq[j] = q[(size_t)i * dof + j];
+  Xf frames[kMaxLinks];
+  fk(qq, frames);
+  int l = links[t];
+  Xf inv = xf_inverse(frames[l]);
+  V3 sp = v3(0, 0, 0), sn = v3(0, 0, 0);
+  double d = closest_on_parts(l, xf_apply(inv, v3_load(obj_p + 3 * t)), &sp, &sn);
+  v3_store(rp + 3 * t, xf_apply(frames[l], sp));
+  v3_store(rn + 3 * t, xf_rotate(frames[l], sn));
+  rl[t] = l;
+  res[t] = d;
+}
+
+// validate_grasp_collisions (collision.cpp:230-288), the full report: thread
+// per configuration, violations deduplicated per link pair in pair order.
+__global__ void k_collision_report(int m, const double* q, int dof, const double* poses, DSamples S,
+                                   double margin, const int* part_link, int cap, int* n_viol,
+                                   int* va, int* vb, double* vd, double* max_pen, int* pairs) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double qq[kMaxDof];
+  for (int j = 0; j < dof; ++j) qq[j] = q[(size_t)i * dof + j];
+  Xf frames[kMaxLinks];
+  fk(qq, frames);
+  Xf op = load_xf(poses + 12 * i);
+  V3 omn = v3(kInf, kInf, kInf), omx = v3(-kInf, -kInf, -kInf);
+  for (int s = 0; s < S.n; ++s) {
+    V3 w = xf_apply(op, S.p(s));
+    omn = vmin(omn, w);
+    omx = vmax(omx, w);
+  }
+  const bool has_obj = S.n > 0;
+  omn = v3(omn.x - margin, omn.y - margin, omn.z - margin);
+  omx = v3(omx.x + margin, omx.y + margin, omx.z + margin);
+  const int np = c_hand.n_parts;
+  int nv = 0, npairs = 0;
+  double mp = 0.0;
+  int* A = va + (size_t)i * cap;
+  int* Bv = vb + (size_t)i * cap;
+  double* D = vd + (size_t)i * cap;
+  auto record = [&](int la, int lb, double depth) {
+    for (int v = 0; v < nv && v < cap; ++v)
+      if (A[v] == la && Bv[v] == lb) {
+        D[v] = dmax(D[v], depth);
+        return;
+      }
+    if (nv < cap) {
+      A[nv] = la;
+      Bv[nv] = lb;
+      D[nv] = depth;
+    }
+    ++nv;
+  };
+  for (int a = 0; a < np; ++a) {
+    const int la = part_link[a];
+    V3 amn, amx;
+    world_bounds(a, frames[la], &amn, &amx);
+    amn = v3(amn.x - margin, amn.y - margin, amn.z - margin);
+    amx = v3(amx.x + margin, amx.y + margin, amx.z + margin);
+    for (int b = a + 1; b < np; ++b) {
+      const int lb = part_link[b];
+      V3 bmn, bmx;
+      world_bounds(b, frames[lb], &bmn, &bmx);
+      bmn = v3(bmn.x - margin, bmn.y - margin, bmn.z - margin);
+      bmx = v3(bmx.x + margin, bmx.y + margin, bmx.z + margin);
+      const bool ov = amn.x <= bmx.x && amn.y <= bmx.y && amn.z <= bmx.z && amx.x >= bmn.x &&
+                      amx.y >= bmn.y && amx.z >= bmn.z;
+      if (!ov) continue;
+      ++npairs;
+      if (la == lb || c_hand.parent[la] == lb || c_hand.parent[lb] == la) continue;
+      if (gjk_distance(a, frames[la], b, frames[lb]) == 0.0) record(la < lb ? la : lb, la < lb ? lb : la, 0.0);
+    }
+    if (has_obj && amn.x <= omx.x && amn.y <= omx.y && amn.z <= omx.z && amx.x >= omn.x &&
+        amx.y >= omn.y && amx.z >= omn.z) {
+      ++npairs;
+      // object_penetration (collision.cpp:209-228)
+      Xf inv = xf_inverse(frames[la]);
+      const double* bb = c_hand.bounds + 6 * a;
+      double md = 0.0;
+      bool off = false;
+      for (int s = 0; s < S.n; ++s) {
+        V3 local = xf_apply(inv, xf_apply(op, S.p(s)));
+        if (!(local.x >= bb[0] - 1e-9 && local.y >= bb[1] - 1e-9 && local.z >= bb[2] - 1e-9 &&
+              local.x <= bb[3] + 1e-9 && local.y <= bb[4] + 1e-9 && local.z <= bb[5] + 1e-9))
+          continue;
+        double depth = part_interior_depth(a, local);
+        if (depth > margin) {
+          off = true;
+          md = dmax(md, depth);
+        }
+      }
+      if (off) {
+        record(la, -1, md);
+        mp = dmax(mp, md);
+      }
+    }
+  }
+  n_viol[i] = nv;
+  max_pen[i] = mp;
+  pairs[i] = npairs;
+}
+
+}  // namespace lgd
+
+struct lg_domains {
+  int n_groups = 0;
+  std::vector<long long> group_off;  // [G+1] element ranges per group
+  std::vector<long long> hit_off;    // [E+1]
+  std::vector<int> sample, hit_patch, hit_box;
+  std::vector<double> pos, nrm, score;
+};
+
+extern "C" {
+
+int lg_query_domains_elements(lg_ctx* ctx, lg_field* f, const int* group_of_patch, int n_groups,
+                              const double* samples, int n, const double* pose, double theta_hit,
+                              lg_domains** out) {
+  return lgc::guard([&] {
+    if (!ctx || !f || !group_of_patch || !samples || !pose || !out || n < 0 || n_groups < 0)
+      throw std::invalid_argument("lg_query_domains_elements: bad argument");
+    for (int p = 0; p < f->f.P; ++p)
+      if (group_of_patch[p] >= n_groups)
+        throw std::invalid_argument("query_domains: index link out of range");
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    auto d = std::make_unique<lg_domains>();
+    d->n_groups = n_groups;
+    const int G = n_groups;
+    std::vector<double> col((size_t)std::max(n, 1));
+    Buf sc[6], bg, bc;
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < n; ++i) col[i] = samples[6 * i + a];
+      dupload(sc[a], col.data(), (size_t)n, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    DSamples S = make_samples(sc, n);
+    Xf x = lgm::xf_identity();
+    x.R = lgm::m3_load(pose);
+    x.t = lgm::v3_load(pose + 9);
+    int* d_g = dupload(bg, group_of_patch, (size_t)f->f.P, s);
+    int* d_c = dalloc<int>(bc, (size_t)std::max(G, 1) * std::max(n, 1));
+    CK(cudaMemsetAsync(d_c, 0, sizeof(int) * (size_t)std::max(G, 1) * std::max(n, 1), s));
+    d->group_off.assign((size_t)G + 1, 0);
+    d->hit_off.assign(1, 0);
+    if (n > 0 && G > 0) {
+      lgd::k_qe_count<<<grid_for(n, 128), 128, 0, s>>>(n, f->f, S, x, theta_hit, d_g, G, d_c);
+      check_launch();
+      LAUNCH(ctx);
+      auto cnt = ddownload(d_c, (size_t)G * n, s);
+      std::vector<long long> eo((size_t)G * n, -1), ho((size_t)G * n, 0);
+      long long E = 0, H = 0;
+      for (int g = 0; g < G; ++g) {
+        for (int i = 0; i < n; ++i) {
+          int c = cnt[(size_t)g * n + i];
+          if (!c) continue;
+          eo[(size_t)g * n + i] = E++;
+          ho[(size_t)g * n + i] = H;
+          H += c;
+        }
+        d->group_off[g + 1] = E;
+      }
+      d->hit_off.assign((size_t)E + 1, H);
+      d->sample.resize(E);
+      d->pos.resize(3 * E);
+      d->nrm.resize(3 * E);
+      d->score.resize(E);
+      d->hit_patch.resize(H);
+      d->hit_box.resize(H);
+      if (E > 0) {
+        Buf be, bh, bho, bs, bp, bn, bsc, bhp, bhb;
+        long long* d_eo = dupload(be, eo.data(), eo.size(), s);
+        long long* d_ho = dupload(bh, ho.data(), ho.size(), s);
+        long long* d_hoff = dalloc<long long>(bho, (size_t)E);
+        int* d_s = dalloc<int>(bs, (size_t)E);
+        double* d_p = dalloc<double>(bp, 3 * (size_t)E);
+        double* d_n = dalloc<double>(bn, 3 * (size_t)E);
+        double* d_sc = dalloc<double>(bsc, (size_t)E);
+        int* d_hp = dalloc<int>(bhp, (size_t)H);
+        int* d_hb = dalloc<int>(bhb, (size_t)H);
+        lgd::k_qe_fill<<<grid_for(n, 128), 128, 0, s>>>(n, f->f, S, x, theta_hit, d_g, G, d_eo, d_ho,
+                                                       d_hoff, d_s, d_p, d_n, d_sc, d_hp, d_hb);
+        check_launch();
+        LAUNCH(ctx);
+        auto hoff = ddownload(d_hoff, (size_t)E, s);
+        std::copy(hoff.begin(), hoff.end(), d->hit_off.begin());
+        d->sample = ddownload(d_s, (size_t)E, s);
+        d->pos = ddownload(d_p, 3 * (size_t)E, s);
+        d->nrm = ddownload(d_n, 3 * (size_t)E, s);
+        d->score = ddownload(d_sc, (size_t)E, s);
+        d->hit_patch = ddownload(d_hp, (size_t)H, s);
+        d->hit_box = ddownload(d_hb, (size_t)H, s);
+      }
+    }
+    *out = d.release();
+  });
+}
+
+int lg_domains_group(const lg_domains* d, int group, long long* first, long long* count) {
+  return lgc::guard([&] {
+    if (!d || group < 0 || group >= d->n_groups || !first || !count)
+      throw std::invalid_argument("lg_domains_group: bad argument");
+    *first = d->group_off[group];
+    *count = d->group_off[group + 1] - d->group_off[group];
+  });
+}
+
+int lg_domains_elements(const lg_domains* d, long long* n_elements, const int** sample,
+                        const double** pos, const double** nrm, const double** score,
+                        const long long** hit_off, const int** hit_patch, const int** hit_box) {
+  return lgc::guard([&] {
+    if (!d) throw std::invalid_argument("lg_domains_elements: null handle");
+    if (n_elements) *n_elements = (long long)d->sample.size();
+    if (sample) *sample = d->sample.data();
+    if (pos) *pos = d->pos.data();
+    if (nrm) *nrm = d->nrm.data();
+    if (score) *score = d->score.data();
+    if (hit_off) *hit_off = d->hit_off.data();
+    if (hit_patch) *hit_patch = d->hit_patch.data();
+    if (hit_box) *hit_box = d->hit_box.data();
+  });
+}
+
+void lg_domains_destroy(lg_domains* d) { delete d; }
+
+int lg_reverse_lookup_batch(lg_ctx* ctx, lg_field* f, int m, const long long* hit_off,
+                            const int* hit_patch, const int* hit_box, const double* normals,
+                            const uint64_t* seeds, int* link, double* point, double* normal) {
+  return lgc::guard([&] {
+    if (!ctx || !f || m < 0 || (m && (!hit_off || !normals || !seeds || !link || !point || !normal)))
+      throw std::invalid_argument("lg_reverse_lookup_batch: bad argument");
+    if (m == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    const long long H = hit_off[m] - hit_off[0];
+    Buf bo, bp, bb, bn, bs, bl, bpt, bnr, be;
+    std::vector<long long> off(hit_off, hit_off + m + 1);
+    for (auto& o : off) o -= hit_off[0];
+    long long* d_o = dupload(bo, off.data(), off.size(), s);
+    int* d_p = dupload(bp, hit_patch ? hit_patch + hit_off[0] : nullptr, (size_t)H, s);
+    int* d_b = dupload(bb, hit_box ? hit_box + hit_off[0] : nullptr, (size_t)H, s);
+    double* d_n = dupload(bn, normals, 3 * (size_t)m, s);
+    uint64_t* d_s = dupload(bs, seeds, (size_t)m, s);
+    int* d_l = dalloc<int>(bl, (size_t)m);
+    double* d_pt = dalloc<double>(bpt, 3 * (size_t)m);
+    double* d_nr = dalloc<double>(bnr, 3 * (size_t)m);
+    int zero = 0;
+    int* d_e = dupload(be, &zero, 1, s);
+    lgd::k_reverse_lookup<<<grid_for(m, 128), 128, 0, s>>>(m, f->f, d_o, d_p, d_b, d_n, d_s, d_l, d_pt,
+                                                          d_nr, d_e);
+    check_launch();
+    LAUNCH(ctx);
+    int err = ddownload(d_e, 1, s)[0];
+    if (err == 1) throw std::out_of_range("reverse_lookup: element has no hits");
+    if (err == 2) throw std::out_of_range("reverse_lookup: stale element");
+    auto l = ddownload(d_l, (size_t)m, s);
+    auto pt = ddownload(d_pt, 3 * (size_t)m, s);
+    auto nr = ddownload(d_nr, 3 * (size_t)m, s);
+    std::copy(l.begin(), l.end(), link);
+    std::copy(pt.begin(), pt.end(), point);
+    std::copy(nr.begin(), nr.end(), normal);
+  });
+}
+
+int lg_place_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* patches,
+                   lg_field* field, const double* raw, int n_raw, const lg_run_params* p, int c0,
+                   int m, double* pose, int* accepted, double* penetration, int* n_static,
+                   double* static_p, double* static_n, int* static_link) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || !patches || !raw || !p || m < 0 || c0 < 0)
+      throw std::invalid_argument("lg_place_batch: bad argument");
+    if (m == 0) return;
+    use_ctx(ctx);
+    RunOut ro;
+    PlaceOnly po;
+    po.c0 = c0;
+    po.m = m;
+    lg_run_params q = *p;
+    q.passes = 1;
+    q.want_trace = 0;
+    q.shard_count = 1;
+    run_batch_device(ctx, *hand, *patches, field, raw, n_raw, q, ro, &po);
+    std::copy(po.pose.begin(), po.pose.end(), pose);
+    std::copy(po.acc.begin(), po.acc.end(), accepted);
+    std::copy(po.pen.begin(), po.pen.end(), penetration);
+    std::copy(po.nst.begin(), po.nst.end(), n_static);
+    if (static_p) std::copy(po.stp.begin(), po.stp.end(), static_p);
+    if (static_n) std::copy(po.stn.begin(), po.stn.end(), static_n);
+    if (static_link) std::copy(po.stl.begin(), po.stl.end(), static_link);
+  });
+}
+
+int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_off,
+                               const double* dom_pos, const double* dom_nrm, const int* n_static,
+                               const double* static_p, const double* static_n,
+                               const lg_run_params* p, const uint64_t* seeds, int* element_ids,
+                               double* objective, int* anchor, double* alpha, double* beta_x,
+                               double* beta_y, long long* evaluations) {
+  return lgc::guard([&] {
+    if (!ctx || !p || m < 0 || (m && (!dom_off || !dom_pos || !dom_nrm || !seeds)))
+      throw std::invalid_argument("lg_optimize_contacts_batch: bad argument");
+    if (k < 1 || k > kMaxK) throw std::invalid_argument("optimize_contacts: 1..5 domains");
+    if (p->n_outer < 0 || p->n_inner < 1 || p->restarts < 1)
+      throw std::invalid_argument("optimize_contacts: bad iteration counts");
+    if (m == 0) return;
+    for (long long t = 0; t < (long long)m * k; ++t)
+      if (dom_off[t + 1] <= dom_off[t]) throw std::invalid_argument("optimize_contacts: empty domain");
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    const long long nel = dom_off[(size_t)m * k] - dom_off[0];
+    std::vector<long long> eloff(dom_off, dom_off + (size_t)m * k + 1);
+    for (auto& o : eloff) o -= dom_off[0];
+    std::vector<int> aidx(m), nst(m, 0);
+    for (int i = 0; i < m; ++i) {
+      aidx[i] = i;
+      nst[i] = n_static ? n_static[i] : 0;
+      if (nst[i] < 0 || nst[i] > 1) throw std::invalid_argument("optimize_contacts: at most one static contact");
+    }
+    std::vector<double> sp(3 * (size_t)m, 0.0), sn(3 * (size_t)m, 0.0);
+    if (static_p) std::copy(static_p, static_p + 3 * (size_t)m, sp.begin());
+    if (static_n) std::copy(static_n, static_n + 3 * (size_t)m, sn.begin());
+    const int R = p->restarts;
+    const long long per_restart = k + 2ll * p->n_outer * k * p->n_inner;
+    const long long per_cand = (long long)R * per_restart;
+    Buf ba, bn, bsp, bsn, bo, bp, bnr, bsd, bdr, boid, bobj, ban, bsol, bbal;
+    int* d_aidx = dupload(ba, aidx.data(), aidx.size(), s);
+    int* d_nst = dupload(bn, nst.data(), nst.size(), s);
+    double* d_stp = dupload(bsp, sp.data(), sp.size(), s);
+    double* d_stn = dupload(bsn, sn.data(), sn.size(), s);
+    long long* d_eloff = dupload(bo, eloff.data(), eloff.size(), s);
+    double* d_elp = dupload(bp, dom_pos + 3 * dom_off[0], 3 * (size_t)nel, s);
+    double* d_eln = dupload(bnr, dom_nrm + 3 * dom_off[0], 3 * (size_t)nel, s);
+    uint64_t* d_seeds = dupload(bsd, seeds, (size_t)m, s);
+    uint64_t* d_draws = dalloc<uint64_t>(bdr, (size_t)m * per_cand);
+    lgd::k_copt_draws_seeded<<<grid_for(m, 64), 64, 0, s>>>(m, d_seeds, per_cand, d_draws);
+    check_launch();
+    LAUNCH(ctx);
+    const int prp = p->n_outer * k * p->n_inner;
+    const long long np = (long long)m * R * prp;
+    if (np > 0) {
+      k_copt_normals<<<grid_for(np, 256), 256, 0, s>>>(np, prp, k, per_restart, p->sigma, d_draws);
+      check_launch();
+      LAUNCH(ctx);
+    }
+    int* d_oid = dalloc<int>(boid, (size_t)m * kMaxK);
+    double* d_oobj = dalloc<double>(bobj, (size_t)m);
+    int* d_oan = dalloc<int>(ban, (size_t)m);
+    double* d_osol = dalloc<double>(bsol, (size_t)m * 3 * kMaxC);
+    int* d_bal = dalloc<int>(bbal, (size_t)m);
+    CoptCfg co;
+    co.k = k;
+    co.n_outer = p->n_outer;
+    co.n_inner = p->n_inner;
+    co.restarts = R;
+    co.sigma = p->sigma;
+    co.lambda = p->lambda_torque;
+    co.mu = p->mu;
+    co.o.iterations = p->pgd_iterations;
+    co.o.warm_iterations = p->pgd_warm_iterations;
+    co.o.step = p->pgd_step;
+    co.o.max_bt = 20;
+    co.per_restart = per_restart;
+    co.per_cand = per_cand;
+    const int nw = std::min(R, 4);
+    CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    auto kern = k + 1 <= 3 ? k_contact_opt2<3, 4> : k_contact_opt2<kMaxC, 4>;
+    size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
+    DomIdx dom{};
+    kern<<<m, 32 * nw, smem, s>>>(m, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, dom,
+                                  d_draws, d_oid, d_oobj, d_oan, d_osol, kInf, d_bal);
+    check_launch();
+    LAUNCH(ctx);
+    auto ids = ddownload(d_oid, (size_t)m * kMaxK, s);
+    auto obj = ddownload(d_oobj, (size_t)m, s);
+    auto an = ddownload(d_oan, (size_t)m, s);
+    auto sol = ddownload(d_osol, (size_t)m * 3 * kMaxC, s);
+    for (int i = 0; i < m; ++i) {
+      for (int q = 0; q < k; ++q) element_ids[(size_t)i * k + q] = ids[(size_t)i * kMaxK + q];
+      objective[i] = obj[i];
+      anchor[i] = an[i];
+      for (int c = 0; c < kMaxC; ++c) {
+        if (alpha) alpha[(size_t)i * kMaxC + c] = sol[(size_t)i * 3 * kMaxC + c];
+        if (beta_x) beta_x[(size_t)i * kMaxC + c] = sol[(size_t)i * 3 * kMaxC + kMaxC + c];
+        if (beta_y) beta_y[(size_t)i * kMaxC + c] = sol[(size_t)i * 3 * kMaxC + 2 * kMaxC + c];
+      }
+      if (evaluations) evaluations[i] = (long long)R * (1 + (long long)p->n_outer * k * p->n_inner);
+    }
+  });
+}
+
+int lg_realized_contacts_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                               const double* q, const int* links, const double* object_points,
+                               double* realized_p, double* realized_n, int* realized_link,
+                               double* residuals) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || m < 0 || (m && (!k || !q || !links || !object_points)))
+      throw std::invalid_argument("lg_realized_contacts_batch: bad argument");
+    if (m == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    std::vector<int> tl((size_t)m * kMaxK, 0);
+    std::vector<double> op((size_t)m * kMaxK * 3, 0.0);
+    std::vector<long long> first(m);
+    long long off = 0;
+    for (int i = 0; i < m; ++i) {
+      if (k[i] < 1 || k[i] > kMaxK) throw std::invalid_argument("realize_grasp: 1..5 targets");
+      first[i] = off;
+      for (int c = 0; c < k[i]; ++c, ++off) {
+        if (links[off] < 0 || links[off] >= hand->n_links)
+          throw std::invalid_argument("solve_contact_ik: invalid target link");
+        tl[(size_t)i * kMaxK + c] = links[off];
+        for (int a = 0; a < 3; ++a) op[((size_t)i * kMaxK + c) * 3 + a] = object_points[3 * off + a];
+      }
+    }
+    Buf bk, bq, bl, bo, brp, brn, brl, brs;
+    int* d_k = dupload(bk, k, (size_t)m, s);
+    double* d_q = dupload(bq, q, (size_t)m * hand->dof, s);
+    int* d_l = dupload(bl, tl.data(), tl.size(), s);
+    double* d_o = dupload(bo, op.data(), op.size(), s);
+    double* d_rp = dalloc<double>(brp, op.size());
+    double* d_rn = dalloc<double>(brn, op.size());
+    int* d_rl = dalloc<int>(brl, tl.size());
+    double* d_rs = dalloc<double>(brs, tl.size());
+    lgd::k_realized<<<grid_for((long long)m * kMaxK, 64), 64, 0, s>>>(m, kMaxK, d_k, d_q, hand->dof, d_l,
+                                                                     d_o, d_rp, d_rn, d_rl, d_rs);
+    check_launch();
+    LAUNCH(ctx);
+    auto rp = ddownload(d_rp, op.size(), s);
+    auto rn = ddownload(d_rn, op.size(), s);
+    auto rl = ddownload(d_rl, tl.size(), s);
+    auto rs = ddownload(d_rs, tl.size(), s);
+    for (int i = 0; i < m; ++i)
+      for (int c = 0; c < k[i]; ++c) {
+        long long o = first[i] + c;
+        size_t t = (size_t)i * kMaxK + c;
+        for (int a = 0; a < 3; ++a) {
+          if (realized_p) realized_p[3 * o + a] = rp[3 * t + a];
+          if (realized_n) realized_n[3 * o + a] = rn[3 * t + a];
+        }
+        if (realized_link) realized_link[o] = rl[t];
+        if (residuals) residuals[o] = rs[t];
+      }
+  });
+}
+
+int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const double* q,
+                              const double* poses, const double* samples, int n, double margin,
+                              int cap, int* n_violations, int* link_a, int* link_b, double* depth,
+                              double* max_penetration, int* broad_pairs) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || m < 0 || cap < 0 || (m && (!q || !poses || !n_violations)))
+      throw std::invalid_argument("lg_collision_report_batch: bad argument");
+    if (margin < 0.0) throw std::invalid_argument("broad_phase: negative margin");
+    if (m == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    for (int p = 0; p < hand->n_parts; ++p)
+      if (hand->part_plane_off[p + 1] == hand->part_plane_off[p])
+        throw std::invalid_argument("object_penetration: part has no face planes");
+    std::vector<double> col((size_t)std::max(n, 1));
+    Buf sc[6];
+    for (int a = 0; a < 6; ++a) {
+      for (int i = 0; i < n; ++i) col[i] = samples[6 * i + a];
+      dupload(sc[a], col.data(), (size_t)n, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    DSamples S = make_samples(sc, n);
+    const int cp = std::max(cap, 1);
+    Buf bq, bp, bpl, bnv, ba, bb, bd, bm, bbp;
+    double* d_q = dupload(bq, q, (size_t)m * hand->dof, s);
+    double* d_p = dupload(bp, poses, 12 * (size_t)m, s);
+    int* d_pl = dupload(bpl, hand->part_link, (size_t)hand->n_parts, s);
+    int* d_nv = dalloc<int>(bnv, (size_t)m);
+    int* d_a = dalloc<int>(ba, (size_t)m * cp);
+    int* d_b = dalloc<int>(bb, (size_t)m * cp);
+    double* d_d = dalloc<double>(bd, (size_t)m * cp);
+    double* d_m = dalloc<double>(bm, (size_t)m);
+    int* d_bp = dalloc<int>(bbp, (size_t)m);
+    lgd::k_collision_report<<<grid_for(m, 32), 32, 0, s>>>(m, d_q, hand->dof, d_p, S, margin, d_pl, cp,
+                                                         d_nv, d_a, d_b, d_d, d_m, d_bp);
+    check_launch();
+    LAUNCH(ctx);
+    auto nv = ddownload(d_nv, (size_t)m, s);
+    std::copy(nv.begin(), nv.end(), n_violations);
+    if (link_a) {
+      auto a = ddownload(d_a, (size_t)m * cp, s);
+      std::copy(a.begin(), a.begin() + (size_t)m * cap, link_a);
+    }
+    if (link_b) {
+      auto b = ddownload(d_b, (size_t)m * cp, s);
+      std::copy(b.begin(), b.begin() + (size_t)m * cap, link_b);
+    }
+    if (depth) {
+      auto d = ddownload(d_d, (size_t)m * cp, s);
+      std::copy(d.begin(), d.begin() + (size_t)m * cap, depth);
+    }
+    if (max_penetration) {
+      auto mp = ddownload(d_m, (size_t)m, s);
+      std::copy(mp.begin(), mp.end(), max_penetration);
+    }
+    if (broad_pairs) {
+      auto bpv = ddownload(d_bp, (size_t)m, s);
+      std::copy(bpv.begin(), bpv.end(), broad_pairs);
     }
   });
 }
