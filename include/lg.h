@@ -369,11 +369,12 @@ int lg_realized_contacts_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, con
  * collision.hpp:57-65) for m configurations: violations deduplicated per
  * link pair in the reference's pair order (link_b = -1: the object; depth 0
  * for hand-hand), up to cap per configuration ([m][cap]); n_violations[i]
- * is the full count; max_penetration and the broad-phase pair count. */
+ * is the full count; max_penetration; pair_counts [m][3] = broad_pairs,
+ * narrow_gjk, narrow_halfplane. */
 int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const double* q,
                               const double* poses, const double* samples, int n, double margin,
                               int cap, int* n_violations, int* link_a, int* link_b, double* depth,
-                              double* max_penetration, int* broad_pairs);
+                              double* max_penetration, int* pair_counts);
 
 /* preprocess_object (pipeline.cpp:71-98): keep[i] = 1 when sample i survives. */
 int lg_preprocess(lg_ctx* ctx, const double* samples, int n,

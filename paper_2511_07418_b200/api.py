@@ -603,7 +603,7 @@ def collision_report_batch(ctx, hand, q, poses, samples, margin=0.002, cap=64):
     m = q.shape[0]
     poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(m, 12)
     s = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1, 6)
-    nv, bp = np.zeros(m, np.int32), np.zeros(m, np.int32)
+    nv, bp = np.zeros(m, np.int32), np.zeros((m, 3), np.int32)
     la, lb = np.zeros((m, cap), np.int32), np.zeros((m, cap), np.int32)
     dd, mp = np.zeros((m, cap)), np.zeros(m)
     check(lib().lg_collision_report_batch(ctx._h, C.byref(hand.desc), m, _dp(q), _dp(poses), _dp(s),
@@ -613,7 +613,8 @@ def collision_report_batch(ctx, hand, q, poses, samples, margin=0.002, cap=64):
     for i in range(m):
         n = min(nv[i], cap)
         out.append(dict(n_violations=int(nv[i]), max_penetration=float(mp[i]),
-                        broad_pairs=int(bp[i]),
+                        broad_pairs=int(bp[i, 0]), narrow_gjk=int(bp[i, 1]),
+                        narrow_halfplane=int(bp[i, 2]),
                         violations=list(zip(la[i, :n].tolist(), lb[i, :n].tolist(),
                                             dd[i, :n].tolist()))))
     return out

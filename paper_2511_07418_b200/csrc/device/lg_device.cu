@@ -2269,6 +2269,7 @@ __global__ void k_realized(int m, int kmax, const int* k, const double* q, int d
 __global__ void k_collision_report(int m, const double* q, int dof, const double* poses, DSamples S,
                                    double margin, const int* part_link, int cap, int* n_viol,
                                    int* va, int* vb, double* vd, double* max_pen, int* pairs) {
+  // pairs[3i..3i+2] = broad_pairs, narrow_gjk, narrow_halfplane (collision.hpp:57-65)
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   double qq[kMaxDof];
@@ -2286,7 +2287,7 @@ __global__ void k_collision_report(int m, const double* q, int dof, const double
   omn = v3(omn.x - margin, omn.y - margin, omn.z - margin);
   omx = v3(omx.x + margin, omx.y + margin, omx.z + margin);
   const int np = c_hand.n_parts;
-  int nv = 0, npairs = 0;
+  int nv = 0, npairs = 0, ngjk = 0, nhp = 0;
   double mp = 0.0;
   int* A = va + (size_t)i * cap;
   int* Bv = vb + (size_t)i * cap;
@@ -2321,11 +2322,13 @@ __global__ void k_collision_report(int m, const double* q, int dof, const double
       if (!ov) continue;
       ++npairs;
       if (la == lb || c_hand.parent[la] == lb || c_hand.parent[lb] == la) continue;
+      ++ngjk;
       if (gjk_distance(a, frames[la], b, frames[lb]) == 0.0) record(la < lb ? la : lb, la < lb ? lb : la, 0.0);
     }
     if (has_obj && amn.x <= omx.x && amn.y <= omx.y && amn.z <= omx.z && amx.x >= omn.x &&
         amx.y >= omn.y && amx.z >= omn.z) {
       ++npairs;
+      ++nhp;
       // object_penetration (collision.cpp:209-228)
       Xf inv = xf_inverse(frames[la]);
       const double* bb = c_hand.bounds + 6 * a;
@@ -2350,7 +2353,9 @@ __global__ void k_collision_report(int m, const double* q, int dof, const double
   }
   n_viol[i] = nv;
   max_pen[i] = mp;
-  pairs[i] = npairs;
+  pairs[3 * i] = npairs;
+  pairs[3 * i + 1] = ngjk;
+  pairs[3 * i + 2] = nhp;
 }
 
 }  // namespace lgd
@@ -2551,12 +2556,14 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
   return lgc::guard([&] {
     if (!ctx || !p || m < 0 || (m && (!dom_off || !dom_pos || !dom_nrm || !seeds)))
       throw std::invalid_argument("lg_optimize_contacts_batch: bad argument");
-    if (k < 1 || k > kMaxK) throw std::invalid_argument("optimize_contacts: 1..5 domains");
-    if (p->n_outer < 0 || p->n_inner < 1 || p->restarts < 1)
-      throw std::invalid_argument("optimize_contacts: bad iteration counts");
+    // contact_opt.cpp:49-59 (messages as the reference words them)
+    if (k < 1) throw std::invalid_argument("optimize_contacts: no domains");
+    if (k > kMaxK) throw std::invalid_argument("optimize_contacts: device limit is 5 domains");
     if (m == 0) return;
     for (long long t = 0; t < (long long)m * k; ++t)
       if (dom_off[t + 1] <= dom_off[t]) throw std::invalid_argument("optimize_contacts: empty domain");
+    if (p->sigma <= 0.0 || p->n_inner < 1 || p->n_outer < 0 || p->restarts < 1)
+      throw std::invalid_argument("optimize_contacts: bad parameters");
     use_ctx(ctx);
     cudaStream_t s = ctx->stream;
     const long long nel = dom_off[(size_t)m * k] - dom_off[0];
@@ -2566,7 +2573,8 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
     for (int i = 0; i < m; ++i) {
       aidx[i] = i;
       nst[i] = n_static ? n_static[i] : 0;
-      if (nst[i] < 0 || nst[i] > 1) throw std::invalid_argument("optimize_contacts: at most one static contact");
+      if (nst[i] < 0 || nst[i] > 1)
+        throw std::invalid_argument("optimize_contacts: device limit is one static contact");
     }
     std::vector<double> sp(3 * (size_t)m, 0.0), sn(3 * (size_t)m, 0.0);
     if (static_p) std::copy(static_p, static_p + 3 * (size_t)m, sp.begin());
@@ -2700,7 +2708,7 @@ int lg_realized_contacts_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, con
 int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const double* q,
                               const double* poses, const double* samples, int n, double margin,
                               int cap, int* n_violations, int* link_a, int* link_b, double* depth,
-                              double* max_penetration, int* broad_pairs) {
+                              double* max_penetration, int* pair_counts) {
   return lgc::guard([&] {
     if (!ctx || !hand || m < 0 || cap < 0 || (m && (!q || !poses || !n_violations)))
       throw std::invalid_argument("lg_collision_report_batch: bad argument");
@@ -2730,7 +2738,7 @@ int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, cons
     int* d_b = dalloc<int>(bb, (size_t)m * cp);
     double* d_d = dalloc<double>(bd, (size_t)m * cp);
     double* d_m = dalloc<double>(bm, (size_t)m);
-    int* d_bp = dalloc<int>(bbp, (size_t)m);
+    int* d_bp = dalloc<int>(bbp, 3 * (size_t)m);
     lgd::k_collision_report<<<grid_for(m, 32), 32, 0, s>>>(m, d_q, hand->dof, d_p, S, margin, d_pl, cp,
                                                          d_nv, d_a, d_b, d_d, d_m, d_bp);
     check_launch();
@@ -2753,9 +2761,9 @@ int lg_collision_report_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, cons
       auto mp = ddownload(d_m, (size_t)m, s);
       std::copy(mp.begin(), mp.end(), max_penetration);
     }
-    if (broad_pairs) {
-      auto bpv = ddownload(d_bp, (size_t)m, s);
-      std::copy(bpv.begin(), bpv.end(), broad_pairs);
+    if (pair_counts) {
+      auto bpv = ddownload(d_bp, 3 * (size_t)m, s);
+      std::copy(bpv.begin(), bpv.end(), pair_counts);
     }
   });
 }

@@ -1,0 +1,57 @@
+"""The drop-in, end to end: integration/graspgen_b200.cpp (the adapter a
+maintainer adds to the reference) linked into the reference's own binaries
+in place of run_batch / optimize_contacts / validate_grasp_collisions
+(oracle/Makefile `integration`):
+
+* the reference's CLI `graspgen synthesize` on the device writes the same
+  grasps.jsonl, byte for byte, as the unmodified reference CLI;
+* the reference's own Catch2 suites test_contact_opt and test_collision pass
+  with optimize_contacts / validate_grasp_collisions served by the device.
+"""
+import json
+import os
+import subprocess
+
+import pytest
+
+from conftest import ASSETS
+from oracle import ref_py as R
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(os.path.join(R.REF_DIR, "graspgen_b200")),
+                                 reason="oracle/_ref integration binaries not built")]
+
+
+def _run(exe, *args, timeout=900):
+    out = subprocess.run([os.path.join(R.REF_DIR, exe), *args], capture_output=True, text=True,
+                         timeout=timeout)
+    return out
+
+
+@pytest.mark.parametrize("suite", ["contact_opt", "collision"])
+def test_reference_catch2_suite_on_the_device(suite):
+    out = _run(f"test_{suite}_b200")
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "All tests passed" in out.stdout
+
+
+@pytest.mark.parametrize("hand,obj,cfg,batch", [
+    ("four_finger.urdf", "sphere_r030.obj", "four_finger.cfg", 256),
+    ("two_finger.urdf", "box_040.obj", "two_finger.cfg", 256),
+])
+def test_reference_cli_on_the_device_writes_the_same_dataset(tmp_path, hand, obj, cfg, batch):
+    args = ["synthesize", "--hand", os.path.join(ASSETS, "hands", hand),
+            "--object", os.path.join(ASSETS, "objects", obj),
+            "--config", os.path.join(ASSETS, "configs", cfg), "--seed", "0",
+            "--batch", str(batch), "--workers", "0"]
+    ref = _run("graspgen", *args, "--out", str(tmp_path / "ref"))
+    dev = _run("graspgen_b200", *args, "--out", str(tmp_path / "dev"))
+    assert ref.returncode in (0, 1) and dev.returncode == ref.returncode, dev.stderr[-2000:]
+    a = (tmp_path / "ref" / "grasps.jsonl").read_bytes()
+    b = (tmp_path / "dev" / "grasps.jsonl").read_bytes()
+    assert len(a) > 0 and a == b
+    pa = json.loads((tmp_path / "ref" / "profile.json").read_text())
+    pb = json.loads((tmp_path / "dev" / "profile.json").read_text())
+    for k in ("candidates", "placements_accepted", "contact_sets_balanced", "ik_finite",
+              "penetration_free", "ik_converged", "stable", "valid"):
+        assert pa[k] == pb[k], k
