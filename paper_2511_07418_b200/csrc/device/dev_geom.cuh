@@ -319,7 +319,8 @@ __device__ __forceinline__ void world_bounds(int p, const Xf& pose, V3* bmin, V3
 // ------------------------------------------------------------------- GJK
 // simplex_closest (collision.cpp:52-169); the degenerate-triangle recursion
 // is at most one level deep (n == 2 after keep({0,1})).
-__device__ bool simplex_closest(V3* s, int& n, V3& closest) {
+// Up to a triangle (no recursion: keeps the stack size static).
+__device__ __forceinline__ bool simplex_closest_le3(V3* s, int& n, V3& closest) {
   if (n == 1) {
     closest = s[0];
     return false;
@@ -396,6 +397,11 @@ __device__ bool simplex_closest(V3* s, int& n, V3& closest) {
     }
     return false;
   }
+  return false;
+}
+
+__device__ bool simplex_closest(V3* s, int& n, V3& closest) {
+  if (n <= 3) return simplex_closest_le3(s, n, closest);
   // tetrahedron
   const int faces[4][3] = {{0, 1, 2}, {0, 3, 1}, {0, 2, 3}, {1, 3, 2}};
   const int opposite[4] = {3, 2, 1, 0};
@@ -414,7 +420,7 @@ __device__ bool simplex_closest(V3* s, int& n, V3& closest) {
     V3 sb[4] = {a, b, c, a};
     int sn = 3;
     V3 cp;
-    simplex_closest(sb, sn, cp);
+    simplex_closest_le3(sb, sn, cp);
     double d2 = sqnorm(cp);
     if (d2 < best) {
       best = d2;
