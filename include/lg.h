@@ -458,6 +458,10 @@ int lg_validation_issues(const char* const* joint_names, int n_links,
  * against the host's std:: functions. */
 int lg_libm_eval(lg_ctx* ctx, int which, long long n, const double* x, const double* y,
                  double* out);
+/* With LG_CHECK_CANARY=1 in the environment every device buffer carries a
+ * guard band checked at release: the number of buffers found overwritten
+ * past their end so far (0 expected). */
+long long lg_debug_canary_violations(void);
 
 /* run_batch (pipeline.cpp:308-625): the whole forward pass on the device,
  * field build included.  raw_samples = sample_surface of the object. */

@@ -81,6 +81,7 @@ def lib():
         "lg_result_traces": (P(A.Trace), [vp]),
         "lg_result_destroy": (None, [vp]),
         "lg_libm_eval": (C.c_int, [vp, C.c_int, C.c_longlong, A.dp, A.dp, A.dp]),
+        "lg_debug_canary_violations": (C.c_longlong, []),
         "lg_query_domains_elements": (C.c_int, [vp, vp, A.ip, C.c_int, A.dp, C.c_int, A.dp,
                                                 C.c_double, P(vp)]),
         "lg_domains_group": (C.c_int, [vp, C.c_int, P(C.c_longlong), P(C.c_longlong)]),

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <filesystem>
 #include <climits>
@@ -112,29 +113,61 @@ void drop_cache(cudaStream_t s) {
   g_cache_bytes.erase(s);
 }
 
+// Canary mode (LG_CHECK_CANARY=1, read once): every device buffer gets a
+// 4 KiB guard band after the requested bytes, filled with 0xA5 at allocation
+// and verified at release; a kernel writing past the end of any buffer is
+// counted (lg_debug_canary_violations) and reported on stderr.  The device
+// substitute for compute-sanitizer's out-of-bounds-write check, which this
+// GPU pool does not allow.
+constexpr size_t kGuard = 4096;
+bool canary_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LG_CHECK_CANARY");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+std::atomic<long long> g_canary_bad{0};
+
 struct Buf {
   void* p = nullptr;
   size_t n = 0;
+  size_t req = 0;  // requested bytes (canary mode: the guard starts here)
   cudaStream_t s = nullptr;
   Buf() = default;
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
   ~Buf() { release(); }
+  void check_guard() {
+    if (!p || !canary_on()) return;
+    std::vector<unsigned char> g(n - req);
+    if (cudaStreamSynchronize(s) != cudaSuccess ||
+        cudaMemcpy(g.data(), (char*)p + req, g.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return;
+    for (unsigned char c : g)
+      if (c != 0xA5) {
+        ++g_canary_bad;
+        std::fprintf(stderr, "lg: canary: write past the end of a %zu-byte device buffer\n", req);
+        return;
+      }
+  }
   void release() {
+    check_guard();
     if (p) free_on(p, n, s);
     p = nullptr;
     n = 0;
   }
   void alloc(size_t bytes) {
-    if (bytes <= n && p) return;
-    if (p) free_on(p, n, s);
-    p = nullptr;
-    n = 0;
+    if (bytes <= n && p && !canary_on()) return;
+    if (p) release();
+    req = bytes;
     bytes = (bytes + 255) & ~(size_t)255;
     if (bytes == 0) bytes = 256;
+    if (canary_on()) bytes += kGuard;
     s = g_alloc_stream;
     p = cached_alloc(bytes, s);
     n = bytes;
+    if (canary_on()) CK(cudaMemsetAsync((char*)p + req, 0xA5, n - req, s));
   }
   template <typename T>
   T* as() const {
@@ -1861,6 +1894,8 @@ __global__ void k_libm_eval(int which, int n, const double* x, const double* y, 
   }
 }
 }  // namespace lgd
+
+long long lg_debug_canary_violations(void) { return g_canary_bad.load(); }
 
 int lg_libm_eval(lg_ctx* ctx, int which, long long n, const double* x, const double* y,
                  double* out) {

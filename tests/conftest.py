@@ -87,3 +87,15 @@ def mismatched_fields(a, b, names=None):
         if len(rows):
             out[n] = rows.tolist()
     return out
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Under LG_CHECK_CANARY=1 every device buffer is guard-banded; fail the
+    session when any kernel wrote past the end of one (test_canary.py)."""
+    if os.environ.get("LG_CHECK_CANARY") != "1":
+        return
+    import paper_2511_07418_b200 as lg
+    v = lg.lib().lg_debug_canary_violations()
+    print(f"\ncanary_violations={v}")
+    if v:
+        session.exitstatus = 1
