@@ -272,67 +272,98 @@ __device__ __forceinline__ WarpWs warp_ws(char* base, int k, int dof) {
   return w;
 }
 
-// Eigen LDLT factor + solve, warp-parallel; A (n x n, smem) destroyed,
-// x (smem) rhs in / solution out.
-__device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, int* tr,
+// Final position of each diagonal entry under Eigen's diagonal pivoting
+// (ldlt_inplace: step k swaps position k with the first position holding the
+// largest |A(i,i)|, i >= k).  Only the diagonal decides, and at step k its
+// entries i >= k are still the original ones (the left-looking update writes
+// column k only; the swaps move diagonal entries as a whole), so the pivot
+// order is fixed before the factorization.  Lane a < n holds v = A(a,a), not
+// NaN; returns a's final position.  Non-negative doubles order like their
+// bit patterns: the maximum is two 32-bit warp reductions and the first
+// position among its holders a third.
+__device__ __forceinline__ int pivot_positions(double v, int n, int lane) {
+  const unsigned long long bits =
+      lane < n ? (unsigned long long)__double_as_longlong(dabs(v)) : 0ull;
+  int pos = lane;
+  #pragma unroll 1
+  for (int k = 0; k + 1 < n; ++k) {
+    const bool act = lane < n && pos >= k;
+    const unsigned hi = __reduce_max_sync(kFull, act ? (unsigned)(bits >> 32) : 0u);
+    const bool t1 = act && (unsigned)(bits >> 32) == hi;
+    const unsigned lo = __reduce_max_sync(kFull, t1 ? (unsigned)bits : 0u);
+    const bool t2 = t1 && (unsigned)bits == lo;
+    const int big = (int)__reduce_min_sync(kFull, t2 ? (unsigned)pos : 0xffffffffu);
+    if (act && pos == k) pos = big;        // the entry at k moves to big
+    else if (t2 && pos == big) pos = k;    // the pivot moves to k
+  }
+  return pos;
+}
+
+// Eigen LDLT factor + solve, warp-parallel; A (n x n, smem, lower triangle
+// read and written) destroyed, x (smem) rhs in / solution out.  piv: pivot
+// during the factorization (A and x in their original order); otherwise A
+// and x are already symmetrically permuted to the pivot order (lane a's
+// entry at position pos) and the solution is scattered back through pos.
+__device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x, bool piv, int pos,
                                             double* tmp, int lane) {
-  (void)tr;
   // pidx: the transpositions applied so far to the index vector (lane i
   // holds entry i), so P^T b is a gather and P y a scatter at the end
   int pidx = lane;
   #pragma unroll 1
   for (int k = 0; k < n; ++k) {
-    // pivot = first index of max |A(i,i)|, i >= k.  Non-negative doubles
-    // order like their bit patterns, so the max is two 32-bit warp
-    // reductions (high word, then low word among the ties) and the first
-    // lane holding it; a NaN diagonal takes the comparison-based reduction.
-    const bool act = lane >= k && lane < n;
-    double v = act ? dabs(A[lane * ld + lane]) : -1.0;
-    int big;
-    if (!__any_sync(kFull, act && v != v)) {
-      unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-      unsigned hi = __reduce_max_sync(kFull, act ? (unsigned)(bits >> 32) : 0u);
-      bool tie = act && (unsigned)(bits >> 32) == hi;
-      unsigned lo = __reduce_max_sync(kFull, tie ? (unsigned)bits : 0u);
-      big = __ffs(__ballot_sync(kFull, tie && (unsigned)bits == lo)) - 1;
-    } else {
-      int idx = act ? lane : 0x7fff;
+    if (piv) {
+      // pivot = first index of max |A(i,i)|, i >= k.  Non-negative doubles
+      // order like their bit patterns, so the max is two 32-bit warp
+      // reductions (high word, then low word among the ties) and the first
+      // lane holding it; a NaN diagonal takes the comparison-based reduction.
+      const bool act = lane >= k && lane < n;
+      double v = act ? dabs(A[lane * ld + lane]) : -1.0;
+      int big;
+      if (!__any_sync(kFull, act && v != v)) {
+        unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+        unsigned hi = __reduce_max_sync(kFull, act ? (unsigned)(bits >> 32) : 0u);
+        bool tie = act && (unsigned)(bits >> 32) == hi;
+        unsigned lo = __reduce_max_sync(kFull, tie ? (unsigned)bits : 0u);
+        big = __ffs(__ballot_sync(kFull, tie && (unsigned)bits == lo)) - 1;
+      } else {
+        int idx = act ? lane : 0x7fff;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(kFull, v, o);
-        int oi = __shfl_xor_sync(kFull, idx, o);
-        if (ov > v || (ov == v && oi < idx)) {
-          v = ov;
-          idx = oi;
+        for (int o = 16; o > 0; o >>= 1) {
+          double ov = __shfl_xor_sync(kFull, v, o);
+          int oi = __shfl_xor_sync(kFull, idx, o);
+          if (ov > v || (ov == v && oi < idx)) {
+            v = ov;
+            idx = oi;
+          }
         }
+        big = idx;
       }
-      big = idx;
-    }
-    if (k != big) {
-      const int pk = __shfl_sync(kFull, pidx, k), pb = __shfl_sync(kFull, pidx, big);
-      if (lane == k) pidx = pb;
-      else if (lane == big) pidx = pk;
-      if (lane < k) {
-        double t = A[k * ld + lane];
-        A[k * ld + lane] = A[big * ld + lane];
-        A[big * ld + lane] = t;
+      if (k != big) {
+        const int pk = __shfl_sync(kFull, pidx, k), pb = __shfl_sync(kFull, pidx, big);
+        if (lane == k) pidx = pb;
+        else if (lane == big) pidx = pk;
+        if (lane < k) {
+          double t = A[k * ld + lane];
+          A[k * ld + lane] = A[big * ld + lane];
+          A[big * ld + lane] = t;
+        }
+        if (lane > big && lane < n) {
+          double t = A[lane * ld + k];
+          A[lane * ld + k] = A[lane * ld + big];
+          A[lane * ld + big] = t;
+        }
+        if (lane == 0) {
+          double t = A[k * ld + k];
+          A[k * ld + k] = A[big * ld + big];
+          A[big * ld + big] = t;
+        }
+        if (lane > k && lane < big) {
+          double u = A[lane * ld + k];
+          A[lane * ld + k] = A[big * ld + lane];
+          A[big * ld + lane] = u;
+        }
+        __syncwarp();
       }
-      if (lane > big && lane < n) {
-        double t = A[lane * ld + k];
-        A[lane * ld + k] = A[lane * ld + big];
-        A[lane * ld + big] = t;
-      }
-      if (lane == 0) {
-        double t = A[k * ld + k];
-        A[k * ld + k] = A[big * ld + big];
-        A[big * ld + big] = t;
-      }
-      if (lane > k && lane < big) {
-        double u = A[lane * ld + k];
-        A[lane * ld + k] = A[big * ld + lane];
-        A[big * ld + lane] = u;
-      }
-      __syncwarp();
     }
     if (k > 0) {
       // temp_j = D_j * A(k, j), j < k, broadcast through shared memory
@@ -351,7 +382,7 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     if (dabs(akk) > 0.0 && lane > k && lane < n) A[lane * ld + k] /= akk;
     __syncwarp();
   }
-  double xi = lane < n ? x[pidx] : 0.0;  // P^T b (the forward transpositions)
+  double xi = lane < n ? x[pidx] : 0.0;  // P^T b (the forward transpositions; identity if !piv)
   __syncwarp();
   double s = 0.0;
   #pragma unroll 1
@@ -372,7 +403,12 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
     if (lane == j) xi = xj;
     if (lane < j) s = s + A[j * ld + lane] * xj;
   }
-  if (lane < n) x[pidx] = xi;  // P y (the transpositions in reverse order)
+  if (piv) {
+    if (lane < n) x[pidx] = xi;  // P y (the transpositions in reverse order)
+  } else {
+    const double y = __shfl_sync(kFull, xi, pos & 31);
+    if (lane < n) x[lane] = y;
+  }
   __syncwarp();
 }
 
@@ -435,10 +471,10 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     }
     used = __reduce_or_sync(kFull, (unsigned)used);  // dof <= 32: one word
     __syncwarp();
-    // J^T J (upper triangle, mirrored) and J^T r
-    // J^T J upper-triangle entries e < ne and J^T r entries ne <= e < ne +
-    // dof share one branch-free loop (same row-ordered dot product: column
-    // a of J against column b of J, or against r)
+    // J^T J entries (a <= b) e < ne and J^T r entries ne <= e < ne + dof
+    // share one branch-free loop (same row-ordered dot product: column a of
+    // J against column b of J, or against r).  Off-diagonal entries are
+    // staged in the upper triangle, the diagonal in qt.
     const int ne = dof * (dof + 1) / 2;
     for (int e = lane; e < ne + dof; e += 32) {
       const bool jj = e < ne;
@@ -448,23 +484,38 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
       double s = 0.0;
       #pragma unroll 4
       for (int rr = 0; rr < rows; ++rr) s = s + ws.J[rr * dof + a] * o2[rr * st2];
-      if (jj) {
-        ws.A[a * ld + b] = s;
-        ws.A[b * ld + a] = s;
-      } else {
-        ws.x[a] = s;
-      }
+      if (!jj) ws.x[a] = s;
+      else if (a == b) ws.qt[a] = s;
+      else ws.A[a * ld + b] = s;
     }
     __syncwarp();
     double tr = 0.0;
     if (lane == 0)
       #pragma unroll 4
-      for (int a = 0; a < dof; ++a) tr = tr + ws.A[a * ld + a];
+      for (int a = 0; a < dof; ++a) tr = tr + ws.qt[a];
     tr = __shfl_sync(kFull, tr, 0);
     double lambda = dmax(P.damping_min, P.damping_scale * tr / (double)(dof > 1 ? dof : 1));
-    if (lane < dof) ws.A[lane * ld + lane] += lambda;
+    // damped diagonal; the pivot order it implies is applied to A and J^T r
+    // as they move to the lower triangle (a NaN diagonal keeps the original
+    // order and pivots during the factorization)
+    const double dv = lane < dof ? ws.qt[lane] + lambda : 0.0;
+    const bool piv = __any_sync(kFull, lane < dof && dv != dv);
+    const int pos = piv ? lane : pivot_positions(dv, dof, lane);
+    const double bv = lane < dof ? ws.x[lane] : 0.0;
+    if (lane < dof) ws.tr[lane] = pos;
     __syncwarp();
-    wldlt_solve(dof, ld, ws.A, ws.x, ws.tr, ws.qt, lane);
+    if (lane < dof) {
+      ws.A[pos * ld + pos] = dv;
+      ws.x[pos] = bv;
+    }
+    for (int e = lane; e < ne; e += 32) {
+      const int a = ab[e] & 0xff, b = ab[e] >> 8;
+      if (a == b) continue;
+      const int pa = ws.tr[a], pb = ws.tr[b];
+      ws.A[(pa > pb ? pa : pb) * ld + (pa > pb ? pb : pa)] = ws.A[a * ld + b];
+    }
+    __syncwarp();
+    wldlt_solve(dof, ld, ws.A, ws.x, piv, pos, ws.qt, lane);
     bool bad = lane < dof && !is_finite(ws.x[lane]);
     if (__any_sync(kFull, bad)) {
       finite = false;
