@@ -200,6 +200,7 @@ typedef struct lg_profile {
   long long realize_calls, collision_calls;
   double realize_seconds, contact_opt_seconds;
   long long index_from_cache; /* RunResult.index.from_cache */
+  long long index_codes;      /* codes (= representatives) over all boxes */
 } lg_profile;
 
 /* Per-candidate record of every stage decision, used by the stage parity

@@ -261,6 +261,20 @@ RunResult run_batch(const RunConfig& cfg) {
   out.index.patches = static_cast<std::size_t>(prof.patches);
   out.index.boxes = static_cast<std::size_t>(prof.boxes);
   out.index.from_cache = prof.index_from_cache != 0;
+  // ContactFieldIndex::total_memory_bytes (contact_field.cpp:336-353) of the
+  // same index: every patch in the index holds >= 1 box, and each BVH is a
+  // binary tree with one leaf per item (2 b - 1 nodes per patch, 2 P - 1 on
+  // top), so the count follows from P, B and the code count
+  if (prof.patches > 0) {
+    const std::size_t P = static_cast<std::size_t>(prof.patches);
+    const std::size_t B = static_cast<std::size_t>(prof.boxes);
+    const std::size_t R = static_cast<std::size_t>(prof.index_codes);
+    out.index.memory_bytes = sizeof(ContactFieldIndex) +
+                             static_cast<std::size_t>(cfg.codebook_size) * sizeof(Vec3) +
+                             (2 * P - 1) * sizeof(BvhNode) + P * sizeof(PatchIndex) +
+                             B * sizeof(IndexBox) + R * (sizeof(std::uint16_t) + sizeof(IndexRep)) +
+                             (2 * B - P) * sizeof(BvhNode);
+  }
   sp.total = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   sp.grasps_per_second = sp.total > 0.0 ? sp.valid / sp.total : 0.0;
   return out;

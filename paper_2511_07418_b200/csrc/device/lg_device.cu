@@ -593,6 +593,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   const DevPatches& DP = field->from_cache ? cache_patches : field->patches;
   out.profile.patches = F.P;
   out.profile.boxes = F.B;
+  out.profile.index_codes = field->n_codes;
   out.profile.field_vectors = field->n_vectors;
   out.profile.object_samples = n_raw;
 

@@ -106,7 +106,7 @@ class Profile(C.Structure):
         "ik_iterations", "fk_evals", "wrench_evals", "wrench_grads", "proj_evals",
         "realize_calls", "collision_calls")] + [
         ("realize_seconds", C.c_double), ("contact_opt_seconds", C.c_double),
-        ("index_from_cache", C.c_longlong)]
+        ("index_from_cache", C.c_longlong), ("index_codes", C.c_longlong)]
 
 
 class GraspCheck(C.Structure):

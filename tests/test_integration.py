@@ -55,3 +55,11 @@ def test_reference_cli_on_the_device_writes_the_same_dataset(tmp_path, hand, obj
     for k in ("candidates", "placements_accepted", "contact_sets_balanced", "ik_finite",
               "penetration_free", "ik_converged", "stable", "valid"):
         assert pa[k] == pb[k], k
+    # RunResult.loads and RunResult.index (patches, boxes, memory_bytes, cache)
+    assert (tmp_path / "ref" / "load_report.json").read_bytes() == \
+        (tmp_path / "dev" / "load_report.json").read_bytes()
+
+    def stage(out, tag):
+        return [ln for ln in out.stdout.splitlines() if ln.startswith("[stage] " + tag)]
+    for tag in ("load", "field"):
+        assert stage(ref, tag) and stage(ref, tag) == stage(dev, tag), tag
