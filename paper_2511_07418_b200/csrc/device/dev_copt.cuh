@@ -386,52 +386,88 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
     }
     unsigned long long ev = (unsigned long long)(ne - cbest * kChunk < kChunk ? ne - cbest * kChunk : kChunk);
     // pass 2: every other box whose lower bound does not exceed the best
-    const double thr = bd * (1.0 + 0x1p-40);
+    double thr = bd * (1.0 + 0x1p-40);
     double dl = bd;
     int ol = bi;
-    for (int tb = 0; tb < nsu; tb += 32) {
-      const int t = tb + lane;
-      const bool ns = t < nsu && (nsu == 1 || !(box_lb(D.sb, D.sstride, s0 + t, cp) > thr));
-      unsigned ms = __ballot_sync(kFull, ns);
-      while (ms) {
-        const int ss = tb + __ffs(ms) - 1;
-        ms &= ms - 1;
-        const int c2 = ss * 32 + lane;
-        const bool nc = c2 < nch && c2 != cbest && !(box_lb(D.cb, D.cstride, c0 + c2, cp) > thr);
-        unsigned mc = __ballot_sync(kFull, nc);
-        ev += (unsigned long long)__popc(mc) * kChunk;
-        // up to four needed chunks at a time: their loads are independent
-        // (the large domains stream from L2/HBM), the comparisons follow
-        while (mc) {
-          int jj[4];
+    // the needed chunks of super-chunk ss, up to four at a time: their loads
+    // are independent (the large domains stream from L2/HBM), the
+    // comparisons follow
+    auto eval_super = [&](int ss) {
+      const int c2 = ss * 32 + lane;
+      const bool nc = c2 < nch && c2 != cbest && !(box_lb(D.cb, D.cstride, c0 + c2, cp) > thr);
+      unsigned mc = __ballot_sync(kFull, nc);
+      ev += (unsigned long long)__popc(mc) * kChunk;
+      while (mc) {
+        int jj[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            jj[u] = -1;
-            if (mc) {
-              jj[u] = (ss * 32 + __ffs(mc) - 1) * kChunk + lane;
-              mc &= mc - 1;
-            }
+        for (int u = 0; u < 4; ++u) {
+          jj[u] = -1;
+          if (mc) {
+            jj[u] = (ss * 32 + __ffs(mc) - 1) * kChunk + lane;
+            mc &= mc - 1;
           }
-          double px[4], py[4], pz[4];
-          int po[4];
+        }
+        double px[4], py[4], pz[4];
+        int po[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const bool ok = jj[u] >= 0 && jj[u] < ne;
-            const int j = ok ? jj[u] : 0;
-            px[u] = ok ? SX[j] : 0.0;
-            py[u] = ok ? SY[j] : 0.0;
-            pz[u] = ok ? SZ[j] : 0.0;
-            po[u] = ok ? SI[j] : -1;
-          }
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = jj[u] >= 0 && jj[u] < ne;
+          const int j = ok ? jj[u] : 0;
+          px[u] = ok ? SX[j] : 0.0;
+          py[u] = ok ? SY[j] : 0.0;
+          pz[u] = ok ? SZ[j] : 0.0;
+          po[u] = ok ? SI[j] : -1;
+        }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (po[u] < 0) continue;
-            const double d = sqnorm(sub(v3(px[u], py[u], pz[u]), cp));
-            if (d < dl || (d == dl && po[u] < ol)) {
-              dl = d;
-              ol = po[u];
-            }
+        for (int u = 0; u < 4; ++u) {
+          if (po[u] < 0) continue;
+          const double d = sqnorm(sub(v3(px[u], py[u], pz[u]), cp));
+          if (d < dl || (d == dl && po[u] < ol)) {
+            dl = d;
+            ol = po[u];
           }
+        }
+      }
+    };
+    if (nsu <= 128) {
+      // best first: super-chunks in ascending lower-bound order, the
+      // threshold tightened to the best distance after each one, until the
+      // smallest remaining bound exceeds it
+      double sl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = lane + 32 * u;
+        sl[u] = t < nsu ? (nsu == 1 ? 0.0 : box_lb(D.sb, D.sstride, s0 + t, cp)) : kInf;
+      }
+      for (;;) {
+        double v = sl[0];
+        int tt = lane;
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (sl[u] < v) {
+            v = sl[u];
+            tt = lane + 32 * u;
+          }
+        warp_lexmin(v, tt);
+        if (!(v <= thr)) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (lane + 32 * u == tt) sl[u] = kInf;
+        eval_super(tt);
+        double bd2 = dl;
+        int bi2 = ol;
+        warp_lexmin(bd2, bi2);
+        thr = bd2 * (1.0 + 0x1p-40);
+      }
+    } else {
+      for (int tb = 0; tb < nsu; tb += 32) {
+        const int t = tb + lane;
+        const bool ns = t < nsu && !(box_lb(D.sb, D.sstride, s0 + t, cp) > thr);
+        unsigned ms = __ballot_sync(kFull, ns);
+        while (ms) {
+          const int ss = tb + __ffs(ms) - 1;
+          ms &= ms - 1;
+          eval_super(ss);
         }
       }
     }

@@ -24,6 +24,7 @@ namespace lgd {
 // max, both order independent.  With clean_only (the pipeline consumes only
 // clean()), work stops at the first violation.
 constexpr int kCollWarps = 4;
+constexpr int kCollGridMin = 20000;
 struct CollWarpSmem {
   double q[kMaxDof];
   double fr[kMaxLinks * kFS];
@@ -88,8 +89,69 @@ k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, c
   // prefilter (widened 1e-6), then the exact local test and depth
   double mx = 0.0;
   const int nobj = W.nobj;
-  if (nobj > 0) {
-    const Xf x = load_xf(pose + 12 * i);
+  const Xf x = load_xf(pose + 12 * i);
+  // Through the raw-sample grid: part by part, only the cells of the
+  // object-frame box around the preimage of the part's widened world box.
+  // For w = R p + t with R orthonormal, |p - c_o| <= |R|^T h componentwise,
+  // so every sample whose world point passes the world-box test lies in it
+  // (rounding ~1e-16 relative, covered by the grid's w 2^-20 widening).  A
+  // pose whose R is not orthonormal to 1e-9 takes the full sweep, and so do
+  // objects with few samples (a part's rows hold too few samples to keep
+  // the lanes busy: the sweep, one world point per sample, is faster).
+  bool use_grid = C.grid.ok && nobj > 0 && C.raw.n >= kCollGridMin;
+  if (use_grid) {
+    const M3 RtR = mul(transpose(x.R), x.R);
+    for (int a = 0; a < 9; ++a)
+      use_grid = use_grid && dabs(RtR.m[a] - ((a % 4) == 0 ? 1.0 : 0.0)) <= 1e-9;
+  }
+  if (use_grid) {
+    const DGrid& g = C.grid;
+    for (int o = 0; o < nobj; ++o) {
+      if (clean_only && *(volatile int*)&W.viol) break;
+      const int pa = W.obj[o];
+      const double* bx = W.box + 6 * pa;
+      const double cw[3] = {0.5 * (bx[0] + bx[3]) - x.t.x, 0.5 * (bx[1] + bx[4]) - x.t.y,
+                            0.5 * (bx[2] + bx[5]) - x.t.z};
+      const double hw[3] = {0.5 * (bx[3] - bx[0]) + 1e-6, 0.5 * (bx[4] - bx[1]) + 1e-6,
+                            0.5 * (bx[5] - bx[2]) + 1e-6};
+      int c0[3], c1[3];
+      for (int a = 0; a < 3; ++a) {
+        double co = 0.0, ho = 0.0;
+        for (int b = 0; b < 3; ++b) {
+          co += x.R.m[3 * b + a] * cw[b];
+          ho += dabs(x.R.m[3 * b + a]) * hw[b];
+        }
+        const double m = g.w * 0x1p-20 + (dabs(co) + ho) * 0x1p-40;
+        c0[a] = grid_cell(g, a, co - ho - m);
+        c1[a] = grid_cell(g, a, co + ho + m);
+      }
+      const Xf li = ld_xf(W.inv + kFS * C.part_link[pa]);
+      const double* b = c_hand.bounds + 6 * pa;
+      bool hit = false;
+      for (int z = c0[2]; z <= c1[2]; ++z)
+        for (int y = c0[1]; y <= c1[1]; ++y) {
+          const int row = (z * g.dim[1] + y) * g.dim[0];
+          const int t1 = g.start[row + c1[0] + 1];
+          for (int t = g.start[row + c0[0]] + lane; t < t1; t += 32) {
+            if (clean_only && *(volatile int*)&W.viol) break;
+            const V3 w = xf_apply(x, v3(g.x[0][t], g.x[1][t], g.x[2][t]));
+            if (!(w.x >= bx[0] - 1e-6 && w.y >= bx[1] - 1e-6 && w.z >= bx[2] - 1e-6 &&
+                  w.x <= bx[3] + 1e-6 && w.y <= bx[4] + 1e-6 && w.z <= bx[5] + 1e-6))
+              continue;
+            const V3 local = xf_apply(li, w);
+            if (!(local.x >= b[0] - 1e-9 && local.y >= b[1] - 1e-9 && local.z >= b[2] - 1e-9 &&
+                  local.x <= b[3] + 1e-9 && local.y <= b[4] + 1e-9 && local.z <= b[5] + 1e-9))
+              continue;
+            const double depth = part_interior_depth(pa, local);
+            if (depth > C.margin) {
+              hit = true;
+              mx = dmax(mx, depth);
+            }
+          }
+        }
+      if (hit) atomicOr(&W.viol, 1);
+    }
+  } else if (nobj > 0) {
     for (int j = lane; j < C.raw.n; j += 32) {
       if (clean_only && *(volatile int*)&W.viol) break;
       V3 w = xf_apply(x, C.raw.p(j));

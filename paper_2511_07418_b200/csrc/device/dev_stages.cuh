@@ -62,6 +62,79 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return r;
 }
 
+// --------------------------------------------------- object sample grid
+// Uniform grid over object-frame samples: cell width w from origin lo, the
+// sample ids sorted by cell (ascending inside a cell), per-cell offsets and
+// the samples in cell order (SoA).  It only decides which samples a test
+// visits: a region test (an axis box in the object frame) visits every cell
+// the box touches, widened by w 2^-20, far more than the rounding of any
+// coordinate involved, so no sample that can pass is skipped; the test on a
+// visited sample is the reference's, unchanged.  Cells along x are
+// contiguous in the order, so each (y, z) row of a box is one sample range.
+struct DGrid {
+  int ok;
+  double lo[3], w;
+  int dim[3];
+  const int* start;    // [cells + 1]
+  const int* id;       // [n] sample id in cell order
+  const double* x[6];  // samples in cell order (position, normal)
+};
+
+__device__ __forceinline__ int grid_cell(const DGrid& g, int a, double v) {
+  const double f = floor((v - g.lo[a]) / g.w);
+  if (!(f > 0.0)) return 0;  // below the grid, or NaN
+  return f >= (double)(g.dim[a] - 1) ? g.dim[a] - 1 : (int)f;
+}
+
+__global__ void k_grid_keys(DSamples s, DGrid g, unsigned* keys, int* vals, int* cnt) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < s.n; j += gridDim.x * blockDim.x) {
+    const V3 p = s.p(j);
+    const unsigned c = (unsigned)((grid_cell(g, 2, p.z) * g.dim[1] + grid_cell(g, 1, p.y)) * g.dim[0] +
+                                  grid_cell(g, 0, p.x));
+    keys[j] = c;
+    vals[j] = j;
+    atomicAdd(cnt + c, 1);
+  }
+}
+
+__global__ void k_grid_gather(DSamples s, const int* id, DGrid g) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < s.n; t += gridDim.x * blockDim.x) {
+    const int j = id[t];
+    for (int a = 0; a < 6; ++a) const_cast<double*>(g.x[a])[t] = s.x[a][j];
+  }
+}
+
+// preprocess_object (pipeline.cpp:71-98) through the grid: the j loop visits
+// the cells of the probe cube [c - h, c + h] only (any j outside it fails the
+// reference's |d| > h test); blocked is an existential, so the visit order
+// does not matter.
+__global__ void k_preprocess_grid(DSamples s, DGrid g, double h, double d, uint8_t* keep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n) return;
+  const V3 ni = s.nrm(i);
+  const V3 c = axpy(s.p(i), d, ni);
+  const double m = g.w * 0x1p-20;
+  const int x0 = grid_cell(g, 0, c.x - h - m), x1 = grid_cell(g, 0, c.x + h + m);
+  const int y0 = grid_cell(g, 1, c.y - h - m), y1 = grid_cell(g, 1, c.y + h + m);
+  const int z0 = grid_cell(g, 2, c.z - h - m), z1 = grid_cell(g, 2, c.z + h + m);
+  bool blocked = false;
+  for (int z = z0; z <= z1 && !blocked; ++z)
+    for (int y = y0; y <= y1 && !blocked; ++y) {
+      const int row = (z * g.dim[1] + y) * g.dim[0];
+      const int t1 = g.start[row + x1 + 1];
+      for (int t = g.start[row + x0]; t < t1; ++t) {
+        if (g.id[t] == i) continue;
+        const V3 dd = sub(v3(g.x[0][t], g.x[1][t], g.x[2][t]), c);
+        if (dabs(dd.x) > h || dabs(dd.y) > h || dabs(dd.z) > h) continue;
+        if (dot(v3(g.x[3][t], g.x[4][t], g.x[5][t]), ni) < 0.0) {
+          blocked = true;
+          break;
+        }
+      }
+    }
+  keep[i] = blocked ? 0 : 1;
+}
+
 // -------------------------------------------------------- preprocess_object
 // pipeline.cpp:71-98: sample i is dropped when some j != i lies inside the
 // axis cube of half width h around p_i + d n_i and n_j . n_i < 0.  The
@@ -571,6 +644,7 @@ struct CollCfg {
   double margin;
   DSamples raw;
   const int* part_link;
+  DGrid grid;  // over raw (grid.ok == 0: sweep every sample)
 };
 
 // ------------------------------------------------------------ postprocess

@@ -522,6 +522,83 @@ DSamples make_samples(Buf* cols, int n) {
   return d;
 }
 
+// Object sample grid (dev_stages.cuh DGrid) over the n samples S, whose host
+// copy `host` is [n][6].  Cell width w (doubled until the grid has at most
+// kGridMaxCells cells); ok = 0 (callers sweep every sample) when a sample
+// coordinate is not finite.
+struct GridBufs {
+  Buf cnt, start, keys, keys2, vals, id, cols;
+};
+constexpr long long kGridMaxCells = 1ll << 22;
+DGrid build_grid(lg_ctx* ctx, const DSamples& S, const double* host, int n, double w, GridBufs& gb,
+                 cudaStream_t s) {
+  DGrid g{};
+  g.ok = 0;
+  if (n <= 0 || !(w > 0.0) || !std::isfinite(w)) return g;
+  double lo[3] = {kInf, kInf, kInf}, hi[3] = {-kInf, -kInf, -kInf};
+  for (int i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const double v = host[6 * i + a];
+      if (!std::isfinite(v)) return g;
+      lo[a] = std::min(lo[a], v);
+      hi[a] = std::max(hi[a], v);
+    }
+  long long cells = 0;
+  for (;;) {
+    cells = 1;
+    for (int a = 0; a < 3; ++a) {
+      const double d = std::floor((hi[a] - lo[a]) / w) + 1.0;
+      g.dim[a] = d > 2e6 ? 2000000 : (int)d;
+      cells *= g.dim[a];
+    }
+    if (cells <= kGridMaxCells) break;
+    w *= 2.0;
+  }
+  for (int a = 0; a < 3; ++a) g.lo[a] = lo[a];
+  g.w = w;
+  int* cnt = dalloc<int>(gb.cnt, (size_t)cells + 1);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)cells + 1), s));
+  unsigned* keys = dalloc<unsigned>(gb.keys, (size_t)n);
+  unsigned* keys2 = dalloc<unsigned>(gb.keys2, (size_t)n);
+  int* vals = dalloc<int>(gb.vals, (size_t)n);
+  int* id = dalloc<int>(gb.id, (size_t)n);
+  int* start = dalloc<int>(gb.start, (size_t)cells + 1);
+  k_grid_keys<<<grid_for(n, 256), 256, 0, s>>>(S, g, keys, vals, cnt);
+  LAUNCH(ctx);
+  check_launch();
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, start, (int)cells + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(ctx->tmp(tb), tb, cnt, start, (int)cells + 1, s));
+  LAUNCH(ctx);
+  int bits = 1;
+  while (bits < 32 && (1ll << bits) < cells) ++bits;
+  tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, vals, id, n, 0, bits, s));
+  CK(cub::DeviceRadixSort::SortPairs(ctx->tmp(tb), tb, keys, keys2, vals, id, n, 0, bits, s));
+  LAUNCH(ctx);
+  double* cols = dalloc<double>(gb.cols, 6 * (size_t)n);
+  for (int a = 0; a < 6; ++a) g.x[a] = cols + (size_t)a * n;
+  g.start = start;
+  g.id = id;
+  k_grid_gather<<<grid_for(n, 256), 256, 0, s>>>(S, id, g);
+  LAUNCH(ctx);
+  check_launch();
+  g.ok = 1;
+  return g;
+}
+
+// preprocess_object on the device: through the sample grid (cells of half
+// the probe width) when it exists, else the all-pairs sweep.
+void preprocess_device(lg_ctx* ctx, const DSamples& S, const DGrid& g, double h, double d,
+                       uint8_t* keep, cudaStream_t s) {
+  if (g.ok)
+    k_preprocess_grid<<<grid_for(S.n, 128), 128, 0, s>>>(S, g, h, d, keep);
+  else
+    k_preprocess<<<grid_for(S.n, 256), 256, 0, s>>>(S, h, d, keep);
+  LAUNCH(ctx);
+  check_launch();
+}
+
 // place_object for candidates [c0, c0 + m) only (lg_place_batch): run_batch's
 // stage-1 placement, then return the records.
 struct PlaceOnly {
@@ -621,9 +698,10 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   uint8_t* d_keep = dalloc<uint8_t>(keepb, (size_t)n_raw);
   if (cfg.probe_half_width <= 0.0 || cfg.probe_depth_threshold < 0.0)
     throw std::invalid_argument("preprocess_object: bad probe dimensions");
-  k_preprocess<<<grid_for(n_raw, 256), 256, 0, s>>>(RS, cfg.probe_half_width, cfg.probe_depth_threshold, d_keep);
-  LAUNCH(ctx);
-  check_launch();
+  // raw-sample grid: preprocess here, the collision sweeps later
+  GridBufs rgrid_b;
+  const DGrid RG = build_grid(ctx, RS, raw, n_raw, 0.5 * cfg.probe_half_width, rgrid_b, s);
+  preprocess_device(ctx, RS, RG, cfg.probe_half_width, cfg.probe_depth_threshold, d_keep, s);
   auto keep = ddownload(d_keep, (size_t)n_raw, s);
   std::vector<int> kept;
   for (int i = 0; i < n_raw; ++i)
@@ -735,6 +813,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   cc.margin = cfg.penetration_margin;
   cc.raw = RS;
   cc.part_link = ctx->h_part_link.as<int>();
+  cc.grid = RG;
 
   mark("candidate_state");
   for (int pass = 0; pass < cfg.passes && Bl > 0; ++pass) {
@@ -1613,10 +1692,12 @@ int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const doubl
       k_obj_aabb<<<m, 256, 0, s>>>(m, S, d_p, d_a, d_b);
       check_launch();
     }
+    GridBufs gb;
     CollCfg cc;
     cc.margin = margin;
     cc.raw = S;
     cc.part_link = ctx->h_part_link.as<int>();
+    cc.grid = build_grid(ctx, S, samples, n, 0.005, gb, s);
     coll_kernel()<<<(m + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(m, cc, d_i, nullptr, d_q,
                                                                              d_p, d_b, 0, d_c, d_m);
     check_launch();
@@ -1871,8 +1952,10 @@ int lg_preprocess(lg_ctx* ctx, const double* samples, int n, double h, double d,
       CK(cudaStreamSynchronize(s));
     }
     uint8_t* d_keep = dalloc<uint8_t>(bk, (size_t)n);
-    k_preprocess<<<grid_for(n, 256), 256, 0, s>>>(make_samples(sc, n), h, d, d_keep);
-    check_launch();
+    const DSamples S = make_samples(sc, n);
+    GridBufs gb;
+    const DGrid g = build_grid(ctx, S, samples, n, 0.5 * h, gb, s);
+    preprocess_device(ctx, S, g, h, d, d_keep, s);
     CK(cudaMemcpyAsync(keep, d_keep, n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   });
