@@ -204,3 +204,35 @@ def test_collision_report_matches_reference(setup, ctx):
         assert dev[i]["broad_pairs"] == ref["broad_pairs"]
         dirty += ref["n_violations"] > 0
     assert dirty > 0
+
+
+def test_collision_batch_grid_path_matches_reference(ctx):
+    """lg_collision_batch on >= 20k object samples (the object-sample grid
+    path of k_collision3) == validate_grasp_collisions' clean() and
+    max_penetration, on placements of the Allegro-class hand around a dense
+    icosphere and random joint values (many of them penetrating)."""
+    import paper_2511_07418_b200 as lg
+    inp = R.RefInputs(config=os.path.join(ASSETS, "configs", "allegro.cfg"),
+                      extra="samples_per_cm2 = 250\nfield_configs = 64\n",
+                      hand=os.path.join(ASSETS, "hands", "allegro_like.urdf"),
+                      object=os.path.join(ASSETS, "objects", "icosphere_r030_s6.obj"),
+                      batch=24, workers=8)
+    assert len(inp.raw) >= 20000
+    H = types.SimpleNamespace(desc=inp.hand_desc, dof=inp.hand_desc.dof)
+    Pt = types.SimpleNamespace(desc=inp.patches_desc)
+    pl = lg.api.place_batch(ctx, H, Pt, inp.raw, inp.params, 0, 24)
+    d = inp.hand_desc
+    lo, hi = np.zeros(d.dof), np.zeros(d.dof)
+    for l in range(d.n_links):
+        j = d.joint_index[l]
+        if j >= 0:
+            lo[j], hi[j] = d.limit_lo[l], d.limit_hi[l]
+    q = np.random.default_rng(9).uniform(lo, hi, size=(24, d.dof))
+    clean, depth = lg.api.collision_batch(ctx, H, q, pl["pose"], inp.raw, inp.params.penetration_margin)
+    dirty = 0
+    for i in range(24):
+        ref = R.collision(inp, q[i], pl["pose"][i], inp.raw, inp.params.penetration_margin)
+        assert bool(clean[i]) == (ref["n_violations"] == 0), i
+        assert depth[i] == ref["max_penetration"], i
+        dirty += ref["n_violations"] > 0
+    assert dirty > 0
