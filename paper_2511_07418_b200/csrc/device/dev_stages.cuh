@@ -109,8 +109,11 @@ __global__ void k_grid_gather(DSamples s, const int* id, DGrid g) {
 // reference's |d| > h test); blocked is an existential, so the visit order
 // does not matter.
 __global__ void k_preprocess_grid(DSamples s, DGrid g, double h, double d, uint8_t* keep) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= s.n) return;
+  // threads take the samples in cell order, so a warp's probe cubes overlap
+  // and their row loads hit L1
+  const int ti = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ti >= s.n) return;
+  const int i = g.id[ti];
   const V3 ni = s.nrm(i);
   const V3 c = axpy(s.p(i), d, ni);
   const double m = g.w * 0x1p-20;
