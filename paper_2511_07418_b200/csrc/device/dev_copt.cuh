@@ -208,6 +208,7 @@ struct DomIdx {
   long long cstride;
   const double* sb;         // super-chunk boxes [6][sstride]
   long long sstride;
+  const int* cs;            // chunk starts (element offset in its domain), [cstride]
   const long long* choff;   // first chunk of each (candidate, slot) domain
   const long long* suoff;   // first super-chunk of each domain
 };
@@ -247,20 +248,76 @@ __global__ void k_dom_keys(int nA, int k, const int* alive_idx, const double* aa
   }
 }
 
-// Sorted SoA copy of each domain, its chunk boxes and super-chunk boxes
-// (block per domain).
+// Chunks: runs of the Morton order cut where the key changes above bit
+// kSplitBit (a jump of the curve to another 2^(kSplitBit/3)-cell block: a
+// chunk spanning one is long and thin, and its box is hit by many queries),
+// and every 32 elements inside a run.  head(t) = run head, or (t - run
+// start) % 32 == 0; the run start is a block max-scan of the head positions.
+constexpr int kSplitBit = 17;
+
+template <typename F>
+__device__ void dom_chunk_heads(const uint32_t* key, int ne, F&& emit) {
+  typedef cub::BlockScan<int, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_carry_run, s_carry_cnt;
+  if (threadIdx.x == 0) {
+    s_carry_run = 0;
+    s_carry_cnt = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < ne; base += 256) {
+    const int t = base + threadIdx.x;
+    const bool in = t < ne;
+    const bool jump = in && (t == 0 || ((key[t] ^ key[t - 1]) >> kSplitBit) != 0);
+    int run = jump ? t : -1, run_incl;
+    Scan(tmp).InclusiveScan(run, run_incl, cub::Max());
+    __syncthreads();
+    if (run_incl < s_carry_run) run_incl = s_carry_run;
+    const bool head = in && ((t - run_incl) % 32 == 0);
+    int pos, total;
+    Scan(tmp).ExclusiveSum(head ? 1 : 0, pos, total);
+    if (head) emit(s_carry_cnt + pos, t);
+    __syncthreads();
+    if (threadIdx.x == 255) s_carry_run = run_incl;
+    if (threadIdx.x == 0) s_carry_cnt += total;
+    __syncthreads();
+  }
+}
+
+// Number of chunks of each domain (block per domain; keys sorted).
+__global__ void k_dom_chunk_count(int nseg, const long long* el_off, const uint32_t* keys_sorted,
+                                  int* nch) {
+  const int seg = blockIdx.x;
+  if (seg >= nseg) return;
+  const long long b = el_off[seg];
+  const int ne = (int)(el_off[seg + 1] - b);
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  dom_chunk_heads(keys_sorted + b, ne, [&](int c, int) { atomicMax(&s_n, c + 1); });
+  __syncthreads();
+  if (threadIdx.x == 0) nch[seg] = s_n;
+}
+
+// Sorted SoA copy of each domain, its chunk starts, chunk boxes and
+// super-chunk boxes (block per domain).
 __global__ void k_dom_chunks(int nseg, const long long* el_off, const long long* ch_off,
-                             const long long* su_off, const int* vals_sorted, const double* el_p,
-                             DomIdx d) {
+                             const long long* su_off, const uint32_t* keys_sorted,
+                             const int* vals_sorted, const double* el_p, DomIdx d) {
   const int seg = blockIdx.x;
   if (seg >= nseg) return;
   double* sx = const_cast<double*>(d.sx);
   double* sy = const_cast<double*>(d.sy);
   double* sz = const_cast<double*>(d.sz);
   int* si = const_cast<int*>(d.si);
+  int* cs = const_cast<int*>(d.cs);
   double* cb = const_cast<double*>(d.cb);
   double* sb = const_cast<double*>(d.sb);
   const long long b = el_off[seg], e = el_off[seg + 1];
+  const int ne = (int)(e - b);
+  const long long c0 = ch_off[seg];
+  const int nch = (int)(ch_off[seg + 1] - c0);
+  dom_chunk_heads(keys_sorted + b, ne, [&](int c, int t) { cs[c0 + c] = t; });
   for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
     const int o = vals_sorted[t];
     const long long src = b + o;
@@ -270,11 +327,9 @@ __global__ void k_dom_chunks(int nseg, const long long* el_off, const long long*
     si[t] = o;
   }
   __syncthreads();
-  const long long c0 = ch_off[seg];
-  const int nch = (int)(ch_off[seg + 1] - c0);
   for (int c = threadIdx.x; c < nch; c += blockDim.x) {
-    const long long j0 = b + (long long)c * kChunk;
-    const long long j1 = j0 + kChunk < e ? j0 + kChunk : e;
+    const long long j0 = b + cs[c0 + c];
+    const long long j1 = b + (c + 1 < nch ? cs[c0 + c + 1] : ne);
     double mn[3] = {kInf, kInf, kInf}, mx[3] = {-kInf, -kInf, -kInf};
     for (long long j = j0; j < j1; ++j) {
       const double v[3] = {sx[j], sy[j], sz[j]};
@@ -332,9 +387,11 @@ __device__ __forceinline__ void warp_lexmin(double& d, int& o) {
 __device__ int project_coop(const DomIdx& D, long long seg, long long base, int ne, V3 cp_own,
                             bool act_own, int cur_id, V3 cur_p, int lane,
                             unsigned long long& evals) {
-  const int nch = (ne + kChunk - 1) / kChunk;
-  const int nsu = (nch + 31) / 32;
   const long long c0 = D.choff[seg], s0 = D.suoff[seg];
+  const int nch = (int)(D.choff[seg + 1] - c0);
+  const int nsu = (int)(D.suoff[seg + 1] - s0);
+  const int* CS = D.cs + c0;
+  auto chunk_end = [&](int c) { return c + 1 < nch ? CS[c + 1] : ne; };
   const double* SX = D.sx + base;
   const double* SY = D.sy + base;
   const double* SZ = D.sz + base;
@@ -373,8 +430,8 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
     double bd = sqnorm(sub(cur_p, cp));
     int bi = cur_id;
     {
-      const int j = cbest * kChunk + lane;
-      if (j < ne) {
+      const int j = CS[cbest] + lane;
+      if (j < chunk_end(cbest)) {
         const double d = sqnorm(sub(v3(SX[j], SY[j], SZ[j]), cp));
         const int o = SI[j];
         if (d < bd || (d == bd && o < bi)) {
@@ -384,7 +441,7 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
       }
       warp_lexmin(bd, bi);
     }
-    unsigned long long ev = (unsigned long long)(ne - cbest * kChunk < kChunk ? ne - cbest * kChunk : kChunk);
+    unsigned long long ev = (unsigned long long)(chunk_end(cbest) - CS[cbest]);
     // pass 2: every other box whose lower bound does not exceed the best
     double thr = bd * (1.0 + 0x1p-40);
     double dl = bd;
@@ -396,14 +453,22 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
       const int c2 = ss * 32 + lane;
       const bool nc = c2 < nch && c2 != cbest && !(box_lb(D.cb, D.cstride, c0 + c2, cp) > thr);
       unsigned mc = __ballot_sync(kFull, nc);
-      ev += (unsigned long long)__popc(mc) * kChunk;
+      {  // elements evaluated: the needed chunks' sizes
+        int sz = nc ? chunk_end(c2) - CS[c2] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sz += __shfl_xor_sync(kFull, sz, o);
+        ev += (unsigned long long)sz;
+      }
       while (mc) {
-        int jj[4];
+        int jj[4], je[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           jj[u] = -1;
+          je[u] = 0;
           if (mc) {
-            jj[u] = (ss * 32 + __ffs(mc) - 1) * kChunk + lane;
+            const int cc = ss * 32 + __ffs(mc) - 1;
+            jj[u] = CS[cc] + lane;
+            je[u] = chunk_end(cc);
             mc &= mc - 1;
           }
         }
@@ -411,7 +476,7 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
         int po[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const bool ok = jj[u] >= 0 && jj[u] < ne;
+          const bool ok = jj[u] >= 0 && jj[u] < je[u];
           const int j = ok ? jj[u] : 0;
           px[u] = ok ? SX[j] : 0.0;
           py[u] = ok ? SY[j] : 0.0;

@@ -51,7 +51,7 @@ std::mutex g_streams_mu;
 std::set<cudaStream_t> g_live_streams;  // streams of live contexts
 std::map<cudaStream_t, std::multimap<size_t, void*>> g_cache;
 std::map<cudaStream_t, size_t> g_cache_bytes;
-constexpr size_t kCacheCap = size_t(16) << 30;
+constexpr size_t kCacheCap = size_t(64) << 30;  // of 180 GB HBM
 
 void drop_cache(cudaStream_t s);
 
@@ -964,20 +964,12 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       const char* e = std::getenv("LG_PROJ");
       return e && std::string(e) == "brute";
     }();
-    Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff;
+    Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff, b_cs, b_nch;
     DomIdx dom{};
     long long max_dom = 0;
     for (size_t t = 0; t + 1 < eloff.size(); ++t) max_dom = std::max(max_dom, eloff[t + 1] - eloff[t]);
     if (!proj_brute && max_dom >= kCoopMin) {
       const int nseg = nA * k;
-      std::vector<long long> choff((size_t)nseg + 1, 0), suoff((size_t)nseg + 1, 0);
-      for (int t = 0; t < nseg; ++t) {
-        const long long nch = (eloff[t + 1] - eloff[t] + kChunk - 1) / kChunk;
-        choff[t + 1] = choff[t] + nch;
-        suoff[t + 1] = suoff[t] + (nch + 31) / 32;
-      }
-      long long* d_choff = dupload(b_choff, choff.data(), choff.size(), s);
-      long long* d_suoff = dupload(b_suoff, suoff.data(), suoff.size(), s);
       uint32_t* d_k = dalloc<uint32_t>(b_keys, (size_t)nel);
       uint32_t* d_k2 = dalloc<uint32_t>(b_keys2, (size_t)nel);
       int* d_v = dalloc<int>(b_vals, (size_t)nel);
@@ -991,21 +983,36 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       CK(cub::DeviceSegmentedSort::SortPairs(ctx->tmp(tb), tb, d_k, d_k2, d_v, d_v2, (int)nel, nseg,
                                              d_eloff, d_eloff + 1, s));
       LAUNCH(ctx);
+      // chunk counts (runs of the Morton order split at jumps), then offsets
+      int* d_nch = dalloc<int>(b_nch, (size_t)nseg);
+      k_dom_chunk_count<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_k2, d_nch);
+      LAUNCH(ctx);
+      check_launch();
+      const std::vector<int> nch = ddownload(d_nch, (size_t)nseg, s);
+      std::vector<long long> choff((size_t)nseg + 1, 0), suoff((size_t)nseg + 1, 0);
+      for (int t = 0; t < nseg; ++t) {
+        choff[t + 1] = choff[t] + nch[t];
+        suoff[t + 1] = suoff[t] + (nch[t] + 31) / 32;
+      }
+      long long* d_choff = dupload(b_choff, choff.data(), choff.size(), s);
+      long long* d_suoff = dupload(b_suoff, suoff.data(), suoff.size(), s);
       double* d_sp = dalloc<double>(b_sp, 3 * (size_t)nel);
       const long long cs = std::max(choff.back(), 1ll), ss = std::max(suoff.back(), 1ll);
       double* d_cb = dalloc<double>(b_cb, 6 * (size_t)cs);
       double* d_sb = dalloc<double>(b_sb, 6 * (size_t)ss);
+      int* d_cs = dalloc<int>(b_cs, (size_t)cs);
       dom.sx = d_sp;
       dom.sy = d_sp + nel;
       dom.sz = d_sp + 2 * nel;
       dom.si = reinterpret_cast<int*>(d_k);  // the key buffer is free after the sort
+      dom.cs = d_cs;
       dom.cb = d_cb;
       dom.cstride = cs;
       dom.sb = d_sb;
       dom.sstride = ss;
       dom.choff = d_choff;
       dom.suoff = d_suoff;
-      k_dom_chunks<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_choff, d_suoff, d_v2, d_elp, dom);
+      k_dom_chunks<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_choff, d_suoff, d_k2, d_v2, d_elp, dom);
       LAUNCH(ctx);
       check_launch();
     }
