@@ -382,7 +382,7 @@ int lg_preprocess(lg_ctx* ctx, const double* samples, int n,
                   double probe_half_width, double depth_threshold,
                   uint8_t* keep);
 
-/* Batched wrench solves (wrench.cpp:323-411): problem i has n[i] <= 6
+/* Batched wrench solves (solve_fswo / solve_gswo, wrench.cpp:179-228,247-258): problem i has n[i] <= 6
  * contacts given as points/inward normals [i][6][3]; tangent frames come from
  * tangent_basis.  mode 0 = solve_fswo, 1 = solve_gswo. Outputs objective,
  * anchor, alpha/beta_x/beta_y [i][6]. */

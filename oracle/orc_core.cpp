@@ -304,13 +304,13 @@ void point_jacobian(const Hand& h, const std::vector<Xf>& frames, int link, V3 l
   }
 }
 
-int Groups::group_of(int link) const {  // hand.cpp:506-513
+int Groups::group_of(int link) const {  // hand.cpp:365-372
   for (size_t g = 0; g < groups.size(); ++g)
     if (std::binary_search(groups[g].begin(), groups[g].end(), link)) return (int)g;
   return -1;
 }
 
-Groups dependency_groups(const Hand& h) {  // hand.cpp:515-552
+Groups dependency_groups(const Hand& h) {  // hand.cpp:374-411
   int n = (int)h.links.size();
   std::vector<bool> is_static(n, false);
   for (int l : h.topo) {

@@ -399,7 +399,7 @@ def _bind_batch_sigs():
 
 def wrench_solve_batch(ctx, problems, lambda_torque=10.0, mu=0.0, gswo=None, iterations=64,
                        warm_iterations=8, step=0.1, max_backtracks=20):
-    """Batched solve_fswo / solve_gswo (wrench.cpp:391-402), cold start.
+    """Batched solve_fswo / solve_gswo (wrench.cpp:247-258), cold start.
     problems: list of (points (n,3), inward normals (n,3)), n <= 6."""
     L = _bind_batch_sigs()
     m = len(problems)

@@ -149,7 +149,7 @@ __device__ double pv_descend(const PV& w, int anchor, int iterations, double ste
   return current;
 }
 
-// One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
+// One anchor of run_solver (wrench.cpp:179-228): cold (warm == nullptr) or
 // warm-started from `warm` ([3][kMaxC]); state st = [3][kMaxC].
 template <int NC>
 __device__ __forceinline__ double pv_anchor(const PV& w, int anchor, const WOpts& o,

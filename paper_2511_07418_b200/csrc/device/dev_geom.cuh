@@ -590,7 +590,7 @@ struct WOpts {
   double step;
 };
 
-// One anchor of run_solver (wrench.cpp:336-367): cold (warm == nullptr) or
+// One anchor of run_solver (wrench.cpp:179-228): cold (warm == nullptr) or
 // warm-started; returns the anchor's final objective, state in s.
 __device__ __forceinline__ double wsolve_anchor(const WProb& w, int anchor, bool fr,
                                                 const WOpts& o, const WState* warm, WState& s,
@@ -615,7 +615,7 @@ __device__ __forceinline__ double wsolve_anchor(const WProb& w, int anchor, bool
   return wdescend(w, anchor, false, iters, o.step, o.max_bt, s, ctr);
 }
 
-// run_solver (wrench.cpp:323-370) sequentially over anchors in one thread;
+// run_solver (wrench.cpp:179-228) sequentially over anchors in one thread;
 // fr = (mu > 0) is solve() of contact_opt.cpp:37-41 / solve_gswo.
 __device__ double wsolve(const WProb& w, const WOpts& o, const WState* warm, int* anchor_out,
                          WState& best, Ctr& ctr) {

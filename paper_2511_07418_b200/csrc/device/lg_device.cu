@@ -214,7 +214,7 @@ int bits_for(unsigned long long range) {
   return b;
 }
 
-// Host-side dependency groups from a flat description (hand.cpp:515-552).
+// Host-side dependency groups from a flat description (hand.cpp:374-411).
 std::vector<int> groups_of(const lg_hand_desc& h, int* n_groups) {
   int n = h.n_links;
   std::vector<bool> st(n, false);

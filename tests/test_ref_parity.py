@@ -126,6 +126,10 @@ GPU_CASES = CPU_CASES + [
     # configs[2] (LEAP-class on tools) at leap.cfg as written
     ("leap.cfg", "leap_like.urdf", "mug.obj", 192, ""),
     ("leap.cfg", "leap_like.urdf", "drill.obj", 256, ""),
+    # the largest codebook the config accepts in shared memory for the query
+    # kernels (C = 2048: 48 KiB of codebook plus the kernels' static arrays)
+    ("four_finger.cfg", "four_finger.urdf", "sphere_r030.obj", 96,
+     "codebook_size = 2048\nfield_configs = 48"),
 ]
 
 
