@@ -412,6 +412,26 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
                      int finetune_iterations, double* q, double* max_residual,
                      int* finite, unsigned long long* used_joints);
 
+/* solve_contact_ik (ik.cpp:30-139; ik.hpp:49-51) for m problems: problem i
+ * has k[i] <= LG_MAX_K targets (CSR over the target arrays, as in
+ * lg_realize_batch) and starts from q0 [m][dof]; the remaining arguments are
+ * IkParams.  Writes q [m][dof], finite, used_joints (bit j = joint j),
+ * IkResult.iterations and .objective, and per target (CSR) the position
+ * residual and the cosine std::clamp(hand normal . object normal, -1, 1)
+ * whose std::acos is IkResult.residuals[].normal_angle (the caller applies
+ * its libm).  Invalid arguments return LG_ERR_INVALID_ARGUMENT with the
+ * reference's messages. */
+int lg_contact_ik_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                        const double* q0, const double* object_points,
+                        const double* object_normals, const int* links,
+                        const double* hand_points, const double* hand_normals,
+                        double beta, int iterations, double step_clamp,
+                        double residual_tol, double damping_scale, double damping_min,
+                        int max_backtracks, double* q, int* finite,
+                        unsigned long long* used_joints, int* iterations_out,
+                        double* objective, double* position_residual,
+                        double* normal_cosine);
+
 /* validate_dataset (validate.cpp:56-175) per grasp: every measured quantity
  * the reference's checks read, in its check order.  status: 0 fully checked,
  * 1 joint vector size mismatch, 2 pose not rigid, 3 joint limits violated,

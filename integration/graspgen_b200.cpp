@@ -7,6 +7,7 @@
 //   run_batch                 (pipeline.hpp:150, pipeline.cpp:308-625)
 //   optimize_contacts         (contact_opt.hpp:49-52, contact_opt.cpp:45-142)
 //   validate_grasp_collisions (collision.hpp:71-74, collision.cpp:230-288)
+//   solve_contact_ik          (ik.hpp:49-51, ik.cpp:30-139)
 //
 // Everything the reference keeps on the host stays the reference's code:
 // parse_config, load_hand (URDF + quickhull parts), load_mesh,
@@ -22,6 +23,7 @@
 //   oracle/_ref/graspgen_b200          the reference CLI on the device
 //   oracle/_ref/test_contact_opt_b200  the reference's Catch2 tests
 //   oracle/_ref/test_collision_b200    against the device entry points
+//   oracle/_ref/test_ik_b200
 // and tests/test_integration.py runs them on the GPU.
 #include <chrono>
 #include <cstring>
@@ -35,6 +37,7 @@
 #include "graspgen/contact_field.hpp"
 #include "graspgen/contact_opt.hpp"
 #include "graspgen/hand.hpp"
+#include "graspgen/ik.hpp"
 #include "graspgen/mesh.hpp"
 #include "graspgen/pipeline.hpp"
 #include "graspgen/rng.hpp"
@@ -363,6 +366,51 @@ CollisionReport validate_grasp_collisions(const HandModel& model, const Eigen::V
   rep.narrow_gjk = static_cast<std::size_t>(pairs[1]);
   rep.narrow_halfplane = static_cast<std::size_t>(pairs[2]);
   return rep;
+}
+
+// solve_contact_ik (ik.cpp:30-139) on the device.  The device returns each
+// target's clamped normal cosine; normal_angle is its std::acos, as in
+// ik.cpp:136-137.
+IkResult solve_contact_ik(const HandModel& model, const Eigen::VectorXd& q0,
+                          const std::vector<ContactTarget>& targets, const IkParams& params) {
+  if (q0.size() != model.actuated_count)
+    throw std::invalid_argument("solve_contact_ik: config dimension mismatch");
+  FlatHand hand(model);
+  const int k = static_cast<int>(targets.size());
+  std::vector<double> op, on, hp, hn;
+  std::vector<int> links;
+  for (const ContactTarget& t : targets) {
+    op.insert(op.end(), {t.object_point.x(), t.object_point.y(), t.object_point.z()});
+    on.insert(on.end(), {t.object_normal.x(), t.object_normal.y(), t.object_normal.z()});
+    hp.insert(hp.end(), {t.hand_point_local.x(), t.hand_point_local.y(), t.hand_point_local.z()});
+    hn.insert(hn.end(), {t.hand_normal_local.x(), t.hand_normal_local.y(), t.hand_normal_local.z()});
+    links.push_back(t.link);
+  }
+  const int dof = model.actuated_count;
+  std::vector<double> qi(q0.data(), q0.data() + dof), q(std::max(dof, 1));
+  std::vector<double> pos(std::max(k, 1)), cosv(std::max(k, 1));
+  int finite = 0, iters = 0;
+  unsigned long long used = 0;
+  double objective = 0.0;
+  check(lg_contact_ik_batch(context(), &hand.d, 1, &k, qi.data(), op.data(), on.data(), links.data(),
+                            hp.data(), hn.data(), params.beta, params.iterations, params.step_clamp,
+                            params.residual_tol, params.damping_scale, params.damping_min,
+                            params.max_backtracks, q.data(), &finite, &used, &iters, &objective,
+                            pos.data(), cosv.data()));
+  IkResult res;
+  res.q = Eigen::VectorXd(dof);
+  for (int j = 0; j < dof; ++j) res.q[j] = q[j];
+  res.used_joints.assign(dof, false);
+  for (int j = 0; j < dof; ++j) res.used_joints[j] = ((used >> j) & 1ull) != 0;
+  res.finite = finite != 0;
+  res.iterations = iters;
+  res.objective = objective;
+  res.residuals.resize(k);
+  for (int i = 0; i < k; ++i) {
+    res.residuals[i].position = pos[i];
+    res.residuals[i].normal_angle = std::acos(cosv[i]);
+  }
+  return res;
 }
 
 }  // namespace graspgen

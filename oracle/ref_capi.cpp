@@ -775,6 +775,50 @@ int ref_realize(const ref_inputs* in, const double* q0, int k, const double* obj
   });
 }
 
+// solve_contact_ik (ik.cpp:30-139) with every IkParams field: q, finite,
+// used joints, iterations, objective, per-target residuals.
+int ref_contact_ik(const ref_inputs* in, const double* q0, int k, const double* obj_p,
+                   const double* obj_n, const int* link, const double* hand_p, const double* hand_n,
+                   double beta, int iterations, double step_clamp, double residual_tol,
+                   double damping_scale, double damping_min, int max_backtracks, double* q,
+                   int* finite, unsigned long long* used_joints, int* iters, double* objective,
+                   double* position, double* normal_angle) {
+  return guard([&] {
+    const int dof = in->model.actuated_count;
+    Eigen::VectorXd q0v(dof);
+    for (int j = 0; j < dof; ++j) q0v[j] = q0[j];
+    std::vector<ContactTarget> t(static_cast<std::size_t>(k));
+    for (int i = 0; i < k; ++i) {
+      t[i].object_point = get3(obj_p + 3 * i);
+      t[i].object_normal = get3(obj_n + 3 * i);
+      t[i].link = link[i];
+      t[i].hand_point_local = get3(hand_p + 3 * i);
+      t[i].hand_normal_local = get3(hand_n + 3 * i);
+    }
+    IkParams ikp;
+    ikp.beta = beta;
+    ikp.iterations = iterations;
+    ikp.step_clamp = step_clamp;
+    ikp.residual_tol = residual_tol;
+    ikp.damping_scale = damping_scale;
+    ikp.damping_min = damping_min;
+    ikp.max_backtracks = max_backtracks;
+    IkResult r = solve_contact_ik(in->model, q0v, t, ikp);
+    for (int j = 0; j < dof; ++j) q[j] = r.q[j];
+    *finite = r.finite ? 1 : 0;
+    unsigned long long m = 0;
+    for (std::size_t j = 0; j < r.used_joints.size(); ++j)
+      if (r.used_joints[j]) m |= 1ull << j;
+    *used_joints = m;
+    *iters = r.iterations;
+    *objective = r.objective;
+    for (int i = 0; i < k; ++i) {
+      position[i] = r.residuals[i].position;
+      normal_angle[i] = r.residuals[i].normal_angle;
+    }
+  });
+}
+
 // validate_grasp_collisions (collision.cpp:230-288): the report's clean flag,
 // max penetration and the violation list (link_b = -1 for the object).
 int ref_collision(const ref_inputs* in, const double* q, const double* pose12, const double* samples,

@@ -81,6 +81,9 @@ def lib():
                                       ip, P(C.c_ulonglong), dp, dp, ip, dp]),
             "ref_collision": (C.c_int, [vp, dp, dp, dp, C.c_int, C.c_double, ip, dp, ip, C.c_int,
                                         ip, ip, dp, ip]),
+            "ref_contact_ik": (C.c_int, [vp, dp, C.c_int, dp, dp, ip, dp, dp, C.c_double, C.c_int,
+                                         C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
+                                         dp, ip, P(C.c_ulonglong), ip, dp, dp, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -402,6 +405,26 @@ def realize(inputs, q0, targets, beta=0.01, iterations=30, step_clamp=0.2, resid
                             _p(rp), _p(rn), _i(rl), _p(res)))
     return {"q": q, "max_residual": mr.value, "finite": fin.value, "used_joints": used.value,
             "realized_p": rp, "realized_n": rn, "realized_link": rl, "residuals": res}
+
+
+def contact_ik(inputs, q0, targets, beta=0.01, iterations=30, step_clamp=0.2, residual_tol=1e-4,
+               damping_scale=1e-4, damping_min=1e-6, max_backtracks=10):
+    """solve_contact_ik; targets = [(obj_p, obj_n, link, hand_p, hand_n), ...]."""
+    k = len(targets)
+    op = _d([t[0] for t in targets]).reshape(-1, 3)
+    on = _d([t[1] for t in targets]).reshape(-1, 3)
+    lk = np.array([t[2] for t in targets], dtype=np.int32)
+    hp = _d([t[3] for t in targets]).reshape(-1, 3)
+    hn = _d([t[4] for t in targets]).reshape(-1, 3)
+    q = np.zeros(inputs.hand_desc.dof)
+    fin, used, its, obj = C.c_int(0), C.c_ulonglong(0), C.c_int(0), C.c_double(0)
+    pos, ang = np.zeros(max(k, 1)), np.zeros(max(k, 1))
+    check(lib().ref_contact_ik(inputs._h, _p(_d(q0)), k, _p(op), _p(on), _i(lk), _p(hp), _p(hn),
+                               beta, iterations, step_clamp, residual_tol, damping_scale,
+                               damping_min, max_backtracks, _p(q), C.byref(fin), C.byref(used),
+                               C.byref(its), C.byref(obj), _p(pos), _p(ang)))
+    return {"q": q, "finite": fin.value, "used_joints": used.value, "iterations": its.value,
+            "objective": obj.value, "position": pos[:k], "normal_angle": ang[:k]}
 
 
 def collision(inputs, q, pose12, samples, margin=0.002, cap=256):

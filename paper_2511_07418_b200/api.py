@@ -393,6 +393,11 @@ def _bind_batch_sigs():
                                    A.dp, A.dp, C.c_double, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, C.c_int, A.dp, A.dp, A.ip,
                                    P(C.c_ulonglong)]
+    L.lg_contact_ik_batch.restype = C.c_int
+    L.lg_contact_ik_batch.argtypes = [C.c_void_p, P(A.HandDesc), C.c_int, A.ip, A.dp, A.dp, A.dp,
+                                      A.ip, A.dp, A.dp, C.c_double, C.c_int, C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_int, A.dp, A.ip,
+                                      P(C.c_ulonglong), A.ip, A.dp, A.dp, A.dp]
     L._batch_bound = True
     return L
 
@@ -438,6 +443,40 @@ def collision_batch(ctx, hand, q, poses, samples, margin=0.002):
     check(L.lg_collision_batch(ctx._h, C.byref(hand.desc), m, _dp(q), _dp(p), _dp(s), len(s),
                                float(margin), clean.ctypes.data_as(C.POINTER(C.c_uint8)), _dp(mp)))
     return clean.astype(bool), mp
+
+
+def contact_ik_batch(ctx, hand, q0, problems, beta=0.01, iterations=30, step_clamp=0.2,
+                     residual_tol=1e-4, damping_scale=1e-4, damping_min=1e-6, max_backtracks=10):
+    """Batched solve_contact_ik (ik.cpp:30-139).  problems: list of target
+    lists, each target (object_point, inward normal, link, hand point, hand
+    normal).  Returns a dict of q, finite, used_joints, iterations, objective,
+    and per problem the position residuals and clamped normal cosines."""
+    L = _bind_batch_sigs()
+    m = len(problems)
+    k = np.array([len(t) for t in problems], dtype=np.int32)
+    flat = [t for ts in problems for t in ts]
+    nt = max(len(flat), 1)
+    op = np.ascontiguousarray([t[0] for t in flat] or [[0, 0, 0]], dtype=np.float64).reshape(-1, 3)
+    on = np.ascontiguousarray([t[1] for t in flat] or [[0, 0, 0]], dtype=np.float64).reshape(-1, 3)
+    links = np.ascontiguousarray([t[2] for t in flat] or [0], dtype=np.int32)
+    hp = np.ascontiguousarray([t[3] for t in flat] or [[0, 0, 0]], dtype=np.float64).reshape(-1, 3)
+    hn = np.ascontiguousarray([t[4] for t in flat] or [[0, 0, 0]], dtype=np.float64).reshape(-1, 3)
+    q0 = np.ascontiguousarray(q0, dtype=np.float64).reshape(m, hand.dof)
+    q = np.zeros_like(q0)
+    fin = np.zeros(m, dtype=np.int32)
+    used = np.zeros(m, dtype=np.uint64)
+    its = np.zeros(m, dtype=np.int32)
+    obj = np.zeros(m)
+    pos, cos = np.zeros(nt), np.zeros(nt)
+    check(L.lg_contact_ik_batch(ctx._h, C.byref(hand.desc), m, _ip(k), _dp(q0), _dp(op), _dp(on),
+                                _ip(links), _dp(hp), _dp(hn), beta, iterations, step_clamp,
+                                residual_tol, damping_scale, damping_min, max_backtracks, _dp(q),
+                                _ip(fin), used.ctypes.data_as(C.POINTER(C.c_ulonglong)), _ip(its),
+                                _dp(obj), _dp(pos), _dp(cos)))
+    off = np.concatenate([[0], np.cumsum(k)])
+    return {"q": q, "finite": fin, "used_joints": used, "iterations": its, "objective": obj,
+            "position": [pos[off[i]:off[i + 1]] for i in range(m)],
+            "cosine": [cos[off[i]:off[i + 1]] for i in range(m)]}
 
 
 def realize_batch(ctx, hand, q0, problems, beta=0.01, iterations=30, step_clamp=0.2,

@@ -417,7 +417,8 @@ __device__ __forceinline__ void wldlt_solve(int n, int ld, double* A, double* x,
 // joints with a nonzero column.
 __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const IkCfg& P, int iterations,
                     unsigned long long& used, WarpWs& ws, double* F, const WChain& C, double* FG,
-                    double* rtG, bool have_frames, const unsigned short* ab, Ctr& ctr, int lane) {
+                    double* rtG, bool have_frames, const unsigned short* ab, Ctr& ctr, int lane,
+                    int* it_out = nullptr, double* obj_out = nullptr) {
   const int dof = c_hand.dof;
   const int ld = dof | 1;  // odd row stride: column accesses hit distinct banks
   const int rows = 6 * k;
@@ -432,12 +433,18 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
     wchain_commit(C, FG, 0, F, lane);
   }
   ++ctr.fk;
+  if (it_out) {  // IkResult.iterations / objective of the k == 0 early return
+    *it_out = 0;
+    *obj_out = 0.0;
+  }
   if (k == 0) return true;
   bool finite = true;
   double* r = ws.r;
   double objective = wresidual(F, T, k, P.beta, r, lane);
+  int iters = 0;
   for (int it = 0; it < iterations; ++it) {
     ++ctr.ik_it;
+    iters = it + 1;
     // Jacobian points: lane p < 2k -> target p/2, half p%2
     if (lane < 2 * k) {
       int i = lane >> 1;
@@ -570,6 +577,10 @@ __device__ __forceinline__ bool wik(double* q, const WTargets& T, int k, const I
   }
   bool nonfin = lane < dof && !is_finite(q[lane]);
   if (__any_sync(kFull, nonfin)) finite = false;
+  if (it_out) {
+    *it_out = iters;
+    *obj_out = objective;
+  }
   return finite;
 }
 
@@ -666,12 +677,22 @@ __host__ __device__ __forceinline__ size_t realize_warp_bytes(int dof, int kmax,
 
 // One warp per problem; targets [t][kMaxK][12] + links [t][kMaxK]; q_out
 // [t][kMaxDof] holds q0 on entry (mid_config when q_init == nullptr).
-template <int MINB>
+// IKO: solve_contact_ik alone (ik.cpp:30-139) instead of realize_grasp, with
+// IkResult's iterations, objective, per-target position residuals and the
+// clamped cosines of the normal angles in ik_out.
+struct IkOut {
+  int* iterations;
+  double* objective;
+  double* position;  // [t][kMaxK]
+  double* cosine;    // [t][kMaxK]
+};
+
+template <int MINB, bool IKO = false>
 __global__ void __launch_bounds__(128, MINB)
 k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, int fine_iters,
                const double* tgt, int tgt_stride, const int* tl, int tl_stride,
                const double* q_init, double* q_out, double* max_res, int* finite,
-               unsigned long long* used, int* next) {
+               unsigned long long* used, int* next, IkOut ik_out = IkOut{}) {
   // Persistent warps: each takes the next problem when it finishes one
   // (problem cost varies by an order of magnitude, and a CTA's shared memory
   // is held until its slowest warp is done).
@@ -719,10 +740,30 @@ k_realize_warp(int nAct, int k, const int* kk, int kmax, IkCfg P, int rounds, in
     __syncwarp();
     wchain_build(C, T.link, kt, lane);
     wchain_static(T.link, kt, F, lane);
-    double mr;
+    double mr = 0.0;
     unsigned long long u;
-    bool fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, s_ab, ctr,
-                        lane);
+    bool fin;
+    if constexpr (IKO) {
+      int its;
+      double obj;
+      fin = wik(q, T, kt, P, P.iterations, u, ws, F, C, FG, rtG, false, s_ab, ctr, lane, &its, &obj);
+      if (lane < kt) {  // result.residuals (ik.cpp:130-137)
+        const double* tt = T.t + 12 * lane;
+        const V3 hn = xf_rotate(ld_xf(F + kFS * T.link[lane]), v3_load(tt + 9));
+        double c = dot(hn, v3_load(tt + 3));
+        c = c < -1.0 ? -1.0 : (1.0 < c ? 1.0 : c);  // std::clamp
+        ik_out.position[(size_t)t * kMaxK + lane] =
+            norm(v3(ws.r[6 * lane], ws.r[6 * lane + 1], ws.r[6 * lane + 2]));
+        ik_out.cosine[(size_t)t * kMaxK + lane] = c;
+      }
+      if (lane == 0) {
+        ik_out.iterations[t] = its;
+        ik_out.objective[t] = obj;
+      }
+    } else {
+      fin = wrealize(q, qs, T, Ref, kt, P, rounds, fine_iters, &mr, &u, ws, F, C, FG, rtG, s_ab, ctr,
+                     lane);
+    }
     if (lane < dof) q_out[(size_t)t * kMaxDof + lane] = q[lane];
     if (lane == 0) {
       max_res[t] = mr;

@@ -412,7 +412,8 @@ CollKern coll_kernel() {
 void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCfg& P, int rounds,
                          int fine_iters, const double* tgt, int tgt_stride, const int* tl,
                          int tl_stride, const double* q_init, double* q_out, double* max_res,
-                         int* finite, unsigned long long* used, int dof, int n_links) {
+                         int* finite, unsigned long long* used, int dof, int n_links,
+                         const IkOut* ik_out = nullptr) {
   const int wpb = 4;
   const int kmax = kk ? kMaxK : k;
   size_t smem = realize_warp_smem(dof, kmax, n_links, wpb);
@@ -426,7 +427,11 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
     CK(cudaFuncSetAttribute(k_realize_warp<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_realize_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
-  auto kern = minb == 6 ? k_realize_warp<6> : (minb == 5 ? k_realize_warp<5> : k_realize_warp<4>);
+  if (ik_out && first_on_device(17))
+    CK(cudaFuncSetAttribute(k_realize_warp<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024));
+  auto kern = ik_out ? k_realize_warp<4, true>
+                     : (minb == 6 ? k_realize_warp<6> : (minb == 5 ? k_realize_warp<5> : k_realize_warp<4>));
   // persistent grid: as many CTAs as fit at once (warps fetch problems)
   int dev = 0, sms = 0, per_sm = 0;
   CK(cudaGetDevice(&dev));
@@ -438,7 +443,8 @@ void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCf
   int* d_next = dalloc<int>(bnext, 1);
   CK(cudaMemsetAsync(d_next, 0, sizeof(int), s));
   kern<<<grid, 32 * wpb, smem, s>>>(n, k, kk, kmax, P, rounds, fine_iters, tgt, tgt_stride, tl, tl_stride,
-                                    q_init, q_out, max_res, finite, used, d_next);
+                                    q_init, q_out, max_res, finite, used, d_next,
+                                    ik_out ? *ik_out : IkOut{});
 }
 
 // Flattened patch data on the device.
@@ -1774,6 +1780,92 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
     CK(cudaMemcpy(max_residual, d_r, sizeof(double) * m, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(finite, d_f, sizeof(int) * m, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(used_joints, d_u, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost));
+  });
+}
+
+int lg_contact_ik_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
+                        const double* q0, const double* object_points, const double* object_normals,
+                        const int* links, const double* hand_points, const double* hand_normals,
+                        double beta, int iterations, double step_clamp, double residual_tol,
+                        double damping_scale, double damping_min, int max_backtracks, double* q,
+                        int* finite, unsigned long long* used_joints, int* iterations_out,
+                        double* objective, double* position_residual, double* normal_cosine) {
+  return lgc::guard([&] {
+    if (!ctx || !hand || m < 0 || (m > 0 && (!k || !q0 || !q || !finite || !used_joints ||
+                                             !iterations_out || !objective)))
+      throw std::invalid_argument("lg_contact_ik_batch: bad argument");
+    if (beta <= 0.0) throw std::invalid_argument("solve_contact_ik: beta must be > 0");
+    if (m == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    bind_hand(ctx, *hand);
+    std::vector<double> tg((size_t)m * kMaxK * 12, 0.0);
+    std::vector<int> tl((size_t)m * kMaxK, 0);
+    size_t off = 0;
+    for (int i = 0; i < m; ++i) {
+      if (k[i] < 0 || k[i] > kMaxK)
+        throw std::invalid_argument("solve_contact_ik: the device takes 0..5 targets");
+      for (int c = 0; c < k[i]; ++c, ++off) {
+        if (links[off] < 0 || links[off] >= hand->n_links)
+          throw std::invalid_argument("solve_contact_ik: invalid target link");
+        double* T = &tg[((size_t)i * kMaxK + c) * 12];
+        for (int a = 0; a < 3; ++a) {
+          T[a] = object_points[3 * off + a];
+          T[3 + a] = object_normals[3 * off + a];
+          T[6 + a] = hand_points[3 * off + a];
+          T[9 + a] = hand_normals[3 * off + a];
+        }
+        for (int a = 0; a < 12; ++a)
+          if (!std::isfinite(T[a])) throw std::invalid_argument("solve_contact_ik: non-finite target");
+        tl[(size_t)i * kMaxK + c] = links[off];
+      }
+    }
+    std::vector<double> qi((size_t)m * kMaxDof, 0.0);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < hand->dof; ++j) qi[(size_t)i * kMaxDof + j] = q0[(size_t)i * hand->dof + j];
+    Buf bk, bt, bl, bq, br, bf, bu, bit, bob, bpr, bco;
+    int* d_k = dupload(bk, k, (size_t)m, s);
+    double* d_t = dupload(bt, tg.data(), tg.size(), s);
+    int* d_l = dupload(bl, tl.data(), tl.size(), s);
+    double* d_q = dupload(bq, qi.data(), qi.size(), s);
+    double* d_r = dalloc<double>(br, (size_t)m);
+    int* d_f = dalloc<int>(bf, (size_t)m);
+    auto* d_u = dalloc<unsigned long long>(bu, (size_t)m);
+    IkOut io;
+    io.iterations = dalloc<int>(bit, (size_t)m);
+    io.objective = dalloc<double>(bob, (size_t)m);
+    io.position = dalloc<double>(bpr, (size_t)m * kMaxK);
+    io.cosine = dalloc<double>(bco, (size_t)m * kMaxK);
+    IkCfg P;
+    P.beta = beta;
+    P.step_clamp = step_clamp;
+    P.residual_tol = residual_tol;
+    P.damping_scale = damping_scale;
+    P.damping_min = damping_min;
+    P.iterations = iterations;
+    P.max_backtracks = max_backtracks;
+    launch_realize_warp(s, m, 0, d_k, P, 0, 0, d_t, kMaxK * 12, d_l, kMaxK, d_q, d_q, d_r, d_f, d_u,
+                        hand->dof, hand->n_links, &io);
+    check_launch();
+    auto hq = ddownload(d_q, qi.size(), s);
+    auto hf = ddownload(d_f, (size_t)m, s);
+    auto hu = ddownload(d_u, (size_t)m, s);
+    auto hit = ddownload(io.iterations, (size_t)m, s);
+    auto hob = ddownload(io.objective, (size_t)m, s);
+    auto hpr = ddownload(io.position, (size_t)m * kMaxK, s);
+    auto hco = ddownload(io.cosine, (size_t)m * kMaxK, s);
+    off = 0;
+    for (int i = 0; i < m; ++i) {
+      for (int j = 0; j < hand->dof; ++j) q[(size_t)i * hand->dof + j] = hq[(size_t)i * kMaxDof + j];
+      finite[i] = hf[i];
+      used_joints[i] = hu[i];
+      iterations_out[i] = hit[i];
+      objective[i] = hob[i];
+      for (int c = 0; c < k[i]; ++c, ++off) {
+        if (position_residual) position_residual[off] = hpr[(size_t)i * kMaxK + c];
+        if (normal_cosine) normal_cosine[off] = hco[(size_t)i * kMaxK + c];
+      }
+    }
   });
 }
 

@@ -236,3 +236,45 @@ def test_collision_batch_grid_path_matches_reference(ctx):
         assert depth[i] == ref["max_penetration"], i
         dirty += ref["n_violations"] > 0
     assert dirty > 0
+
+
+def test_contact_ik_matches_reference(setup, ctx):
+    """lg_contact_ik_batch == solve_contact_ik (ik.cpp:30-139): q, finite,
+    used joints, iterations, objective and residuals, bit for bit, from
+    mid-range and random starts, with default and tightened IkParams."""
+    import math
+    import paper_2511_07418_b200 as lg
+    s = setup
+    pl = _placements(s, ctx, 0, 8)
+    t = int(np.flatnonzero(pl["accepted"])[0])
+    _, doms = _domains(s, ctx, pl["pose"][t])
+    d = s.inp.hand_desc
+    lo, hi = np.zeros(d.dof), np.zeros(d.dof)
+    for l in range(d.n_links):
+        j = d.joint_index[l]
+        if j >= 0:
+            lo[j], hi[j] = d.limit_lo[l], d.limit_hi[l]
+    rng = np.random.default_rng(5)
+    problems, starts = [], []
+    for r in range(12):
+        els = [dm[(r * 7 + 3 * g) % len(dm)] for g, dm in enumerate(doms) if dm][: 1 + r % 3]
+        targets = []
+        for j, e in enumerate(els):
+            lk, hp, hn = s.ref_field.reverse_lookup(e, 100 * r + j)
+            targets.append((e["pos"], -e["nrm"], lk, hp, hn))
+        problems.append(targets)
+        starts.append(0.5 * (lo + hi) if r % 2 == 0 else rng.uniform(lo, hi))
+    problems.append([])  # k == 0: clamp only
+    starts.append(rng.uniform(lo - 0.5, hi + 0.5))
+    for kw in (dict(), dict(beta=0.02, iterations=40, step_clamp=0.1, residual_tol=1e-6,
+                            damping_scale=1e-3, damping_min=1e-5, max_backtracks=6)):
+        dev = lg.api.contact_ik_batch(ctx, s.H, np.array(starts), problems, **kw)
+        for i, targets in enumerate(problems):
+            ref = R.contact_ik(s.inp, starts[i], targets, **kw)
+            assert dev["q"][i].tobytes() == ref["q"].tobytes(), i
+            assert dev["finite"][i] == ref["finite"]
+            assert int(dev["used_joints"][i]) == ref["used_joints"]
+            assert dev["iterations"][i] == ref["iterations"]
+            assert dev["objective"][i] == ref["objective"]
+            assert dev["position"][i].tobytes() == ref["position"].tobytes()
+            assert [math.acos(c) for c in dev["cosine"][i]] == ref["normal_angle"].tolist()
