@@ -8,6 +8,9 @@
 //   optimize_contacts         (contact_opt.hpp:49-52, contact_opt.cpp:45-142)
 //   validate_grasp_collisions (collision.hpp:71-74, collision.cpp:230-288)
 //   solve_contact_ik          (ik.hpp:49-51, ik.cpp:30-139)
+//   ContactFieldIndex::build  (contact_field.hpp:125-128, contact_field.cpp:306-334)
+//   query_domains             (contact_field.hpp:147-150, contact_field.cpp:380-448)
+//   reverse_lookup            (contact_field.hpp:154-156, contact_field.cpp:450-484)
 //
 // Everything the reference keeps on the host stays the reference's code:
 // parse_config, load_hand (URDF + quickhull parts), load_mesh,
@@ -24,13 +27,18 @@
 //   oracle/_ref/test_contact_opt_b200  the reference's Catch2 tests
 //   oracle/_ref/test_collision_b200    against the device entry points
 //   oracle/_ref/test_ik_b200
+//   oracle/_ref/test_contact_field_b200
 // and tests/test_integration.py runs them on the GPU.
+#include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <stdexcept>
 #include <string>
+#include <unistd.h>
 #include <vector>
 
 #include "graspgen/collision.hpp"
@@ -365,6 +373,134 @@ CollisionReport validate_grasp_collisions(const HandModel& model, const Eigen::V
   rep.broad_pairs = static_cast<std::size_t>(pairs[0]);
   rep.narrow_gjk = static_cast<std::size_t>(pairs[1]);
   rep.narrow_halfplane = static_cast<std::size_t>(pairs[2]);
+  return rep;
+}
+
+namespace {
+
+// The contact-field index crosses between host and device as its GGCF v1
+// file: the library writes and reads the reference's format byte for byte,
+// so a device-built index loads into the reference's ContactFieldIndex and a
+// host index (built, loaded or edited by the caller) loads onto the device.
+std::string ggcf_scratch() {
+  static std::atomic<long> n{0};
+  const char* dir = std::getenv("TMPDIR");
+  return std::string(dir ? dir : "/tmp") + "/graspgen_b200_" + std::to_string(getpid()) + "_" +
+         std::to_string(n++) + ".ggcf";
+}
+
+struct DeviceIndex {
+  lg_field* f = nullptr;
+  DeviceIndex(const ContactFieldIndex& index, const HandModel& model) {
+    const std::string path = ggcf_scratch();
+    index.save(path);
+    FlatHand hand(model);
+    const int rc = lg_field_load(context(), &hand.d, path.c_str(), index.cache_key, &f);
+    std::remove(path.c_str());
+    check(rc);
+    if (!f) throw std::runtime_error("graspgen_b200: the index did not load on the device");
+  }
+  ~DeviceIndex() { lg_field_destroy(f); }
+  DeviceIndex(const DeviceIndex&) = delete;
+  DeviceIndex& operator=(const DeviceIndex&) = delete;
+};
+
+}  // namespace
+
+// ContactFieldIndex::build (contact_field.cpp:306-334) on the device.
+ContactFieldIndex ContactFieldIndex::build(const HandModel& model,
+                                           const std::vector<ContactPatch>& patches, int N,
+                                           double box_width, std::uint64_t seed,
+                                           int codebook_size) {
+  FlatHand hand(model);
+  FlatPatches flat(patches);
+  lg_field* f = nullptr;
+  check(lg_field_build(context(), &hand.d, &flat.d, N, box_width, seed, codebook_size, &f));
+  std::unique_ptr<lg_field, void (*)(lg_field*)> own(f, lg_field_destroy);
+  const std::string path = ggcf_scratch();
+  check(lg_field_save(f, path.c_str(), 0));
+  std::optional<ContactFieldIndex> index = ContactFieldIndex::load(path, 0);
+  std::remove(path.c_str());
+  if (!index) throw std::runtime_error("graspgen_b200: the device index did not load");
+  return std::move(*index);
+}
+
+// query_domains (contact_field.cpp:380-448) on the device.
+std::vector<ContactDomain> query_domains(const ContactFieldIndex& index,
+                                         const std::vector<SurfaceSample>& samples,
+                                         const RigidTransform& object_pose, double theta_hit,
+                                         const HandModel& model, const DependencyGroups& groups) {
+  const int G = static_cast<int>(groups.groups.size());
+  std::vector<ContactDomain> domains(G);
+  for (int g = 0; g < G; ++g) domains[g].group = g;
+  if (index.patches.empty()) return domains;
+  int max_id = 0;
+  for (const PatchIndex& p : index.patches) max_id = std::max(max_id, p.patch_id);
+  std::vector<int> group_of_patch(static_cast<std::size_t>(max_id) + 1, -1);
+  for (const PatchIndex& p : index.patches) {
+    if (p.link < 0 || p.link >= static_cast<int>(model.links.size()))
+      throw std::invalid_argument("query_domains: index link out of range");
+    group_of_patch[p.patch_id] = groups.group_of(p.link);
+  }
+  if (samples.empty()) return domains;
+  DeviceIndex dev(index, model);
+  auto s = flat_samples(samples);
+  double pose[12];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) pose[3 * r + c] = object_pose.rotation(r, c);
+  put3(pose + 9, object_pose.translation);
+  lg_domains* d = nullptr;
+  check(lg_query_domains_elements(context(), dev.f, group_of_patch.data(), G, s.data(),
+                                  static_cast<int>(samples.size()), pose, theta_hit, &d));
+  std::unique_ptr<lg_domains, void (*)(lg_domains*)> own(d, lg_domains_destroy);
+  long long ne = 0;
+  const int *sample = nullptr, *hp = nullptr, *hb = nullptr;
+  const double *pos = nullptr, *nrm = nullptr, *score = nullptr;
+  const long long* hoff = nullptr;
+  check(lg_domains_elements(d, &ne, &sample, &pos, &nrm, &score, &hoff, &hp, &hb));
+  for (int g = 0; g < G; ++g) {
+    long long first = 0, count = 0;
+    check(lg_domains_group(d, g, &first, &count));
+    for (long long e = first; e < first + count; ++e) {
+      DomainElement el;
+      el.position = get3(pos + 3 * e);
+      el.normal = get3(nrm + 3 * e);
+      el.score = score[e];
+      el.hit_patches.assign(hp + hoff[e], hp + hoff[e + 1]);
+      el.hit_boxes.assign(hb + hoff[e], hb + hoff[e + 1]);
+      domains[g].elements.push_back(std::move(el));
+    }
+  }
+  return domains;
+}
+
+// reverse_lookup (contact_field.cpp:450-484) on the device.
+IndexRep reverse_lookup(const ContactFieldIndex& index, const DomainElement& element,
+                        std::uint64_t choice_seed) {
+  if (element.hit_patches.empty() || element.hit_patches.size() != element.hit_boxes.size())
+    throw std::out_of_range("reverse_lookup: element has no hits");
+  // the device needs only the links of the index's patches: a stand-in
+  // model with one link per patch link id
+  HandModel model;
+  int max_link = 0;
+  for (const PatchIndex& p : index.patches) max_link = std::max(max_link, p.link);
+  model.links.resize(static_cast<std::size_t>(max_link) + 1);
+  for (std::size_t l = 0; l < model.links.size(); ++l) {
+    model.links[l].parent = l == 0 ? -1 : 0;
+    model.topo_order.push_back(static_cast<int>(l));
+  }
+  DeviceIndex dev(index, model);
+  const long long hoff[2] = {0, static_cast<long long>(element.hit_patches.size())};
+  double n[3];
+  put3(n, element.normal);
+  int link = -1;
+  double pt[3], nr[3];
+  check(lg_reverse_lookup_batch(context(), dev.f, 1, hoff, element.hit_patches.data(),
+                                element.hit_boxes.data(), n, &choice_seed, &link, pt, nr));
+  IndexRep rep;
+  rep.link = link;
+  rep.point = get3(pt);
+  rep.normal = get3(nr);
   return rep;
 }
 
