@@ -393,6 +393,23 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
                           int* anchor, double* alpha, double* beta_x,
                           double* beta_y);
 
+/* solve_fswo / solve_gswo (wrench.cpp:179-228,247-258) on explicit
+ * WrenchProblems (wrench.hpp:14-27): problem t has n[t] <= 6 contacts with
+ * points, inward normals and the caller's tangent frames [t][6][3], its own
+ * lambda_torque[t] and mu[t]; mode 0 = solve_fswo, 1 = solve_gswo.  use_warm
+ * (may be NULL) selects a warm start per problem from warm_alpha / beta_x /
+ * beta_y [t][6] — the reference's `warm && warm->valid() && size == n` test
+ * (and zero betas when the warm betas are missing) is the caller's.  Outputs
+ * as lg_wrench_solve_batch. */
+int lg_wrench_problem_batch(lg_ctx* ctx, int m, const int* n, const double* points,
+                            const double* normals, const double* tangent_x,
+                            const double* tangent_y, const double* lambda_torque,
+                            const double* mu, int mode, int iterations, int warm_iterations,
+                            double step, int max_backtracks, const int* use_warm,
+                            const double* warm_alpha, const double* warm_beta_x,
+                            const double* warm_beta_y, double* objective, int* anchor,
+                            double* alpha, double* beta_x, double* beta_y);
+
 /* Batched validate_grasp_collisions (collision.cpp:230-288): clean[i] for
  * configuration q[i] (dof) and object pose[i] (12) against the samples. */
 int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m,

@@ -11,6 +11,7 @@
 //   ContactFieldIndex::build  (contact_field.hpp:125-128, contact_field.cpp:306-334)
 //   query_domains             (contact_field.hpp:147-150, contact_field.cpp:380-448)
 //   reverse_lookup            (contact_field.hpp:154-156, contact_field.cpp:450-484)
+//   solve_fswo / solve_gswo / is_stable (wrench.hpp:56-77, wrench.cpp:179-267)
 //
 // Everything the reference keeps on the host stays the reference's code:
 // parse_config, load_hand (URDF + quickhull parts), load_mesh,
@@ -28,6 +29,7 @@
 //   oracle/_ref/test_collision_b200    against the device entry points
 //   oracle/_ref/test_ik_b200
 //   oracle/_ref/test_contact_field_b200
+//   oracle/_ref/test_wrench_b200
 // and tests/test_integration.py runs them on the GPU.
 #include <atomic>
 #include <chrono>
@@ -49,6 +51,7 @@
 #include "graspgen/mesh.hpp"
 #include "graspgen/pipeline.hpp"
 #include "graspgen/rng.hpp"
+#include "graspgen/wrench.hpp"
 #include "lg.h"
 
 namespace graspgen {
@@ -502,6 +505,67 @@ IndexRep reverse_lookup(const ContactFieldIndex& index, const DomainElement& ele
   rep.point = get3(pt);
   rep.normal = get3(nr);
   return rep;
+}
+
+namespace {
+
+// run_solver (wrench.cpp:179-228) for one problem on the device.
+WrenchSolution wrench_device(const WrenchProblem& p, bool gswo, const WrenchSolveOptions& opts,
+                             const WrenchSolution* warm) {
+  const std::size_t n = p.size();
+  if (n == 0) throw std::invalid_argument("wrench solve: no contacts");
+  double pts[18] = {}, nrm[18] = {}, tx[18] = {}, ty[18] = {};
+  for (std::size_t i = 0; i < n && i < 6; ++i) {
+    put3(pts + 3 * i, p.points[i]);
+    put3(nrm + 3 * i, p.normals[i]);
+    put3(tx + 3 * i, p.tangent_x[i]);
+    put3(ty + 3 * i, p.tangent_y[i]);
+  }
+  const int nn = static_cast<int>(n);
+  const bool use_warm = warm && warm->valid() && warm->alpha.size() == n;
+  const int uw = use_warm ? 1 : 0;
+  double wa[6] = {}, wx[6] = {}, wy[6] = {};
+  if (use_warm)
+    for (std::size_t i = 0; i < n && i < 6; ++i) {
+      wa[i] = warm->alpha[i];
+      wx[i] = warm->beta_x.size() == n ? warm->beta_x[i] : 0.0;
+      wy[i] = warm->beta_y.size() == n ? warm->beta_y[i] : 0.0;
+    }
+  double obj = 0.0, a[6], bx[6], by[6];
+  int anchor = -1;
+  check(lg_wrench_problem_batch(context(), 1, &nn, pts, nrm, tx, ty, &p.lambda_torque, &p.mu,
+                                gswo ? 1 : 0, opts.iterations, opts.warm_iterations, opts.step,
+                                opts.max_backtracks, &uw, wa, wx, wy, &obj, &anchor, a, bx, by));
+  WrenchSolution best;
+  if (anchor < 0) return best;  // no anchor improved on +inf
+  best.objective = obj;
+  best.anchor = anchor;
+  best.alpha.assign(a, a + n);
+  best.beta_x.assign(bx, bx + n);
+  best.beta_y.assign(by, by + n);
+  return best;
+}
+
+}  // namespace
+
+// solve_fswo / solve_gswo / is_stable (wrench.cpp:247-267) on the device.
+WrenchSolution solve_fswo(const WrenchProblem& problem, const WrenchSolveOptions& opts,
+                          const WrenchSolution* warm) {
+  return wrench_device(problem, false, opts, warm);
+}
+
+WrenchSolution solve_gswo(const WrenchProblem& problem, const WrenchSolveOptions& opts,
+                          const WrenchSolution* warm) {
+  return wrench_device(problem, problem.mu != 0.0, opts, warm);
+}
+
+bool is_stable(const WrenchProblem& problem, double eps, WrenchSolution* solution,
+               const WrenchSolveOptions& opts) {
+  if (eps <= 0.0) throw std::invalid_argument("is_stable: eps must be > 0");
+  WrenchSolution s = solve_gswo(problem, opts);
+  const bool stable = s.objective < eps;
+  if (solution) *solution = std::move(s);
+  return stable;
 }
 
 // solve_contact_ik (ik.cpp:30-139) on the device.  The device returns each

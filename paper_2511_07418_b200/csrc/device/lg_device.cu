@@ -1412,9 +1412,122 @@ __global__ void k_wrench_batch(int m, const int* n, const double* pts, const dou
   }
 }
 
+// Explicit WrenchProblems (caller tangents, per-problem lambda and mu) with
+// optional warm starts: run_solver (wrench.cpp:179-228) per thread.
+__global__ void k_wrench_problems(int m, const int* n, const double* pts, const double* nrm,
+                                  const double* tx, const double* ty, const double* lambda,
+                                  const double* mu, int mode, WOpts o, const int* use_warm,
+                                  const double* warm, double* obj, int* anchor, double* sol) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  WProb w;
+  w.n = n[t];
+  w.lambda = lambda[t];
+  w.mu = mode ? mu[t] : 0.0;
+  for (int c = 0; c < w.n; ++c) {
+    const size_t b = (size_t)t * 18 + 3 * c;
+    const V3 p = v3_load(pts + b);
+    w.p[c] = p;
+    w.nn[c] = v3_load(nrm + b);
+    w.tx[c] = v3_load(tx + b);
+    w.ty[c] = v3_load(ty + b);
+    w.cn[c] = cross(p, w.nn[c]);  // Precomp (wrench.cpp:50-64)
+    w.cx[c] = cross(p, w.tx[c]);
+    w.cy[c] = cross(p, w.ty[c]);
+  }
+  WState ws;
+  const bool wm = use_warm && use_warm[t];
+  if (wm)
+    for (int c = 0; c < kMaxC; ++c) {
+      ws.a[c] = warm[(size_t)t * 18 + c];
+      ws.bx[c] = warm[(size_t)t * 18 + 6 + c];
+      ws.by[c] = warm[(size_t)t * 18 + 12 + c];
+    }
+  WState s;
+  int an = -1;
+  Ctr ctr = {0, 0, 0, 0, 0};
+  double v = wsolve(w, o, wm ? &ws : nullptr, &an, s, ctr);
+  obj[t] = v;
+  anchor[t] = an;
+  for (int c = 0; c < kMaxC; ++c) {
+    sol[(size_t)t * 18 + c] = s.a[c];
+    sol[(size_t)t * 18 + 6 + c] = s.bx[c];
+    sol[(size_t)t * 18 + 12 + c] = s.by[c];
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int lg_wrench_problem_batch(lg_ctx* ctx, int m, const int* n, const double* points,
+                            const double* normals, const double* tangent_x,
+                            const double* tangent_y, const double* lambda_torque,
+                            const double* mu, int mode, int iterations, int warm_iterations,
+                            double step, int max_backtracks, const int* use_warm,
+                            const double* warm_alpha, const double* warm_beta_x,
+                            const double* warm_beta_y, double* objective, int* anchor,
+                            double* alpha, double* beta_x, double* beta_y) {
+  return lgc::guard([&] {
+    if (!ctx || m < 0 || (m > 0 && (!n || !points || !normals || !tangent_x || !tangent_y ||
+                                    !lambda_torque || !mu || !objective || !anchor || !alpha ||
+                                    !beta_x || !beta_y)))
+      throw std::invalid_argument("lg_wrench_problem_batch: bad argument");
+    for (int i = 0; i < m; ++i) {
+      if (n[i] < 1) throw std::invalid_argument("wrench solve: no contacts");
+      if (n[i] > kMaxC) throw std::invalid_argument("wrench solve: the device takes 1..6 contacts");
+    }
+    if (m == 0) return;
+    use_ctx(ctx);
+    cudaStream_t s = ctx->stream;
+    std::vector<double> warm;
+    if (use_warm) {
+      if (!warm_alpha || !warm_beta_x || !warm_beta_y)
+        throw std::invalid_argument("lg_wrench_problem_batch: warm arrays missing");
+      warm.assign((size_t)m * 18, 0.0);
+      for (int i = 0; i < m; ++i)
+        for (int c = 0; c < kMaxC; ++c) {
+          warm[(size_t)i * 18 + c] = warm_alpha[6 * i + c];
+          warm[(size_t)i * 18 + 6 + c] = warm_beta_x[6 * i + c];
+          warm[(size_t)i * 18 + 12 + c] = warm_beta_y[6 * i + c];
+        }
+    }
+    Buf bn, bp, bq, bx, by, bl, bm, bu, bw, bo, ba, bs;
+    int* d_n = dupload(bn, n, (size_t)m, s);
+    double* d_p = dupload(bp, points, (size_t)m * 18, s);
+    double* d_q = dupload(bq, normals, (size_t)m * 18, s);
+    double* d_x = dupload(bx, tangent_x, (size_t)m * 18, s);
+    double* d_y = dupload(by, tangent_y, (size_t)m * 18, s);
+    double* d_l = dupload(bl, lambda_torque, (size_t)m, s);
+    double* d_m = dupload(bm, mu, (size_t)m, s);
+    int* d_u = use_warm ? dupload(bu, use_warm, (size_t)m, s) : nullptr;
+    double* d_w = use_warm ? dupload(bw, warm.data(), warm.size(), s) : nullptr;
+    double* d_o = dalloc<double>(bo, (size_t)m);
+    int* d_a = dalloc<int>(ba, (size_t)m);
+    double* d_s = dalloc<double>(bs, (size_t)m * 18);
+    WOpts o;
+    o.iterations = iterations;
+    o.warm_iterations = warm_iterations;
+    o.step = step;
+    o.max_bt = max_backtracks;
+    k_wrench_problems<<<grid_for(m, 64), 64, 0, s>>>(m, d_n, d_p, d_q, d_x, d_y, d_l, d_m, mode, o,
+                                                     d_u, d_w, d_o, d_a, d_s);
+    LAUNCH(ctx);
+    check_launch();
+    auto h_s = ddownload(d_s, (size_t)m * 18, s);
+    auto h_o = ddownload(d_o, (size_t)m, s);
+    auto h_a = ddownload(d_a, (size_t)m, s);
+    for (int i = 0; i < m; ++i) {
+      objective[i] = h_o[i];
+      anchor[i] = h_a[i];
+      for (int c = 0; c < kMaxC; ++c) {
+        alpha[6 * i + c] = h_s[18 * i + c];
+        beta_x[6 * i + c] = h_s[18 * i + 6 + c];
+        beta_y[6 * i + c] = h_s[18 * i + 12 + c];
+      }
+    }
+  });
+}
 
 int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points,
                           const double* normals, double lambda, double mu, int mode,
@@ -1443,8 +1556,9 @@ int lg_wrench_solve_batch(lg_ctx* ctx, int m, const int* n, const double* points
     k_wrench_batch<<<grid_for(m, 64), 64, 0, s>>>(m, d_n, d_p, d_q, lambda, mu, mode, o, d_o, d_a, d_s);
     check_launch();
     auto h_s = ddownload(d_s, (size_t)m * 18, s);
-    CK(cudaMemcpy(objective, d_o, sizeof(double) * m, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(anchor, d_a, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(objective, d_o, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(anchor, d_a, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     for (int i = 0; i < m; ++i)
       for (int c = 0; c < kMaxC; ++c) {
         alpha[6 * i + c] = h_s[18 * i + c];
@@ -1777,9 +1891,10 @@ int lg_realize_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const int* k,
     auto hq = ddownload(d_q, q0.size(), s);
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < hand->dof; ++j) q[(size_t)i * hand->dof + j] = hq[(size_t)i * kMaxDof + j];
-    CK(cudaMemcpy(max_residual, d_r, sizeof(double) * m, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(finite, d_f, sizeof(int) * m, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(used_joints, d_u, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(max_residual, d_r, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(finite, d_f, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(used_joints, d_u, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   });
 }
 

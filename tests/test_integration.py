@@ -28,7 +28,7 @@ def _run(exe, *args, timeout=900):
     return out
 
 
-@pytest.mark.parametrize("suite", ["contact_opt", "collision", "ik", "contact_field"])
+@pytest.mark.parametrize("suite", ["contact_opt", "collision", "ik", "contact_field", "wrench"])
 def test_reference_catch2_suite_on_the_device(suite):
     out = _run(f"test_{suite}_b200")
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
