@@ -12,6 +12,7 @@
 //   query_domains             (contact_field.hpp:147-150, contact_field.cpp:380-448)
 //   reverse_lookup            (contact_field.hpp:154-156, contact_field.cpp:450-484)
 //   solve_fswo / solve_gswo / is_stable (wrench.hpp:56-77, wrench.cpp:179-267)
+//   validate_dataset          (validate.hpp:26-29, validate.cpp:56-175)
 //
 // Everything the reference keeps on the host stays the reference's code:
 // parse_config, load_hand (URDF + quickhull parts), load_mesh,
@@ -51,6 +52,7 @@
 #include "graspgen/mesh.hpp"
 #include "graspgen/pipeline.hpp"
 #include "graspgen/rng.hpp"
+#include "graspgen/validate.hpp"
 #include "graspgen/wrench.hpp"
 #include "lg.h"
 
@@ -566,6 +568,71 @@ bool is_stable(const WrenchProblem& problem, double eps, WrenchSolution* solutio
   const bool stable = s.objective < eps;
   if (solution) *solution = std::move(s);
   return stable;
+}
+
+// validate_dataset (validate.cpp:56-175): the object samples are the
+// reference's sample_surface (stream 'objs', as validate.cpp:63-65 re-draws
+// them); every check runs on the device and the issue texts come from
+// lg_validation_issues.
+ValidationReport validate_dataset(const GraspDataset& dataset, const HandModel& model,
+                                  const TriMesh& object, const RunConfig& config) {
+  ValidationReport report;
+  report.checked = static_cast<long>(dataset.grasps.size());
+  if (dataset.grasps.empty()) return report;
+  FlatHand hand(model);
+  std::vector<lg_grasp> gs(dataset.grasps.size());
+  for (std::size_t i = 0; i < gs.size(); ++i) {
+    const Grasp& g = dataset.grasps[i];
+    lg_grasp& o = gs[i];
+    std::memset(&o, 0, sizeof o);
+    o.g = static_cast<long long>(i);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) o.pose_R[3 * r + c] = g.object_pose.rotation(r, c);
+    put3(o.pose_t, g.object_pose.translation);
+    o.dof = static_cast<int>(g.q.size());
+    for (int j = 0; j < o.dof && j < LG_MAX_DOF; ++j) o.q[j] = g.q[j];
+    if (g.contacts.size() > LG_MAX_CONTACTS)
+      throw std::invalid_argument("validate_dataset: the device checks at most 6 contacts per grasp");
+    o.n_contacts = static_cast<int>(g.contacts.size());
+    for (int c = 0; c < o.n_contacts; ++c) {
+      put3(o.contact_p[c], g.contacts[c].position);
+      put3(o.contact_n[c], g.contacts[c].normal);
+      o.contact_link[c] = g.contacts[c].link;
+    }
+    o.objective = g.objective;
+  }
+  std::vector<double> verts;
+  std::vector<int> tris;
+  for (const Vec3& v : object.vertices) verts.insert(verts.end(), {v.x(), v.y(), v.z()});
+  for (const auto& t : object.triangles) tris.insert(tris.end(), {t[0], t[1], t[2]});
+  auto samples = flat_samples(sample_surface(object, config.samples_per_cm2,
+                                             mix_seed(config.seed, kTagObjectSamples)));
+  const lg_run_params p = params_of(config);
+  std::vector<lg_grasp_check> checks(gs.size());
+  check(lg_validate_batch(context(), &hand.d, gs.data(), static_cast<long long>(gs.size()),
+                          verts.data(), static_cast<int>(object.vertices.size()), tris.data(),
+                          static_cast<int>(object.triangles.size()), samples.data(),
+                          static_cast<int>(samples.size() / 6), &p, checks.data()));
+  std::vector<const char*> names;
+  for (const Link& l : model.links) names.push_back(l.joint_name.c_str());
+  std::size_t need = 0;
+  long long n_issues = 0;
+  check(lg_validation_issues(names.data(), static_cast<int>(names.size()), checks.data(),
+                             static_cast<long long>(checks.size()), &p, nullptr, 0, &need,
+                             &n_issues));
+  std::vector<char> buf(need + 1, '\0');
+  check(lg_validation_issues(names.data(), static_cast<int>(names.size()), checks.data(),
+                             static_cast<long long>(checks.size()), &p, buf.data(), buf.size(),
+                             &need, &n_issues));
+  const std::string text(buf.data());
+  std::size_t pos = 0;
+  while (pos < text.size()) {
+    const std::size_t eol = text.find('\n', pos), tab = text.find('\t', pos);
+    if (eol == std::string::npos || tab == std::string::npos || tab > eol) break;
+    report.issues.push_back({std::stol(text.substr(pos, tab - pos)), text.substr(tab + 1, eol - tab - 1)});
+    pos = eol + 1;
+  }
+  return report;
 }
 
 // solve_contact_ik (ik.cpp:30-139) on the device.  The device returns each
