@@ -122,6 +122,16 @@ void orc_glibc(int which, long long n, const double* x, const double* y, double*
   }
 }
 
+// lgl::hypot_exceeds (the friction-disc test of wrench.cpp:96-104 without
+// evaluating hypot when a bound settles it): out[i] = hypot(x, y) > cap.
+void orc_hypot_exceeds(long long n, const double* x, const double* y, const double* cap,
+                       unsigned char* out) {
+  for (long long i = 0; i < n; ++i) {
+    double r = 0.0;
+    out[i] = lgl::hypot_exceeds(x[i], y[i], cap[i], &r) ? 1 : 0;
+  }
+}
+
 // random_problem of test_wrench.cpp:13-25 (fixture generator): points on a
 // 5 cm sphere, roughly inward unit normals.
 void orc_random_wrench_problem(uint64_t seed, int n, double* pts, double* nrm) {

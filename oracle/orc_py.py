@@ -166,6 +166,14 @@ def glibc(which, x, y=None):
     return out
 
 
+def hypot_exceeds(x, y, cap):
+    x, y, cap = _d(x), _d(y), _d(cap)
+    out = np.zeros(len(x), dtype=np.uint8)
+    lib().orc_hypot_exceeds(C.c_longlong(len(x)), _p(x), _p(y), _p(cap),
+                            out.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return out.astype(bool)
+
+
 def mix_seed(s, a, b=0):
     return int(lib().orc_mix_seed(C.c_uint64(s), C.c_uint64(a), C.c_uint64(b)))
 

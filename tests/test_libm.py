@@ -69,3 +69,21 @@ def test_device_libm_is_glibc_bit_for_bit(ctx, fn):
     ref = orc.glibc(fn, x, y)
     bad = np.flatnonzero(got.view(np.int64) != ref.view(np.int64))
     assert bad.size == 0, (fn, bad.size, x[bad[:3]], got[bad[:3]], ref[bad[:3]])
+
+
+def test_hypot_exceeds_is_glibc_hypot_gt_cap():
+    """The friction-disc test hypot(x, y) > cap (wrench.cpp:96-104) decided
+    through the squared-norm bound == glibc's hypot compared with cap, on
+    random pairs and caps placed at, one ulp around and 2^-44 around the
+    glibc value (where the bound must defer to the exact hypot)."""
+    rng = np.random.default_rng(11)
+    n = 400_000
+    x = rng.normal(size=n) * 10.0 ** rng.uniform(-6, 2, size=n)
+    y = rng.normal(size=n) * 10.0 ** rng.uniform(-6, 2, size=n)
+    h = orc.glibc("hypot", x, y)
+    pick = rng.integers(0, 7, size=n)
+    cap = np.select([pick == 0, pick == 1, pick == 2, pick == 3, pick == 4, pick == 5],
+                    [h, np.nextafter(h, 0), np.nextafter(h, np.inf), h * (1 + 2 ** -44),
+                     h * (1 - 2 ** -44), h * rng.uniform(0.5, 2, size=n)], h * 0.0)
+    got = orc.hypot_exceeds(x, y, cap)
+    assert np.array_equal(got, h > cap)
