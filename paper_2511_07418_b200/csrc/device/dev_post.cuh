@@ -188,6 +188,43 @@ k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, c
   }
 }
 
+// Stable compaction of the kept grasp records (candidate order preserved),
+// one CTA of 1024 threads: per 1024-record tile each warp ballots its flags,
+// warp totals are scanned in shared memory, and every kept record is copied
+// to its rank.  n_out receives the count.
+__global__ void __launch_bounds__(1024) k_compact_grasps(int n, const lg_grasp* in,
+                                                         const uint8_t* keep, lg_grasp* out,
+                                                         int* n_out) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int tile = 0; tile < n; tile += 1024) {
+    const int i = tile + threadIdx.x;
+    const bool f = i < n && keep[i];
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_warp[wid] = __popc(b);
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the 32 warp counts
+      const int c = s_warp[lane];
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      s_warp[lane] = incl - c;
+    }
+    __syncthreads();
+    if (f) out[s_base + s_warp[wid] + __popc(b & ((1u << lane) - 1u))] = in[i];
+    __syncthreads();
+    if (threadIdx.x == 1023) s_base += s_warp[31] + __popc(b);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_out = s_base;
+}
+
 // Funnel counts over the realised candidates (records of the others are
 // zero) and the kept-grasp flags (valid, not dropped) for the compaction.
 __global__ void k_grasp_flags(int nA, const lg_grasp* g, const int* valid, const int* drop,

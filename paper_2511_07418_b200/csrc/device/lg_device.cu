@@ -1060,6 +1060,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     if (first_on_device(2)) {
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CK(cudaFuncSetAttribute(k_contact_opt2<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       // shared-memory carve-out (percent): less shared memory leaves more L1
       // for the domain scans, at the cost of resident CTAs
@@ -1072,9 +1073,14 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     }
     tk.start();
     // k contacts + at most one static
-    auto co_kern = k + 1 <= 3 ? (co_minb == 5 ? k_contact_opt2<3, 5> : k_contact_opt2<3, 4>)
-                              : k_contact_opt2<kMaxC, 4>;
-    size_t co_smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
+    // (the per-lane shared records scale with NC: NC = 4 fits three CTAs per
+    // SM where NC = 6 fits two)
+    auto co_kern = k + 1 <= 3   ? (co_minb == 5 ? k_contact_opt2<3, 5> : k_contact_opt2<3, 4>)
+                   : k + 1 <= 4 ? k_contact_opt2<4, 4>
+                                : k_contact_opt2<kMaxC, 4>;
+    size_t co_smem = k + 1 <= 3   ? copt2_smem<3>(k, nw)
+                     : k + 1 <= 4 ? copt2_smem<4>(k, nw)
+                                  : copt2_smem<kMaxC>(k, nw);
     co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln,
                                          dom, d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
                                          d_bal);
@@ -1310,11 +1316,9 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       check_launch();
       lg_grasp* d_sel = dalloc<lg_grasp>(b_sel, (size_t)nA);
       int* d_nsel = dalloc<int>(b_nsel, 1);
-      size_t bytes = 0;
-      CK(cub::DeviceSelect::Flagged(nullptr, bytes, d_grasp, d_keep8, d_sel, d_nsel, nA, s));
-      void* tmp = ctx->tmp(bytes);
-      CK(cub::DeviceSelect::Flagged(tmp, bytes, d_grasp, d_keep8, d_sel, d_nsel, nA, s));
+      k_compact_grasps<<<1, 1024, 0, s>>>(nA, d_grasp, d_keep8, d_sel, d_nsel);
       LAUNCH(ctx);
+      check_launch();
       int counts[4];
       CK(cudaMemcpyAsync(counts, d_fl, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(counts + 3, d_nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2956,9 +2960,12 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
     co.per_cand = per_cand;
     const int nw = std::min(R, 4);
     CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_contact_opt2<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    auto kern = k + 1 <= 3 ? k_contact_opt2<3, 4> : k_contact_opt2<kMaxC, 4>;
-    size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw) : copt2_smem<kMaxC>(k, nw);
+    auto kern = k + 1 <= 3 ? k_contact_opt2<3, 4>
+                : k + 1 <= 4 ? k_contact_opt2<4, 4> : k_contact_opt2<kMaxC, 4>;
+    size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw)
+                  : k + 1 <= 4 ? copt2_smem<4>(k, nw) : copt2_smem<kMaxC>(k, nw);
     DomIdx dom{};
     kern<<<m, 32 * nw, smem, s>>>(m, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, dom,
                                   d_draws, d_oid, d_oobj, d_oan, d_osol, kInf, d_bal);
