@@ -225,7 +225,7 @@ __device__ __forceinline__ uint32_t morton_spread10(uint32_t v) {
 // Morton keys of the domain elements, quantised inside the candidate's posed
 // object box (k_obj_aabb); value = element index within the domain.
 __global__ void k_dom_keys(int nA, int k, const int* alive_idx, const double* aabb,
-                           const long long* el_off, const double* el_p, uint32_t* keys, int* vals) {
+                           const long long* el_off, ElemSrc el, uint32_t* keys, int* vals) {
   const int seg = blockIdx.x;
   if (seg >= nA * k) return;
   const int i = alive_idx[seg / k];
@@ -238,8 +238,10 @@ __global__ void k_dom_keys(int nA, int k, const int* alive_idx, const double* aa
   }
   for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
     uint32_t q[3];
+    const V3 pt = el.pos(t, seg / k);
+    const double pc[3] = {pt.x, pt.y, pt.z};
     for (int c = 0; c < 3; ++c) {
-      double v = (el_p[3 * t + c] - lo[c]) * sc[c];
+      double v = (pc[c] - lo[c]) * sc[c];
       v = v < 0.0 ? 0.0 : (v > 1023.0 ? 1023.0 : v);
       q[c] = (uint32_t)v;
     }
@@ -303,7 +305,7 @@ __global__ void k_dom_chunk_count(int nseg, const long long* el_off, const uint3
 // super-chunk boxes (block per domain).
 __global__ void k_dom_chunks(int nseg, const long long* el_off, const long long* ch_off,
                              const long long* su_off, const uint32_t* keys_sorted,
-                             const int* vals_sorted, const double* el_p, DomIdx d) {
+                             const int* vals_sorted, ElemSrc el, int k, DomIdx d) {
   const int seg = blockIdx.x;
   if (seg >= nseg) return;
   double* sx = const_cast<double*>(d.sx);
@@ -320,10 +322,10 @@ __global__ void k_dom_chunks(int nseg, const long long* el_off, const long long*
   dom_chunk_heads(keys_sorted + b, ne, [&](int c, int t) { cs[c0 + c] = t; });
   for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
     const int o = vals_sorted[t];
-    const long long src = b + o;
-    sx[t] = el_p[3 * src];
-    sy[t] = el_p[3 * src + 1];
-    sz[t] = el_p[3 * src + 2];
+    const V3 pt = el.pos(b + o, seg / k);
+    sx[t] = pt.x;
+    sy[t] = pt.y;
+    sz[t] = pt.z;
     si[t] = o;
   }
   __syncthreads();
@@ -550,7 +552,7 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
 template <int NC, int MINB>
 __global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
-               const double* st_n, const long long* el_off, const double* el_p, const double* el_n,
+               const double* st_n, const long long* el_off, ElemSrc el,
                DomIdx dom, const uint64_t* draws, int* out_ids, double* out_obj, int* out_anchor,
                double* out_sol, double eps_stable, int* balanced) {
   extern __shared__ __align__(16) double s_co[];
@@ -587,7 +589,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       for (int q = 0; q < k; ++q) ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
       if (lane < k) {
         long long e = off[lane] + ids[lane];
-        slot_make(sp + kSlot * lane, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+        slot_make(sp + kSlot * lane, el.pos(e, a), neg(el.nrm(e, a)));
       } else if (lane == k && s) {
         slot_make(sp + kSlot * k, v3_load(st_p + 3 * i), v3_load(st_n + 3 * i));
       }
@@ -645,13 +647,16 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             const int ne = (int)cnt[q];
             double bd;
             int bi;
-            if (dom.sx && ne >= kCoopMin) {
+            // with the sorted copies present (large domains), every domain
+            // of the launch takes the cooperative search: the plain scan
+            // reads the materialised positions, which large runs skip
+            if (dom.sx) {
               unsigned long long evals = 0;
               bi = project_coop(dom, (long long)a * k + q, off[q], ne, cp, act, ids[q], cur_p, lane,
                                 evals);
               if (act) ctr.proj += evals;
             } else if (act) {
-                const double* P = el_p + 3 * off[q];
+                const double* P = el.p + 3 * off[q];
                 // Every lane scans the same elements (broadcast loads, no
                 // divergence): faster than the pruned search for domains of
                 // a few thousand elements.
@@ -714,7 +719,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             if (act) {
               cand = bi;
               const long long eg = off[q] + bi;
-              slot_make(tslot, v3_load(el_p + 3 * eg), neg(v3_load(el_n + 3 * eg)));
+              slot_make(tslot, el.pos(eg, a), neg(el.nrm(eg, a)));
               PV tw = w;
               tw.tq = q;
               // warm solve over all anchors in this lane (run_solver)
@@ -756,7 +761,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             ids[q] = best_id;
             if (lane == 0) {
               long long e = off[q] + best_id;
-              slot_make(sp + kSlot * q, v3_load(el_p + 3 * e), neg(v3_load(el_n + 3 * e)));
+              slot_make(sp + kSlot * q, el.pos(e, a), neg(el.nrm(e, a)));
             }
             if (lane < 3 * NC) inc[lane] = win[lane];
             __syncwarp();

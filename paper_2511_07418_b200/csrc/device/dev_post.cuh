@@ -243,8 +243,8 @@ __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int 
                               int Bsz, int pass, uint64_t seed, DField f,
                               const int* group_of_patch, const double* patch_pts,
                               const double* patch_nrm, const int* patch_link, const int* chosen,
-                              const int* opt_ids, const long long* el_off, const double* el_p,
-                              const double* el_n, double theta, double* tgt, int* tgt_link,
+                              const int* opt_ids, const long long* el_off, ElemSrc el,
+                              double theta, double* tgt, int* tgt_link,
                               int* err) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)nB * A * k) return;
@@ -255,7 +255,7 @@ __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int 
   int i = alive_idx[a];
   int g = chosen[i * kMaxK + slot];
   long long e = el_off[a * k + slot] + opt_ids[a * kMaxK + slot];
-  V3 p = v3_load(el_p + 3 * e), n = v3_load(el_n + 3 * e);
+  V3 p = el.pos(e, a), n = el.nrm(e, a);
   int nh = 0;
   sample_hits(f, f.codebook, p, n, theta, [&](int patch, int, double) {
     if (group_of_patch[patch] == g) ++nh;

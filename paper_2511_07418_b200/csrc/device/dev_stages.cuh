@@ -554,6 +554,27 @@ __global__ void k_group_pick(int Bl, int c_lo, int B, int pass, uint64_t seed, i
   alive[i] = 1;
 }
 
+// Domain element data: the materialised arrays (p, n: [e][3]), or — for
+// large domains, which skip them — recomputed from the element's sample id
+// and the candidate's pose with k_domain_fill's own arithmetic (the same
+// bits).  a = alive index of the element's candidate.
+struct ElemSrc {
+  const double* p;
+  const double* n;
+  const int* s;
+  DSamples fs;
+  const double* pose;
+  const int* alive_idx;
+  __device__ __forceinline__ V3 pos(long long e, int a) const {
+    if (p) return v3_load(p + 3 * e);
+    return xf_apply(load_xf(pose + 12 * alive_idx[a]), fs.p(s[e]));
+  }
+  __device__ __forceinline__ V3 nrm(long long e, int a) const {
+    if (n) return v3_load(n + 3 * e);
+    return xf_rotate(load_xf(pose + 12 * alive_idx[a]), fs.nrm(s[e]));
+  }
+};
+
 // ------------------------------------------------- chosen domain elements
 // Elements of domain (a, slot) in sample order: block per (a, slot), block
 // scan over the mask row.  Writes sample id, position and normal (SoA).
@@ -580,14 +601,16 @@ __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* ch
     if (flag) {
       long long e = off + s_base + pos;
       el_s[e] = j;
-      V3 p = xf_apply(x, fs.p(j));
-      V3 n = xf_rotate(x, fs.nrm(j));
-      el_p[3 * e] = p.x;
-      el_p[3 * e + 1] = p.y;
-      el_p[3 * e + 2] = p.z;
-      el_n[3 * e] = n.x;
-      el_n[3 * e + 1] = n.y;
-      el_n[3 * e + 2] = n.z;
+      if (el_p) {  // large domains keep the sample ids only (ElemSrc)
+        V3 p = xf_apply(x, fs.p(j));
+        V3 n = xf_rotate(x, fs.nrm(j));
+        el_p[3 * e] = p.x;
+        el_p[3 * e + 1] = p.y;
+        el_p[3 * e + 2] = p.z;
+        el_n[3 * e] = n.x;
+        el_n[3 * e + 1] = n.y;
+        el_n[3 * e + 2] = n.z;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) s_base += total;

@@ -957,30 +957,35 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       }
     const long long nel = eloff.back();
     long long* d_eloff = dupload(b_eloff, eloff.data(), eloff.size(), s);
-    int* d_els = dalloc<int>(b_els, (size_t)nel);
-    double* d_elp = dalloc<double>(b_elp, 3 * (size_t)nel);
-    double* d_eln = dalloc<double>(b_eln, 3 * (size_t)nel);
-    k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
-                                         d_elp, d_eln);
-    LAUNCH(ctx);
-    check_launch();
-    // Morton-ordered copy of every domain + chunk boxes for the exact pruned
-    // projection (dev_copt.cuh DomIdx); LG_PROJ=brute keeps the plain scan.
+    // Large domains take the cooperative search over Morton-ordered copies
+    // (dev_copt.cuh DomIdx; LG_PROJ=brute keeps the plain scan) and keep
+    // only their sample ids: positions and normals are recomputed from the
+    // sample and the pose where needed (ElemSrc), which saves writing and
+    // re-reading 48 bytes per element.
     static const bool proj_brute = [] {
       const char* e = std::getenv("LG_PROJ");
       return e && std::string(e) == "brute";
     }();
-    Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff, b_cs, b_nch;
-    DomIdx dom{};
     long long max_dom = 0;
     for (size_t t = 0; t + 1 < eloff.size(); ++t) max_dom = std::max(max_dom, eloff[t + 1] - eloff[t]);
-    if (!proj_brute && max_dom >= kCoopMin) {
+    const bool large = !proj_brute && max_dom >= kCoopMin;
+    int* d_els = dalloc<int>(b_els, (size_t)nel);
+    double* d_elp = large ? nullptr : dalloc<double>(b_elp, 3 * (size_t)nel);
+    double* d_eln = large ? nullptr : dalloc<double>(b_eln, 3 * (size_t)nel);
+    k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
+                                         d_elp, d_eln);
+    LAUNCH(ctx);
+    check_launch();
+    ElemSrc els{d_elp, d_eln, d_els, FS, d_pose, d_aidx};
+    Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff, b_cs, b_nch;
+    DomIdx dom{};
+    if (large) {
       const int nseg = nA * k;
       uint32_t* d_k = dalloc<uint32_t>(b_keys, (size_t)nel);
       uint32_t* d_k2 = dalloc<uint32_t>(b_keys2, (size_t)nel);
       int* d_v = dalloc<int>(b_vals, (size_t)nel);
       int* d_v2 = dalloc<int>(b_vals2, (size_t)nel);
-      k_dom_keys<<<nseg, 256, 0, s>>>(nA, k, d_aidx, d_aabb, d_eloff, d_elp, d_k, d_v);
+      k_dom_keys<<<nseg, 256, 0, s>>>(nA, k, d_aidx, d_aabb, d_eloff, els, d_k, d_v);
       LAUNCH(ctx);
       check_launch();
       size_t tb = 0;
@@ -1018,7 +1023,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       dom.sstride = ss;
       dom.choff = d_choff;
       dom.suoff = d_suoff;
-      k_dom_chunks<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_choff, d_suoff, d_k2, d_v2, d_elp, dom);
+      k_dom_chunks<<<nseg, 256, 0, s>>>(nseg, d_eloff, d_choff, d_suoff, d_k2, d_v2, els, k, dom);
       LAUNCH(ctx);
       check_launch();
     }
@@ -1081,8 +1086,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     size_t co_smem = k + 1 <= 3   ? copt2_smem<3>(k, nw)
                      : k + 1 <= 4 ? copt2_smem<4>(k, nw)
                                   : copt2_smem<kMaxC>(k, nw);
-    co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln,
-                                         dom, d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
+    co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, els, dom, d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
                                          d_bal);
     LAUNCH(ctx);
     check_launch();
@@ -1148,7 +1152,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_tl = dalloc<int>(b_tl, (size_t)nP * k);
       k_targets_all<<<grid_for(nP * k, 128), 128, 0, s>>>(
           nB, d_bl, d_aidx, k, LA, c_lo, B, pass, cfg.seed, F, d_gop, DP.pts.as<double>(),
-          DP.nrm.as<double>(), DP.link.as<int>(), d_chosen, d_oid, d_eloff, d_elp, d_eln,
+          DP.nrm.as<double>(), DP.link.as<int>(), d_chosen, d_oid, d_eloff, els,
           cfg.theta_hit, d_tgt, d_tl, d_err);
       LAUNCH(ctx);
       check_launch();
@@ -2967,7 +2971,8 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
     size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw)
                   : k + 1 <= 4 ? copt2_smem<4>(k, nw) : copt2_smem<kMaxC>(k, nw);
     DomIdx dom{};
-    kern<<<m, 32 * nw, smem, s>>>(m, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, d_elp, d_eln, dom,
+    ElemSrc els{d_elp, d_eln, nullptr, DSamples{}, nullptr, nullptr};
+    kern<<<m, 32 * nw, smem, s>>>(m, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, els, dom,
                                   d_draws, d_oid, d_oobj, d_oan, d_osol, kInf, d_bal);
     check_launch();
     LAUNCH(ctx);
