@@ -238,7 +238,7 @@ __global__ void k_dom_keys(int nA, int k, const int* alive_idx, const double* aa
   }
   for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
     uint32_t q[3];
-    const V3 pt = el.pos(t, seg / k);
+    const V3 pt = el.pos(t, seg / k, el.big(e - b));
     const double pc[3] = {pt.x, pt.y, pt.z};
     for (int c = 0; c < 3; ++c) {
       double v = (pc[c] - lo[c]) * sc[c];
@@ -322,7 +322,7 @@ __global__ void k_dom_chunks(int nseg, const long long* el_off, const long long*
   dom_chunk_heads(keys_sorted + b, ne, [&](int c, int t) { cs[c0 + c] = t; });
   for (long long t = b + threadIdx.x; t < e; t += blockDim.x) {
     const int o = vals_sorted[t];
-    const V3 pt = el.pos(b + o, seg / k);
+    const V3 pt = el.pos(b + o, seg / k, el.big(e - b));
     sx[t] = pt.x;
     sy[t] = pt.y;
     sz[t] = pt.z;
@@ -589,7 +589,8 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       for (int q = 0; q < k; ++q) ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
       if (lane < k) {
         long long e = off[lane] + ids[lane];
-        slot_make(sp + kSlot * lane, el.pos(e, a), neg(el.nrm(e, a)));
+        const bool bg = el.big(cnt[lane]);
+        slot_make(sp + kSlot * lane, el.pos(e, a, bg), neg(el.nrm(e, a, bg)));
       } else if (lane == k && s) {
         slot_make(sp + kSlot * k, v3_load(st_p + 3 * i), v3_load(st_n + 3 * i));
       }
@@ -647,10 +648,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             const int ne = (int)cnt[q];
             double bd;
             int bi;
-            // with the sorted copies present (large domains), every domain
-            // of the launch takes the cooperative search: the plain scan
-            // reads the materialised positions, which large runs skip
-            if (dom.sx) {
+            if (dom.sx && ne >= kCoopMin) {
               unsigned long long evals = 0;
               bi = project_coop(dom, (long long)a * k + q, off[q], ne, cp, act, ids[q], cur_p, lane,
                                 evals);
@@ -719,7 +717,8 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             if (act) {
               cand = bi;
               const long long eg = off[q] + bi;
-              slot_make(tslot, el.pos(eg, a), neg(el.nrm(eg, a)));
+              const bool bg = el.big(cnt[q]);
+              slot_make(tslot, el.pos(eg, a, bg), neg(el.nrm(eg, a, bg)));
               PV tw = w;
               tw.tq = q;
               // warm solve over all anchors in this lane (run_solver)
@@ -761,7 +760,8 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             ids[q] = best_id;
             if (lane == 0) {
               long long e = off[q] + best_id;
-              slot_make(sp + kSlot * q, el.pos(e, a), neg(el.nrm(e, a)));
+              const bool bg = el.big(cnt[q]);
+              slot_make(sp + kSlot * q, el.pos(e, a, bg), neg(el.nrm(e, a, bg)));
             }
             if (lane < 3 * NC) inc[lane] = win[lane];
             __syncwarp();

@@ -255,7 +255,8 @@ __global__ void k_targets_all(int nB, const int* bal, const int* alive_idx, int 
   int i = alive_idx[a];
   int g = chosen[i * kMaxK + slot];
   long long e = el_off[a * k + slot] + opt_ids[a * kMaxK + slot];
-  V3 p = el.pos(e, a), n = el.nrm(e, a);
+  const bool bg = el.big(el_off[a * k + slot + 1] - el_off[a * k + slot]);
+  V3 p = el.pos(e, a, bg), n = el.nrm(e, a, bg);
   int nh = 0;
   sample_hits(f, f.codebook, p, n, theta, [&](int patch, int, double) {
     if (group_of_patch[patch] == g) ++nh;

@@ -565,12 +565,14 @@ struct ElemSrc {
   DSamples fs;
   const double* pose;
   const int* alive_idx;
-  __device__ __forceinline__ V3 pos(long long e, int a) const {
-    if (p) return v3_load(p + 3 * e);
+  long long big_min;  // domains of at least this many elements are not materialised
+  __device__ __forceinline__ bool big(long long count) const { return count >= big_min; }
+  __device__ __forceinline__ V3 pos(long long e, int a, bool bg) const {
+    if (!bg) return v3_load(p + 3 * e);
     return xf_apply(load_xf(pose + 12 * alive_idx[a]), fs.p(s[e]));
   }
-  __device__ __forceinline__ V3 nrm(long long e, int a) const {
-    if (n) return v3_load(n + 3 * e);
+  __device__ __forceinline__ V3 nrm(long long e, int a, bool bg) const {
+    if (!bg) return v3_load(n + 3 * e);
     return xf_rotate(load_xf(pose + 12 * alive_idx[a]), fs.nrm(s[e]));
   }
 };
@@ -580,7 +582,8 @@ struct ElemSrc {
 // scan over the mask row.  Writes sample id, position and normal (SoA).
 __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* chosen,
                               const uint32_t* mask, DSamples fs, const double* pose,
-                              const long long* el_off, int* el_s, double* el_p, double* el_n) {
+                              const long long* el_off, int* el_s, double* el_p, double* el_n,
+                              long long big_min) {
   typedef cub::BlockScan<int, 256> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
@@ -591,6 +594,8 @@ __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* ch
   const uint32_t* m = mask + (size_t)i * fs.n;
   Xf x = load_xf(pose + 12 * i);
   long long off = el_off[a * k + slot];
+  // large domains keep the sample ids only (ElemSrc)
+  const bool mat = el_off[a * k + slot + 1] - off < big_min;
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
   for (int base = 0; base < fs.n; base += 256) {
@@ -601,7 +606,7 @@ __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* ch
     if (flag) {
       long long e = off + s_base + pos;
       el_s[e] = j;
-      if (el_p) {  // large domains keep the sample ids only (ElemSrc)
+      if (mat) {
         V3 p = xf_apply(x, fs.p(j));
         V3 n = xf_rotate(x, fs.nrm(j));
         el_p[3 * e] = p.x;
@@ -633,6 +638,83 @@ __global__ void k_copt_draws(int nA, const int* alive_idx, int c_lo, int B, int 
   mt_seed(g, mix_seed(seed, kTagContactOpt, gid));
   uint64_t* o = out + (size_t)a * per_cand;
   for (long long d = 0; d < per_cand; ++d) o[d] = mt_next(g);
+}
+
+// The same stream with one warp per candidate: the MT19937-64 state lives in
+// shared memory and each 312-draw block is produced by the block twist in
+// two parallel halves (entries i < 156 read only old words; entries
+// i >= 156 read old words and the new word i - 156, and entry 311 the new
+// word 0: exactly what the element-by-element twist of mt_next reads), then
+// tempered and written by all lanes.  The Box-Muller pairs of every restart
+// are then turned into the tangent-plane offsets in the same launch (the
+// candidate's draws are still in L2): k_copt_draws + k_copt_normals fused.
+constexpr int kDrawWarps = 4;
+__global__ void __launch_bounds__(32 * kDrawWarps)
+k_copt_draws_warp(int nA, const int* alive_idx, int c_lo, int B, int pass, uint64_t seed,
+                  long long per_cand, long long per_restart, int k, int prp, double sigma,
+                  uint64_t* out) {
+  __shared__ uint64_t s_mt[kDrawWarps][312];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int a = blockIdx.x * kDrawWarps + w;
+  if (a >= nA) return;  // warp-uniform
+  uint64_t* mt = s_mt[w];
+  const int i = alive_idx[a];
+  if (lane == 0) {
+    const uint64_t gid = (uint64_t)pass * B + (uint64_t)(c_lo + i);
+    mt[0] = mix_seed(seed, kTagContactOpt, gid);
+    for (int t = 1; t < 312; ++t) mt[t] = 6364136223846793005ull * (mt[t - 1] ^ (mt[t - 1] >> 62)) + (uint64_t)t;
+  }
+  __syncwarp();
+  const uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull, MA = 0xB5026F5AA96619E9ull;
+  uint64_t* o = out + (size_t)a * per_cand;
+  for (long long b0 = 0; b0 < per_cand; b0 += 312) {
+    uint64_t nv[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {  // entries 0..155
+      const int e = lane + 32 * t;
+      if (e < 156) {
+        const uint64_t y = (mt[e] & UM) | (mt[e + 1] & LM);
+        nv[t] = mt[e + 156] ^ (y >> 1) ^ ((y & 1ull) ? MA : 0ull);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+      if (lane + 32 * t < 156) mt[lane + 32 * t] = nv[t];
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {  // entries 156..311
+      const int e = 156 + lane + 32 * t;
+      if (e < 312) {
+        const uint64_t y = (mt[e] & UM) | (mt[e + 1 == 312 ? 0 : e + 1] & LM);
+        nv[t] = mt[e - 156] ^ (y >> 1) ^ ((y & 1ull) ? MA : 0ull);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+      if (156 + lane + 32 * t < 312) mt[156 + lane + 32 * t] = nv[t];
+    __syncwarp();
+    for (int e = lane; e < 312 && b0 + e < per_cand; e += 32) {
+      uint64_t z = mt[e];
+      z ^= (z >> 29) & 0x5555555555555555ull;
+      z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+      z ^= (z << 37) & 0xFFF7EEE000000000ull;
+      z ^= (z >> 43);
+      o[b0 + e] = z;
+    }
+  }
+  __syncwarp();
+  const long long np = (per_cand / per_restart) * (long long)prp;
+  for (long long t = lane; t < np; t += 32) {
+    const long long r = t / prp;
+    const int j = (int)(t - r * prp);
+    uint64_t* d2 = o + r * per_restart + k + 2 * j;
+    double z1, z2;
+    box_muller(d2[0], d2[1], &z1, &z2);
+    d2[0] = (uint64_t)__double_as_longlong(sigma * z1);
+    d2[1] = (uint64_t)__double_as_longlong(sigma * z2);
+  }
 }
 
 // The mutation draws of every restart as the tangent-plane offsets the

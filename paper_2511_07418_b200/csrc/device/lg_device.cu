@@ -970,13 +970,17 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     for (size_t t = 0; t + 1 < eloff.size(); ++t) max_dom = std::max(max_dom, eloff[t + 1] - eloff[t]);
     const bool large = !proj_brute && max_dom >= kCoopMin;
     int* d_els = dalloc<int>(b_els, (size_t)nel);
-    double* d_elp = large ? nullptr : dalloc<double>(b_elp, 3 * (size_t)nel);
-    double* d_eln = large ? nullptr : dalloc<double>(b_eln, 3 * (size_t)nel);
+    // in a large run only the domains below kCoopMin (plain scan) are
+    // materialised (the arrays keep the element indexing; the big domains'
+    // ranges stay unwritten)
+    const long long big_min = large ? kCoopMin : LLONG_MAX;
+    double* d_elp = dalloc<double>(b_elp, 3 * (size_t)nel);
+    double* d_eln = dalloc<double>(b_eln, 3 * (size_t)nel);
     k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
-                                         d_elp, d_eln);
+                                         d_elp, d_eln, big_min);
     LAUNCH(ctx);
     check_launch();
-    ElemSrc els{d_elp, d_eln, d_els, FS, d_pose, d_aidx};
+    ElemSrc els{d_elp, d_eln, d_els, FS, d_pose, d_aidx, big_min};
     Buf b_keys, b_keys2, b_vals, b_vals2, b_sp, b_cb, b_sb, b_choff, b_suoff, b_cs, b_nch;
     DomIdx dom{};
     if (large) {
@@ -1029,17 +1033,12 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     }
     Buf b_draws, b_oid, b_oobj, b_oan, b_osol, b_bal;
     uint64_t* d_draws = dalloc<uint64_t>(b_draws, (size_t)nA * per_cand);
-    k_copt_draws<<<grid_for(nA, 64), 64, 0, s>>>(nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, d_draws);
-    LAUNCH(ctx);
-    check_launch();
     {
       const int prp = cfg.n_outer * k * cfg.n_inner;  // Box-Muller pairs per restart
-      const long long np = (long long)nA * R * prp;
-      if (np > 0) {
-        k_copt_normals<<<grid_for(np, 256), 256, 0, s>>>(np, prp, k, per_restart, cfg.sigma, d_draws);
-        LAUNCH(ctx);
-        check_launch();
-      }
+      k_copt_draws_warp<<<(nA + kDrawWarps - 1) / kDrawWarps, 32 * kDrawWarps, 0, s>>>(
+          nA, d_aidx, c_lo, B, pass, cfg.seed, per_cand, per_restart, k, prp, cfg.sigma, d_draws);
+      LAUNCH(ctx);
+      check_launch();
     }
     int* d_oid = dalloc<int>(b_oid, (size_t)nA * kMaxK);
     double* d_oobj = dalloc<double>(b_oobj, (size_t)nA);
@@ -2971,7 +2970,7 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
     size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw)
                   : k + 1 <= 4 ? copt2_smem<4>(k, nw) : copt2_smem<kMaxC>(k, nw);
     DomIdx dom{};
-    ElemSrc els{d_elp, d_eln, nullptr, DSamples{}, nullptr, nullptr};
+    ElemSrc els{d_elp, d_eln, nullptr, DSamples{}, nullptr, nullptr, LLONG_MAX};
     kern<<<m, 32 * nw, smem, s>>>(m, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, els, dom,
                                   d_draws, d_oid, d_oobj, d_oan, d_osol, kInf, d_bal);
     check_launch();
