@@ -188,13 +188,12 @@ k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, c
   }
 }
 
-// Stable compaction of the kept grasp records (candidate order preserved),
-// one CTA of 1024 threads: per 1024-record tile each warp ballots its flags,
-// warp totals are scanned in shared memory, and every kept record is copied
-// to its rank.  n_out receives the count.
-__global__ void __launch_bounds__(1024) k_compact_grasps(int n, const lg_grasp* in,
-                                                         const uint8_t* keep, lg_grasp* out,
-                                                         int* n_out) {
+// Stable compaction of the kept grasp records (candidate order preserved):
+// one CTA of 1024 threads ranks the flags (per 1024-flag tile each warp
+// ballots, warp totals are scanned in shared memory), then a warp per kept
+// record copies it with coalesced 8-byte lanes.  n_out receives the count.
+__global__ void __launch_bounds__(1024) k_compact_rank(int n, const uint8_t* keep, int* dest,
+                                                       int* n_out) {
   __shared__ int s_warp[32];
   __shared__ int s_base;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -217,12 +216,24 @@ __global__ void __launch_bounds__(1024) k_compact_grasps(int n, const lg_grasp* 
       s_warp[lane] = incl - c;
     }
     __syncthreads();
-    if (f) out[s_base + s_warp[wid] + __popc(b & ((1u << lane) - 1u))] = in[i];
+    if (i < n) dest[i] = f ? s_base + s_warp[wid] + __popc(b & ((1u << lane) - 1u)) : -1;
     __syncthreads();
     if (threadIdx.x == 1023) s_base += s_warp[31] + __popc(b);
     __syncthreads();
   }
   if (threadIdx.x == 0) *n_out = s_base;
+}
+
+__global__ void k_copy_grasps(int n, const lg_grasp* in, const int* dest, lg_grasp* out) {
+  const int lane = threadIdx.x & 31;
+  const int i = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  if (i >= n) return;
+  const int d = dest[i];
+  if (d < 0) return;  // warp-uniform
+  static_assert(sizeof(lg_grasp) % 8 == 0, "lg_grasp copies as 8-byte words");
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(in + i);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(out + d);
+  for (int w = lane; w < (int)(sizeof(lg_grasp) / 8); w += 32) dst[w] = src[w];
 }
 
 // Funnel counts over the realised candidates (records of the others are

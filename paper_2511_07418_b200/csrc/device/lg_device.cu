@@ -1319,7 +1319,12 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       check_launch();
       lg_grasp* d_sel = dalloc<lg_grasp>(b_sel, (size_t)nA);
       int* d_nsel = dalloc<int>(b_nsel, 1);
-      k_compact_grasps<<<1, 1024, 0, s>>>(nA, d_grasp, d_keep8, d_sel, d_nsel);
+      Buf b_dest;
+      int* d_dest = dalloc<int>(b_dest, (size_t)nA);
+      k_compact_rank<<<1, 1024, 0, s>>>(nA, d_keep8, d_dest, d_nsel);
+      LAUNCH(ctx);
+      check_launch();
+      k_copy_grasps<<<grid_for((long long)nA * 32, 256), 256, 0, s>>>(nA, d_grasp, d_dest, d_sel);
       LAUNCH(ctx);
       check_launch();
       int counts[4];
