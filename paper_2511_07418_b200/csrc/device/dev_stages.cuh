@@ -62,6 +62,16 @@ __device__ __forceinline__ double block_max(double v, double* scratch) {
   return r;
 }
 
+// Samples [n_src][6] (position, normal) -> SoA columns out[a][n], rows
+// idx[t] (all rows when idx is null).
+__global__ void k_soa_gather(int n, const double* rows, const int* idx, double* out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const size_t src = idx ? (size_t)idx[t] : (size_t)t;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) out[(size_t)a * n + t] = rows[6 * src + a];
+  }
+}
+
 // --------------------------------------------------- object sample grid
 // Uniform grid over object-frame samples: cell width w from origin lo, the
 // sample ids sorted by cell (ascending inside a cell), per-cell offsets and

@@ -682,14 +682,16 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
 
   // ---- object samples (raw SoA) and preprocess_object
   tm.start();
-  std::vector<double> col(n_raw);
-  Buf rawc[6];
-  for (int a = 0; a < 6; ++a) {
-    for (int i = 0; i < n_raw; ++i) col[i] = raw[6 * i + a];
-    dupload(rawc[a], col.data(), (size_t)n_raw, s);
-    CK(cudaStreamSynchronize(s));
-  }
-  DSamples RS = make_samples(rawc, n_raw);
+  // one upload of the [n][6] rows, columns split on the device
+  Buf raw_rows, raw_cols;
+  const double* d_rows = dupload(raw_rows, raw, 6 * (size_t)n_raw, s);
+  double* d_rawc = dalloc<double>(raw_cols, 6 * (size_t)std::max(n_raw, 1));
+  k_soa_gather<<<grid_for(n_raw, 256), 256, 0, s>>>(n_raw, d_rows, nullptr, d_rawc);
+  LAUNCH(ctx);
+  check_launch();
+  DSamples RS;
+  RS.n = n_raw;
+  for (int a = 0; a < 6; ++a) RS.x[a] = d_rawc + (size_t)a * n_raw;
   // LG_TIMING=1: host-clock marks after stream syncs, printed at the end
   const bool timing = std::getenv("LG_TIMING") != nullptr;
   std::vector<std::pair<const char*, double>> marks;
@@ -715,13 +717,15 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   const int ns = (int)kept.size();
   if (ns == 0) throw std::runtime_error("run_batch: preprocessing stripped every object sample");
   out.profile.field_samples = ns;
-  Buf fsc[6];
-  for (int a = 0; a < 6; ++a) {
-    for (int j = 0; j < ns; ++j) col[j] = raw[6 * kept[j] + a];
-    dupload(fsc[a], col.data(), (size_t)ns, s);
-    CK(cudaStreamSynchronize(s));
-  }
-  DSamples FS = make_samples(fsc, ns);
+  Buf kept_b, fs_cols;
+  const int* d_kept = dupload(kept_b, kept.data(), kept.size(), s);
+  double* d_fsc = dalloc<double>(fs_cols, 6 * (size_t)ns);
+  k_soa_gather<<<grid_for(ns, 256), 256, 0, s>>>(ns, d_rows, d_kept, d_fsc);
+  LAUNCH(ctx);
+  check_launch();
+  DSamples FS;
+  FS.n = ns;
+  for (int a = 0; a < 6; ++a) FS.x[a] = d_fsc + (size_t)a * ns;
 
   // ---- groups, statics (collect_static_surface)
   int G = 0;
