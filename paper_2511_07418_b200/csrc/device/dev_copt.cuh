@@ -549,7 +549,10 @@ __device__ int project_coop(const DomIdx& D, long long seg, long long base, int 
 
 // Block per candidate, warp per restart, lanes over the n_inner mutations.
 // NC = compile-time bound on k + statics (sizes the shared-memory layout).
-template <int NC, int MINB>
+// LARGE: the launch has domains of at least kCoopMin elements (cooperative
+// search, elements recomputed from sample ids); the plain instance keeps the
+// materialised-only code, whose smaller body stays in the instruction cache.
+template <int NC, int MINB, bool LARGE>
 __global__ void __launch_bounds__(128, MINB)
 k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, const double* st_p,
                const double* st_n, const long long* el_off, ElemSrc el,
@@ -589,7 +592,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
       for (int q = 0; q < k; ++q) ids[q] = (int)(D[q] % (uint64_t)cnt[q]);
       if (lane < k) {
         long long e = off[lane] + ids[lane];
-        const bool bg = el.big(cnt[lane]);
+        const bool bg = LARGE && el.big(cnt[lane]);
         slot_make(sp + kSlot * lane, el.pos(e, a, bg), neg(el.nrm(e, a, bg)));
       } else if (lane == k && s) {
         slot_make(sp + kSlot * k, v3_load(st_p + 3 * i), v3_load(st_n + 3 * i));
@@ -648,7 +651,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             const int ne = (int)cnt[q];
             double bd;
             int bi;
-            if (dom.sx && ne >= kCoopMin) {
+            if (LARGE && ne >= kCoopMin) {
               unsigned long long evals = 0;
               bi = project_coop(dom, (long long)a * k + q, off[q], ne, cp, act, ids[q], cur_p, lane,
                                 evals);
@@ -717,7 +720,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             if (act) {
               cand = bi;
               const long long eg = off[q] + bi;
-              const bool bg = el.big(cnt[q]);
+              const bool bg = LARGE && el.big(cnt[q]);
               slot_make(tslot, el.pos(eg, a, bg), neg(el.nrm(eg, a, bg)));
               PV tw = w;
               tw.tq = q;
@@ -760,7 +763,7 @@ k_contact_opt2(int nA, const int* alive_idx, CoptCfg cfg, const int* n_static, c
             ids[q] = best_id;
             if (lane == 0) {
               long long e = off[q] + best_id;
-              const bool bg = el.big(cnt[q]);
+              const bool bg = LARGE && el.big(cnt[q]);
               slot_make(sp + kSlot * q, el.pos(e, a, bg), neg(el.nrm(e, a, bg)));
             }
             if (lane < 3 * NC) inc[lane] = win[lane];

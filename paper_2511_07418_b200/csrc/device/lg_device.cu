@@ -1066,30 +1066,35 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       return (e && std::atoi(e) == 5) ? 5 : 4;
     }();
     if (first_on_device(2)) {
-      CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      CK(cudaFuncSetAttribute(k_contact_opt2<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      for (auto kern : {k_contact_opt2<3, 4, false>, k_contact_opt2<3, 5, false>,
+                        k_contact_opt2<4, 4, false>, k_contact_opt2<kMaxC, 4, false>,
+                        k_contact_opt2<3, 4, true>, k_contact_opt2<4, 4, true>,
+                        k_contact_opt2<kMaxC, 4, true>})
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       // shared-memory carve-out (percent): less shared memory leaves more L1
       // for the domain scans, at the cost of resident CTAs
       const char* cv = std::getenv("LG_COPT_CARVE");
       if (cv) {
         int pct = std::atoi(cv);
-        CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        CK(cudaFuncSetAttribute(k_contact_opt2<3, 5>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        CK(cudaFuncSetAttribute(k_contact_opt2<3, 4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        CK(cudaFuncSetAttribute(k_contact_opt2<3, 5, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
       }
     }
     tk.start();
     // k contacts + at most one static
     // (the per-lane shared records scale with NC: NC = 4 fits three CTAs per
     // SM where NC = 6 fits two)
-    auto co_kern = k + 1 <= 3   ? (co_minb == 5 ? k_contact_opt2<3, 5> : k_contact_opt2<3, 4>)
-                   : k + 1 <= 4 ? k_contact_opt2<4, 4>
-                                : k_contact_opt2<kMaxC, 4>;
+    const bool lg = dom.sx != nullptr;
+    auto co_kern = k + 1 <= 3
+                       ? (lg ? k_contact_opt2<3, 4, true>
+                             : (co_minb == 5 ? k_contact_opt2<3, 5, false> : k_contact_opt2<3, 4, false>))
+                   : k + 1 <= 4 ? (lg ? k_contact_opt2<4, 4, true> : k_contact_opt2<4, 4, false>)
+                                : (lg ? k_contact_opt2<kMaxC, 4, true> : k_contact_opt2<kMaxC, 4, false>);
     size_t co_smem = k + 1 <= 3   ? copt2_smem<3>(k, nw)
                      : k + 1 <= 4 ? copt2_smem<4>(k, nw)
                                   : copt2_smem<kMaxC>(k, nw);
-    co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, els, dom, d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
+    co_kern<<<nA, 32 * nw, co_smem, s>>>(nA, d_aidx, co, d_nst, d_stp, d_stn, d_eloff, els, dom,
+                                         d_draws, d_oid, d_oobj, d_oan, d_osol, cfg.eps_stable,
                                          d_bal);
     LAUNCH(ctx);
     check_launch();
@@ -2971,11 +2976,11 @@ int lg_optimize_contacts_batch(lg_ctx* ctx, int m, int k, const long long* dom_o
     co.per_restart = per_restart;
     co.per_cand = per_cand;
     const int nw = std::min(R, 4);
-    CK(cudaFuncSetAttribute(k_contact_opt2<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_contact_opt2<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    auto kern = k + 1 <= 3 ? k_contact_opt2<3, 4>
-                : k + 1 <= 4 ? k_contact_opt2<4, 4> : k_contact_opt2<kMaxC, 4>;
+    CK(cudaFuncSetAttribute(k_contact_opt2<3, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_contact_opt2<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_contact_opt2<kMaxC, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    auto kern = k + 1 <= 3 ? k_contact_opt2<3, 4, false>
+                : k + 1 <= 4 ? k_contact_opt2<4, 4, false> : k_contact_opt2<kMaxC, 4, false>;
     size_t smem = k + 1 <= 3 ? copt2_smem<3>(k, nw)
                   : k + 1 <= 4 ? copt2_smem<4>(k, nw) : copt2_smem<kMaxC>(k, nw);
     DomIdx dom{};
