@@ -55,13 +55,21 @@ constexpr size_t kCacheCap = size_t(64) << 30;  // of 180 GB HBM
 
 void drop_cache(cudaStream_t s);
 
+// cudaMalloc calls and their host time (LG_TIMING reports them per call)
+thread_local long long g_malloc_calls = 0;
+thread_local double g_malloc_ms = 0.0;
+
 void* cached_alloc(size_t bytes, cudaStream_t s) {
   {
     std::lock_guard<std::mutex> lk(g_streams_mu);
     if (g_live_streams.count(s)) {
       auto& c = g_cache[s];
+      // best fit within 1/8: a request does not take a much larger block
+      // that a later, larger request of the same call needs (the pass makes
+      // the same requests every call, so the cache then settles after one
+      // call; each cudaMalloc costs milliseconds here)
       auto it = c.lower_bound(bytes);
-      if (it != c.end() && it->first <= 2 * bytes + 4096) {
+      if (it != c.end() && it->first <= bytes + bytes / 8 + 4096) {
         void* p = it->second;
         g_cache_bytes[s] -= it->first;
         c.erase(it);
@@ -70,7 +78,10 @@ void* cached_alloc(size_t bytes, cudaStream_t s) {
     }
   }
   void* p = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMalloc(&p, bytes);
+  g_malloc_calls += 1;
+  g_malloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (e == cudaErrorMemoryAllocation) {
     (void)cudaGetLastError();
     CK(cudaStreamSynchronize(s));
@@ -1254,6 +1265,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                                  d_bused, d_qall);
     LAUNCH(ctx);
     check_launch();
+    mark("post_unused_draws");
     {
       std::vector<int> cand(nU);
       for (long long u = 0; u < nU; ++u) cand[u] = alive_idx[real_list[u / UA]];
@@ -1291,6 +1303,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
                                                  d_valid, d_drop);
     LAUNCH(ctx);
     check_launch();
+    mark("post_finalize");
     std::vector<int> uatt;
     std::vector<double> fq_h;
     std::vector<lg_grasp> h_grasp;
@@ -1378,6 +1391,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
   mark("passes_done");
   if (timing)
     for (auto& m : marks) std::fprintf(stderr, "[lg timing] %-20s %9.3f ms\n", m.first, 1e3 * m.second);
+    std::fprintf(stderr, "[lg timing] cudaMalloc calls so far %lld, %.3f ms\n", g_malloc_calls, g_malloc_ms);
   out.profile.valid = (long long)out.grasps.size();
   out.profile.device_seconds = tdev.stop() + out.profile.field_build;
   {
