@@ -34,7 +34,9 @@ struct CollWarpSmem {
   int nobj, viol;
 };
 
-template <int MINB>
+// GRID: the object-sample grid path is compiled in (objects of at least
+// kCollGridMin samples); the plain instance keeps the smaller sweep-only body.
+template <int MINB, bool GRID>
 __global__ void __launch_bounds__(32 * kCollWarps, MINB)
 k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, const double* q_all,
              const double* pose, const double* obj_aabb, int clean_only, uint8_t* clean_out,
@@ -98,13 +100,13 @@ k_collision3(int n_calls, CollCfg C, const int* call_cand, const int* call_on, c
   // pose whose R is not orthonormal to 1e-9 takes the full sweep, and so do
   // objects with few samples (a part's rows hold too few samples to keep
   // the lanes busy: the sweep, one world point per sample, is faster).
-  bool use_grid = C.grid.ok && nobj > 0 && C.raw.n >= kCollGridMin;
+  bool use_grid = GRID && C.grid.ok && nobj > 0 && C.raw.n >= kCollGridMin;
   if (use_grid) {
     const M3 RtR = mul(transpose(x.R), x.R);
     for (int a = 0; a < 9; ++a)
       use_grid = use_grid && dabs(RtR.m[a] - ((a % 4) == 0 ? 1.0 : 0.0)) <= 1e-9;
   }
-  if (use_grid) {
+  if (GRID && use_grid) {
     const DGrid& g = C.grid;
     for (int o = 0; o < nobj; ++o) {
       if (clean_only && *(volatile int*)&W.viol) break;

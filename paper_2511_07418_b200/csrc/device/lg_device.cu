@@ -411,13 +411,14 @@ bool first_on_device(int tag) {
 // k_collision3 instance: LG_COLL_MINB = 4 (128 registers), 5 (96) or 3 (160)
 using CollKern = void (*)(int, CollCfg, const int*, const int*, const double*, const double*,
                           const double*, int, uint8_t*, double*);
-CollKern coll_kernel() {
+CollKern coll_kernel(const CollCfg& c) {
   static const int minb = [] {
     const char* e = std::getenv("LG_COLL_MINB");
     int v = e ? std::atoi(e) : 4;
     return (v == 3 || v == 5) ? v : 4;
   }();
-  return minb == 5 ? k_collision3<5> : (minb == 3 ? k_collision3<3> : k_collision3<4>);
+  if (c.grid.ok && c.raw.n >= kCollGridMin) return k_collision3<4, true>;
+  return minb == 5 ? k_collision3<5, false> : (minb == 3 ? k_collision3<3, false> : k_collision3<4, false>);
 }
 
 void launch_realize_warp(cudaStream_t s, int n, int k, const int* kk, const IkCfg& P, int rounds,
@@ -1195,7 +1196,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nP);
       CK(cudaMemsetAsync(d_clean, 0, nP, s));
-      coll_kernel()<<<((int)nP + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
+      coll_kernel(cc)<<<((int)nP + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
           (int)nP, cc, d_cand, d_on, d_qt, d_pose, d_aabb, 1,
                                             d_clean, nullptr);
       LAUNCH(ctx);
@@ -1272,7 +1273,7 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
       int* d_cand = dupload(b_cand, cand.data(), cand.size(), s);
       uint8_t* d_clean = dalloc<uint8_t>(b_clean, (size_t)nU);
       out.profile.collision_calls += nU;
-      coll_kernel()<<<((int)nU + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
+      coll_kernel(cc)<<<((int)nU + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(
           (int)nU, cc, d_cand, nullptr, d_qall, d_pose, d_aabb, 1,
                                             d_clean, nullptr);
       LAUNCH(ctx);
@@ -1860,7 +1861,7 @@ int lg_collision_batch(lg_ctx* ctx, const lg_hand_desc* hand, int m, const doubl
     cc.raw = S;
     cc.part_link = ctx->h_part_link.as<int>();
     cc.grid = build_grid(ctx, S, samples, n, 0.005, gb, s);
-    coll_kernel()<<<(m + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(m, cc, d_i, nullptr, d_q,
+    coll_kernel(cc)<<<(m + kCollWarps - 1) / kCollWarps, 32 * kCollWarps, 0, s>>>(m, cc, d_i, nullptr, d_q,
                                                                              d_p, d_b, 0, d_c, d_m);
     check_launch();
     CK(cudaMemcpyAsync(clean, d_c, (size_t)m, cudaMemcpyDeviceToHost, s));
