@@ -448,31 +448,51 @@ __global__ void k_finalize_warp(int nT, const int* act, const int* alive_idx, Fi
     return;
   }
   double worst = warp_max_d(lane < k ? d : 0.0);
-  for (int s = 0; s < k; ++s) {
-    V3 ps = v3(__shfl_sync(kFull, pw.x, s), __shfl_sync(kFull, pw.y, s), __shfl_sync(kFull, pw.z, s));
-    double bd = kInf;
-    int bi = 0x7fffffff;
-    for (int j = lane; j < fs.n; j += 32) {
-      double d2 = sqnorm(sub(xf_apply(x, fs.p(j)), ps));
-      if (d2 < bd) {
-        bd = d2;
-        bi = j;
+  // nearest preprocessed sample of every contact in one sweep: each sample
+  // is moved to world once and compared with all k contacts (per contact
+  // the lane's comparisons stay in ascending sample order)
+  V3 ps[kMaxK];
+  double bd[kMaxK];
+  int bi[kMaxK];
+#pragma unroll
+  for (int c = 0; c < kMaxK; ++c) {
+    const int src = c < k ? c : 0;
+    ps[c] = v3(__shfl_sync(kFull, pw.x, src), __shfl_sync(kFull, pw.y, src),
+               __shfl_sync(kFull, pw.z, src));
+    bd[c] = kInf;
+    bi[c] = 0x7fffffff;
+  }
+  for (int j = lane; j < fs.n; j += 32) {
+    const V3 w = xf_apply(x, fs.p(j));
+#pragma unroll
+    for (int c = 0; c < kMaxK; ++c) {
+      if (c >= k) break;
+      const double d2 = sqnorm(sub(w, ps[c]));
+      if (d2 < bd[c]) {
+        bd[c] = d2;
+        bi[c] = j;
       }
     }
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxK; ++c) {
+    if (c >= k) break;
+    double b = bd[c];
+    int ix = bi[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      double od = __shfl_xor_sync(kFull, bd, o);
-      int oi = __shfl_xor_sync(kFull, bi, o);
-      if (od < bd || (od == bd && oi < bi)) {
-        bd = od;
-        bi = oi;
+      double od = __shfl_xor_sync(kFull, b, o);
+      int oi = __shfl_xor_sync(kFull, ix, o);
+      if (od < b || (od == b && oi < ix)) {
+        b = od;
+        ix = oi;
       }
     }
-    int nearest = bi == 0x7fffffff ? 0 : bi;
+    int nearest = ix == 0x7fffffff ? 0 : ix;
     if (lane == 0) {
-      v3_store(g.contact_p[s], ps);
-      v3_store(g.contact_n[s], neg(xf_rotate(x, fs.nrm(nearest))));
-      g.contact_link[s] = best_link[a * kMaxK + s];
+      v3_store(g.contact_p[c], ps[c]);
+      v3_store(g.contact_n[c], neg(xf_rotate(x, fs.nrm(nearest))));
+      g.contact_link[c] = best_link[a * kMaxK + c];
     }
   }
   int nc = k;
