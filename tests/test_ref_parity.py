@@ -126,6 +126,10 @@ GPU_CASES = CPU_CASES + [
     # configs[2] (LEAP-class on tools) at leap.cfg as written
     ("leap.cfg", "leap_like.urdf", "mug.obj", 192, ""),
     ("leap.cfg", "leap_like.urdf", "drill.obj", 256, ""),
+    # k = 3 and k = 4 on small domains: the NC = 4 and NC = 6 instances of
+    # the plain contact search
+    ("allegro.cfg", "allegro_like.urdf", "box_050.obj", 160, "k_contacts = 3"),
+    ("leap.cfg", "leap_like.urdf", "mug.obj", 128, "k_contacts = 4\nstatic_contact_prob = 0.5"),
     # the largest codebook the config accepts in shared memory for the query
     # kernels (C = 2048: 48 KiB of codebook plus the kernels' static arrays)
     ("four_finger.cfg", "four_finger.urdf", "sphere_r030.obj", 96,
