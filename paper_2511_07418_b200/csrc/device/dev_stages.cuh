@@ -588,33 +588,32 @@ struct ElemSrc {
 };
 
 // ------------------------------------------------- chosen domain elements
-// Elements of domain (a, slot) in sample order: block per (a, slot), block
-// scan over the mask row.  Writes sample id, position and normal (SoA).
+// Elements of domain (a, slot) in sample order.  Writes sample id, position
+// and normal.
 __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* chosen,
                               const uint32_t* mask, DSamples fs, const double* pose,
                               const long long* el_off, int* el_s, double* el_p, double* el_n,
                               long long big_min) {
-  typedef cub::BlockScan<int, 256> Scan;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_base;
-  int a = blockIdx.x / k, slot = blockIdx.x % k;
-  if (a >= nA) return;
-  int i = alive_idx[a];
-  int g = chosen[i * kMaxK + slot];
+  // a warp per domain: ballots over 32 samples at a time give each member
+  // its rank, no block-wide scans
+  const int lane = threadIdx.x & 31;
+  const long long seg = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (seg >= (long long)nA * k) return;  // warp-uniform
+  const int a = (int)(seg / k), slot = (int)(seg % k);
+  const int i = alive_idx[a];
+  const int g = chosen[i * kMaxK + slot];
   const uint32_t* m = mask + (size_t)i * fs.n;
-  Xf x = load_xf(pose + 12 * i);
-  long long off = el_off[a * k + slot];
+  const Xf x = load_xf(pose + 12 * i);
+  const long long off = el_off[seg];
   // large domains keep the sample ids only (ElemSrc)
-  const bool mat = el_off[a * k + slot + 1] - off < big_min;
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  for (int base = 0; base < fs.n; base += 256) {
-    int j = base + threadIdx.x;
-    int flag = (j < fs.n && ((m[j] >> g) & 1u)) ? 1 : 0;
-    int pos, total;
-    Scan(tmp).ExclusiveSum(flag, pos, total);
+  const bool mat = el_off[seg + 1] - off < big_min;
+  long long run = off;
+  for (int base = 0; base < fs.n; base += 32) {
+    const int j = base + lane;
+    const bool flag = j < fs.n && ((m[j] >> g) & 1u);
+    const unsigned b = __ballot_sync(0xffffffffu, flag);
     if (flag) {
-      long long e = off + s_base + pos;
+      const long long e = run + __popc(b & ((1u << lane) - 1u));
       el_s[e] = j;
       if (mat) {
         V3 p = xf_apply(x, fs.p(j));
@@ -627,9 +626,7 @@ __global__ void k_domain_fill(int nA, int k, const int* alive_idx, const int* ch
         el_n[3 * e + 2] = n.z;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_base += total;
-    __syncthreads();
+    run += __popc(b);
   }
 }
 

@@ -992,8 +992,8 @@ void run_batch_device(lg_ctx* ctx, const lg_hand_desc& hd, const lg_patches_desc
     const long long big_min = large ? kCoopMin : LLONG_MAX;
     double* d_elp = dalloc<double>(b_elp, 3 * (size_t)nel);
     double* d_eln = dalloc<double>(b_eln, 3 * (size_t)nel);
-    k_domain_fill<<<nA * k, 256, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff, d_els,
-                                         d_elp, d_eln, big_min);
+    k_domain_fill<<<(nA * k + 3) / 4, 128, 0, s>>>(nA, k, d_aidx, d_chosen, d_mask, FS, d_pose, d_eloff,
+                                                   d_els, d_elp, d_eln, big_min);
     LAUNCH(ctx);
     check_launch();
     ElemSrc els{d_elp, d_eln, d_els, FS, d_pose, d_aidx, big_min};
