@@ -2270,13 +2270,15 @@ int lg_run_batch(lg_ctx* ctx, const lg_hand_desc* hand, const lg_patches_desc* p
 }
 
 int lg_result_profile(const lg_result* r, lg_profile* out) {
-  *out = r->r.profile;
-  return LG_OK;
+  return lgc::guard([&] {
+    if (!r || !out) throw std::invalid_argument("lg_result_profile: null argument");
+    *out = r->r.profile;
+  });
 }
-long long lg_result_num_grasps(const lg_result* r) { return (long long)r->r.grasps.size(); }
-const lg_grasp* lg_result_grasps(const lg_result* r) { return r->r.grasps.data(); }
-long long lg_result_num_traces(const lg_result* r) { return (long long)r->r.traces.size(); }
-const lg_trace* lg_result_traces(const lg_result* r) { return r->r.traces.data(); }
+long long lg_result_num_grasps(const lg_result* r) { return r ? (long long)r->r.grasps.size() : 0; }
+const lg_grasp* lg_result_grasps(const lg_result* r) { return r ? r->r.grasps.data() : nullptr; }
+long long lg_result_num_traces(const lg_result* r) { return r ? (long long)r->r.traces.size() : 0; }
+const lg_trace* lg_result_traces(const lg_result* r) { return r ? r->r.traces.data() : nullptr; }
 void lg_result_destroy(lg_result* r) { delete r; }
 
 }  // extern "C"

@@ -55,6 +55,23 @@ def test_no_cpu_fallback_without_device():
         lg.Context(0)
 
 
+def test_result_accessors_reject_null_handles():
+    """The result accessors check their arguments (no device needed)."""
+    import ctypes as C
+    from paper_2511_07418_b200 import lgabi as A
+    L = C.CDLL(lg.api.LIB_PATH)
+    L.lg_result_profile.restype = C.c_int
+    L.lg_result_profile.argtypes = [C.c_void_p, C.c_void_p]
+    prof = A.Profile()
+    assert L.lg_result_profile(None, C.byref(prof)) == -1  # LG_ERR_INVALID_ARGUMENT
+    L.lg_result_num_grasps.restype = C.c_longlong
+    L.lg_result_num_grasps.argtypes = [C.c_void_p]
+    assert L.lg_result_num_grasps(None) == 0
+    L.lg_result_grasps.restype = C.c_void_p
+    L.lg_result_grasps.argtypes = [C.c_void_p]
+    assert L.lg_result_grasps(None) is None
+
+
 def test_four_finger_structure(four_finger):  # test_hand.cpp:31-105
     d = four_finger.desc
     assert (d.n_links, d.dof, d.n_parts) == (13, 12, 13)
