@@ -368,15 +368,18 @@ def run_b200(args):
                 kernel_share_of_step=secs / prof["device_seconds"],
                 note="SIMT FP64 kernel (no HBM- or tensor-bound stage); algorithmic FLOPs from "
                      "device work counters x SURVEY 8(d) per-unit model")
+    # the same config keys as the reference arm; measured workload sizes
+    # go beside it
     config = config_keys(args.workload, p, world)
-    config.update(object_samples=int(prof["object_samples"]), patches=int(prof["patches"]),
-                  forward_seconds=float(dev_s.mean()))
+    workload_stats = dict(object_samples=int(prof["object_samples"]), patches=int(prof["patches"]),
+                          forward_seconds=float(dev_s.mean()))
     line = dict(
         metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
         warmup=args.warmup, ms_per_step=float(dev_s.mean() * 1e3), higher_is_better=True,
         scaling="weak", vs_baseline=None, dtype="f64",
         data="synthetic assets (tools/make_assets.py; BASELINE configs[1])",
         config=config,
+        workload_stats=workload_stats,
         e2e=dict(value=e2e_v, unit=UNIT, h2d_bytes_per_step=int(h2d_t.mean()),
                  d2h_bytes_per_step=int(d2h_t.mean()), ms_per_step=float(e2e_ms.mean()),
                  includes="H2D inputs, the pass, D2H of the kept grasps" +
