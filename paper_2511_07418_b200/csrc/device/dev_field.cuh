@@ -533,9 +533,19 @@ __device__ __forceinline__ uint32_t sample_mask_cm(const DField& f, const double
   int2 rg = cell >= 0 ? f.dl_rng[cell] : make_int2(0, -1);
   uint32_t bits = 0u;
   if (rg.y >= 0) {
-    for (int t = 0; t < rg.y; ++t) {
-      int code = f.dl_codes[rg.x + t];
-      if (-dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta) bits |= row[code];
+    // four listed codes at a time: the tests, then the passing codes' mask
+    // words as independent loads, then the OR (an order-free reduction)
+    for (int t0 = 0; t0 < rg.y; t0 += 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int code = t0 + u < rg.y ? f.dl_codes[rg.x + t0 + u] : 0;
+        const bool pass = t0 + u < rg.y &&
+                          -dot(v3(cb[3 * code], cb[3 * code + 1], cb[3 * code + 2]), n) >= theta;
+        w[u] = pass ? row[code] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bits |= w[u];
     }
   } else {
     for (int code = 0; code < f.C; ++code)
